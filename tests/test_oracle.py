@@ -1,0 +1,273 @@
+"""Pins for the CPU oracle (oracle/) against what the paper and mathematics fix.
+
+Each test names the passage or property it checks. Chosen so that a
+plausible slip in the oracle (dropped gate factor, wrong softmax sign,
+transposed operand, unstable grouping, wrong shard slice, missing ReLU,
+wrong tie-break) fails at least one of them.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+rng = np.random.default_rng(12345)
+
+
+def _rand_layer(T, h, d_ff, E, seed=0):
+    r = np.random.default_rng(seed)
+    x = r.standard_normal((T, h))
+    w_r = r.standard_normal((h, E)) / math.sqrt(h)
+    w_i = r.standard_normal((E, h, d_ff)) / math.sqrt(h)
+    w_o = r.standard_normal((E, d_ff, h)) / math.sqrt(d_ff)
+    return x, w_r, w_i, w_o
+
+
+# ----------------------------------------------------------------- Step 1 router
+def test_router_worked_example(golden):
+    g = golden("router_worked_example.json")
+    rt = O.route(np.array(g["x"]), np.array(g["w_r"]))
+    assert rt.expert.tolist() == g["expert"]
+    assert rt.gate[0] == pytest.approx(g["gate"][0], abs=1e-15)
+    # independent closed form: logistic(5)
+    assert rt.gate[0] == pytest.approx(1.0 / (1.0 + math.exp(-5.0)), abs=1e-15)
+
+
+def test_router_all_zero_gate_goes_to_expert0_with_gate_1_over_E():
+    # tie everywhere -> lowest index, softmax uniform
+    E = 7
+    rt = O.route(rng.standard_normal((11, 5)), np.zeros((5, E)))
+    assert (rt.expert == 0).all()
+    np.testing.assert_allclose(rt.gate, 1.0 / E, rtol=0, atol=1e-15)
+
+
+def test_router_single_expert_gate_is_one():
+    # SPEC.md:132
+    rt = O.route(rng.standard_normal((9, 4)), rng.standard_normal((4, 1)))
+    assert (rt.expert == 0).all()
+    np.testing.assert_array_equal(rt.gate, 1.0)
+
+
+def test_router_tie_break_lowest_index():
+    # R4: columns 1 and 3 identical and maximal -> expert 1
+    w_r = np.array([[0.0, 2.0, -1.0, 2.0], [0.0, 1.0, 0.5, 1.0]])
+    x = np.array([[1.0, 1.0], [3.0, -1.0]])
+    rt = O.route(x, w_r)
+    assert rt.expert.tolist() == [1, 1]
+
+
+def test_router_argmax_invariant_to_positive_scaling():
+    # SPEC.md:153 (softmax argmax invariance)
+    x, w_r, _, _ = _rand_layer(200, 8, 4, 6, seed=3)
+    a = O.route(x, w_r).expert
+    b = O.route(x, 3.7 * w_r).expert
+    np.testing.assert_array_equal(a, b)
+
+
+def test_router_gate_is_softmax_probability_of_chosen_expert():
+    # independent: softmax by explicit normalisation, not the oracle's formula
+    x, w_r, _, _ = _rand_layer(50, 6, 4, 5, seed=4)
+    rt = O.route(x, w_r)
+    for t in range(50):
+        l = [sum(x[t, k] * w_r[k, e] for k in range(6)) for e in range(5)]
+        z = [math.exp(v) for v in l]
+        p = [v / sum(z) for v in z]
+        best = max(range(5), key=lambda e: (l[e], -e))
+        assert rt.expert[t] == best
+        assert rt.gate[t] == pytest.approx(p[best], rel=1e-12)
+    forced = [(t * 3) % 5 for t in range(50)]
+    rf = O.route(x, w_r, forced)
+    for t in range(50):
+        l = [sum(x[t, k] * w_r[k, e] for k in range(6)) for e in range(5)]
+        z = [math.exp(v) for v in l]
+        assert rf.gate[t] == pytest.approx(z[forced[t]] / sum(z), rel=1e-12)
+
+
+def test_router_shape_and_bounds_errors():
+    with pytest.raises(ValueError):
+        O.route(np.zeros((3, 4)), np.zeros((5, 2)))
+    with pytest.raises(IndexError):
+        O.route(np.zeros((2, 4)), np.zeros((4, 2)), forced=[0, 2])
+
+
+# ----------------------------------------------------------------- Step 2 grouping
+def test_grouping_worked_example(golden):
+    g = golden("grouping_example.json")
+    counts, offsets, perm = O.group_per_expert(g["m_expert"], g["E"])
+    assert counts.tolist() == g["counts"]
+    assert perm.tolist() == g["perm"]
+    assert offsets.tolist() == [0, 3, 3, 4, 4]
+
+
+def test_grouping_is_stable_permutation_and_inverts():
+    e = rng.integers(0, 9, size=1000)
+    counts, offsets, perm = O.group_per_expert(e, 9)
+    assert counts.sum() == 1000
+    assert sorted(perm.tolist()) == list(range(1000))           # bijection
+    for k in range(9):
+        seg = perm[offsets[k]:offsets[k + 1]]
+        assert (e[seg] == k).all()
+        assert (np.diff(seg) > 0).all()                          # stable: ascending token id
+    x = rng.standard_normal((1000, 3))
+    grouped = x[perm]
+    back = np.empty_like(grouped)
+    back[perm] = grouped                                         # ungroup(group(x)) == x
+    np.testing.assert_array_equal(back, x)
+
+
+def test_grouping_bounds_error():
+    with pytest.raises(IndexError):
+        O.group_per_expert([0, 4], 4)
+
+
+# ----------------------------------------------------------------- expert FFN
+def test_identity_expert(golden):
+    g = golden("identity_expert.json")
+    y = O.expert_ffn(np.array(g["x"]), np.array(g["w_i"]), np.array(g["w_o"]))
+    np.testing.assert_array_equal(y, np.array(g["y"]))
+    np.testing.assert_array_equal(O.expert_ffn(np.zeros((3, 2)), np.eye(2), np.eye(2)), 0.0)
+
+
+def test_expert_ffn_matches_explicit_loops_and_uses_relu():
+    x, _, w_i, w_o = _rand_layer(5, 4, 6, 1, seed=5)
+    y = O.expert_ffn(x, w_i[0], w_o[0])
+    for t in range(5):
+        hid = [max(0.0, sum(x[t, k] * w_i[0, k, j] for k in range(4))) for j in range(6)]
+        for c in range(4):
+            assert y[t, c] == pytest.approx(sum(hid[j] * w_o[0, j, c] for j in range(6)), abs=1e-12)
+    # without the ReLU the answer differs (guards a dropped activation)
+    assert not np.allclose(y, x @ w_i[0] @ w_o[0])
+
+
+# ----------------------------------------------------------------- sharding plan
+def test_shard_plan_examples(golden):
+    for case in golden("shard_plan_examples.json")["cases"]:
+        if "error" in case:
+            with pytest.raises(ValueError):
+                O.shard_plan(case["d_ff"], case["G"])
+        else:
+            assert [list(r) for r in O.shard_plan(case["d_ff"], case["G"])] == case["ranges"]
+
+
+def test_extract_shard_reassembles_exactly():
+    _, _, w_i, w_o = _rand_layer(1, 6, 8, 3, seed=6)
+    for G in (1, 2, 4, 8):
+        parts = [O.extract_shard(w_i, w_o, g, G) for g in range(G)]
+        np.testing.assert_array_equal(np.concatenate([p[0] for p in parts], axis=2), w_i)
+        np.testing.assert_array_equal(np.concatenate([p[1] for p in parts], axis=1), w_o)
+    # Fig. 2b: GPU 1 of 2 holds the second half of W_i's columns / W_o's rows
+    wi1, wo1 = O.extract_shard(w_i, w_o, 1, 2)
+    np.testing.assert_array_equal(wi1, w_i[:, :, 4:8])
+    np.testing.assert_array_equal(wo1, w_o[:, 4:8, :])
+    with pytest.raises(IndexError):
+        O.extract_shard(w_i, w_o, 2, 2)
+
+
+def test_byte_and_entry_counts(golden):
+    g = golden("byte_counts.json")
+    s = g["scatter"]
+    nbytes = O.scatter_payload_bytes(s["b"], s["s"], s["h"], s["bytes_per_elt"])
+    assert nbytes == s["payload_bytes"]
+    assert round(nbytes / 2**20) == s["payload_mib_approx"]
+    for c in g["transfer"]:
+        assert O.transfer_entries(c["c"], c["h"], c["G"], c["split"]) == c["entries"]
+    for G in (1, 2, 4, 8):          # column split = G x row split
+        assert O.transfer_entries(16, 8, G, "column") == G * O.transfer_entries(16, 8, G, "row")
+    st = g["storage"]
+    assert O.shard_storage_entries(st["h"], st["d_ff"], st["G"]) == st["entries"]
+    assert O.shard_storage_entries(st["h"], st["d_ff"], st["G"]) * st["G"] == st["h"] * st["d_ff"]
+    t = g["time"]
+    ms = t["mib"] * 2**20 / (t["gib_per_s"] * 2**30) * 1e3
+    assert abs(ms - t["ms_approx"]) < 0.01
+
+
+# ----------------------------------------------------------------- whole layer
+@pytest.mark.parametrize("T,h,d_ff,E", [(1, 3, 4, 1), (17, 8, 12, 3), (40, 16, 64, 8), (64, 12, 32, 5)])
+def test_layer_matches_brute_force(T, h, d_ff, E):
+    x, w_r, w_i, w_o = _rand_layer(T, h, d_ff, E, seed=T + E)
+    y = O.moe_layer(x, w_r, w_i, w_o)
+    yb = O.brute_force_layer(x, w_r, w_i, w_o)
+    np.testing.assert_allclose(y, yb, rtol=0, atol=1e-12 * max(1.0, np.abs(yb).max()))
+    forced = [(3 * t + 1) % E for t in range(T)]
+    yf = O.moe_layer(x, w_r, w_i, w_o, forced=forced)
+    ybf = O.brute_force_layer(x, w_r, w_i, w_o, forced=forced)
+    np.testing.assert_allclose(yf, ybf, rtol=0, atol=1e-12 * max(1.0, np.abs(ybf).max()))
+
+
+def test_single_expert_reduces_to_dense_t5_ffn():
+    # E=1 -> gate 1, the layer is relu(x W_i) W_o (textbook T5 v1.0 FFN)
+    x, w_r, w_i, w_o = _rand_layer(30, 8, 16, 1, seed=9)
+    y = O.moe_layer(x, w_r, w_i, w_o)
+    dense = O.brute_force_layer(x, w_r, w_i, w_o)
+    np.testing.assert_allclose(y, dense, atol=1e-12)
+
+
+def test_layer_zero_experts_give_zero_and_all_tokens_kept():
+    x, w_r, w_i, w_o = _rand_layer(50, 8, 16, 4, seed=10)
+    np.testing.assert_array_equal(O.moe_layer(x, w_r, 0 * w_i, w_o), 0.0)
+    y, rt, counts, offsets, perm = O.moe_layer(x, w_r, w_i, w_o, return_routing=True)
+    assert counts.sum() == 50                                   # droplessness
+    assert (np.abs(y).sum(axis=1) > 0).all()                    # every token got its expert output
+
+
+def test_layer_token_permutation_equivariance_and_expert_relabelling():
+    x, w_r, w_i, w_o = _rand_layer(60, 8, 16, 6, seed=11)
+    y = O.moe_layer(x, w_r, w_i, w_o)
+    p = rng.permutation(60)
+    np.testing.assert_allclose(O.moe_layer(x[p], w_r, w_i, w_o), y[p], atol=1e-13)
+    q = rng.permutation(6)
+    np.testing.assert_allclose(O.moe_layer(x, w_r[:, q], w_i[q], w_o[q]), y, atol=1e-13)
+
+
+def test_layer_tokens_sample_matches_full_layer():
+    x, w_r, w_i, w_o = _rand_layer(80, 8, 16, 5, seed=12)
+    y = O.moe_layer(x, w_r, w_i, w_o)
+    rows = np.array([0, 7, 33, 79])
+    ys, rt = O.moe_layer_tokens(x[rows], w_r, lambda e: (w_i[e], w_o[e]))
+    np.testing.assert_allclose(ys, y[rows], atol=1e-14)
+
+
+# ----------------------------------------------------------------- Algorithm 1 sharded
+@pytest.mark.parametrize("G", [1, 2, 4])
+@pytest.mark.parametrize("routing", ["natural", "skewed"])
+def test_sharded_alg1_equals_unsharded(G, routing):
+    # summing y_g over GPUs yields the unsharded output
+    n, h, d_ff, E = 24, 12, 32, 8
+    x, w_r, w_i, w_o = _rand_layer(n * G, h, d_ff, E, seed=20 + G)
+    forced = None
+    if routing == "skewed":
+        forced = np.where(rng.random(n * G) < 0.9, 2, rng.integers(0, E, n * G))
+    y = O.moe_layer(x, w_r, w_i, w_o, forced=forced)
+    stats = {}
+    outs = O.moe_layer_sharded([x[g * n:(g + 1) * n] for g in range(G)], w_r, w_i, w_o,
+                               None if forced is None else [forced[g * n:(g + 1) * n] for g in range(G)],
+                               stats=stats)
+    got = np.concatenate(outs)
+    assert O.max_abs_rel(got, y) <= 1e-12
+    # per-GPU work identical whatever the routing
+    assert stats["macs_per_rank"] == [O.macs_per_rank(n * G, h, d_ff, G)] * G
+    # metadata table: row g is GPU g's m_sizes; column sums are global counts
+    np.testing.assert_array_equal(stats["m_sizes"].sum(axis=0),
+                                  np.bincount(O.route(x, w_r, forced).expert, minlength=E))
+
+
+def test_sharded_partials_are_not_individually_the_answer():
+    # guards an oracle that would forget to sum partials (Step 5)
+    n, h, d_ff, E = 16, 8, 16, 2
+    x, w_r, w_i, w_o = _rand_layer(2 * n, h, d_ff, E, seed=30)
+    wi0, wo0 = O.extract_shard(w_i, w_o, 0, 2)
+    half = O.moe_layer(x, w_r, wi0, wo0)
+    assert O.max_abs_rel(half, O.moe_layer(x, w_r, w_i, w_o)) > 1e-3
+
+
+def test_sharded_divisibility_error():
+    x, w_r, w_i, w_o = _rand_layer(8, 4, 6, 2, seed=31)
+    with pytest.raises(ValueError):
+        O.moe_layer_sharded([x[:2], x[2:4], x[4:6], x[6:]], w_r, w_i, w_o)
+
+
+def test_max_abs_rel_definition():
+    ref = np.array([[1.0, -4.0], [2.0, 0.0]])
+    y = ref + np.array([[0.1, 0.0], [0.0, -0.2]])
+    assert O.max_abs_rel(y, ref) == pytest.approx(0.2 / 4.0)
