@@ -1,0 +1,180 @@
+/*
+ * moeshard.h - C ABI of the B200-native MoEShard sharded Switch-MoE layer.
+ *
+ * The operation (arXiv 2503.08467, "Accelerating MoE Model Inference with
+ * Expert Sharding", PAPER.md = the paper's LaTeX source):
+ *
+ *   Every GPU g of G calls forward(x) on its own tokens x [n, h]
+ *   (Alg. 1). Each GPU holds one shard of EVERY
+ *   expert: columns [g*d_ff/G, (g+1)*d_ff/G) of W_i and the same rows of W_o
+ *   (Sec. 3.2). The router is replicated
+ *   (PAPER.md:249). The five steps are
+ *     1 route      m_expert <- router(x)
+ *     2 metadata   groupPerExpert / countPerExpert, send
+ *     3 scatter    replicate all tokens on all GPUs
+ *     4 compute    every GPU runs all tokens through its   PAPER.md:203-209, 282-287,
+ *                  shard of their expert, fused over all    339-345 (Sec. 3.3)
+ *                  experts/GPUs into one grouped product
+ *     5 gather     partial outputs back to the owner GPU
+ *                  and point-wise summed (aggregateTokens)
+ *   and GPU g's output is, for each of its tokens t,
+ *     y_t = g_t * relu(x_t W_i^{e_t}) W_o^{e_t}   summed over the G shards,
+ *   g_t = softmax(x_t W_r)[e_t], e_t = argmax (lowest index on ties).
+ *   Readings of the paper used here are listed in DESIGN.md ("Readings").
+ *
+ * Conventions (all entry points):
+ *   - Return MOESHARD_OK (0) or a negative moeshard_status; no exceptions
+ *     cross the ABI. moeshard_last_error() gives the detailed text (e.g.
+ *     both shapes on a shape error).
+ *   - Ownership: the CALLER owns every buffer it passes (hidden, router_w,
+ *     hidden_out, workspace, weight storage, routing outputs); the library
+ *     never frees caller memory and performs no device allocation inside
+ *     moeshard_forward. The library owns only its context object and, for
+ *     world > 1 (or MOESHARD_FLAG_FORCE_COLLECTIVES), an NCCL communicator.
+ *   - Pointers marked [dev] are device pointers on the context's device;
+ *     [host] are host pointers. `stream` is a cudaStream_t passed as void*.
+ *   - moeshard_forward is enqueue-only on `stream`: no host synchronisation,
+ *     no data-dependent launch geometry, CUDA-graph capturable.
+ *   - Collective calls (moeshard_init, moeshard_forward) must be made by all
+ *     `world` ranks in the same order with the same `layer` and `n_local`.
+ */
+#ifndef MOESHARD_H
+#define MOESHARD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MOESHARD_OK = 0,
+  MOESHARD_ERR_INVALID_ARG = -1,  /* null pointer, negative size, bad enum */
+  MOESHARD_ERR_SHAPE = -2,        /* shape mismatch (message names both shapes) */
+  MOESHARD_ERR_DIVISIBILITY = -3, /* d_ff not divisible by world */
+  MOESHARD_ERR_BOUNDS = -4,       /* rank/layer/n_local out of range */
+  MOESHARD_ERR_CONFIG = -5,       /* unsupported configuration or device (not sm_100) */
+  MOESHARD_ERR_NOT_LOADED = -6,   /* forward on a layer whose shards were never loaded */
+  MOESHARD_ERR_PROTOCOL = -7,     /* ranks disagree (collective contract violated) */
+  MOESHARD_ERR_CUDA = -8,         /* CUDA runtime / driver error */
+  MOESHARD_ERR_NCCL = -9          /* NCCL error */
+} moeshard_status;
+
+typedef enum {
+  MOESHARD_BF16 = 0, /* bf16 storage, fp32 accumulation, tcgen05 tensor cores */
+  MOESHARD_FP32 = 1  /* fp32 validation mode: fp32 everywhere, FFMA on CUDA cores */
+} moeshard_dtype;
+
+/* config.flags */
+#define MOESHARD_FLAG_FORCE_COLLECTIVES 0x1u /* run the AllGather/ReduceScatter path even at world = 1 */
+#define MOESHARD_FLAG_SIMT_GEMM 0x2u         /* bf16 mode: CUDA-core grouped GEMM (ablation / debug) */
+
+typedef struct {
+  int32_t d_model;             /* h; multiple of 128 */
+  int32_t d_ff;                /* FULL expert hidden width; d_ff/world multiple of 128 */
+  int32_t n_experts;           /* E, 1 <= E <= 1024 */
+  int32_t n_layers;            /* number of weight slots (MoE layers) this context serves */
+  int32_t max_tokens_per_rank; /* upper bound on n_local */
+  int32_t dtype;               /* moeshard_dtype */
+  uint32_t flags;              /* MOESHARD_FLAG_* */
+} moeshard_config;
+
+typedef struct moeshard_ctx moeshard_ctx;
+
+/* NCCL unique id for world > 1 (or FORCE_COLLECTIVES): call on rank 0 only,
+ * broadcast the 128 bytes to all ranks (e.g. torch.distributed), pass to
+ * moeshard_init. out: [host] 128 bytes. */
+int moeshard_get_unique_id(uint8_t out[128]);
+
+/* Bytes of device workspace moeshard_init needs for this config and world
+ * size (activations, routing tables, permutation; sized for
+ * world * max_tokens_per_rank tokens). bytes: [host] out. */
+int moeshard_workspace_size(const moeshard_config* cfg, int world, size_t* bytes);
+
+/* Bytes of device weight storage per layer: 2 * E * h * (d_ff/world) elements
+ * of the config dtype. bytes_per_layer: [host] out. */
+int moeshard_weight_storage_size(const moeshard_config* cfg, int world, size_t* bytes_per_layer);
+
+/* Create a context for `rank` of `world` on CUDA `device`.
+ * uid: [host] 128 bytes from moeshard_get_unique_id (ignored when world == 1
+ *      without FORCE_COLLECTIVES; may be NULL then).
+ * workspace: [dev] caller-owned, >= moeshard_workspace_size bytes, 256-B
+ *      aligned, must stay alive until moeshard_destroy.
+ * Errors: DIVISIBILITY (d_ff % world), CONFIG (shape limits, device not
+ * sm_100), BOUNDS (rank not in [0, world)), NCCL, CUDA. Collective when a
+ * communicator is created. */
+int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int world,
+                  const uint8_t uid[128], void* workspace, size_t ws_bytes, int device);
+
+/* loadShard (Alg. 1 Step 4): install this rank's shard
+ * of every expert of `layer`.
+ *   w_in_shard  [dev] [E][h][d_ff/world] row-major: columns rank*F..(rank+1)*F of W_i
+ *   w_out_shard [dev] [E][d_ff/world][h] row-major: the same rows of W_o
+ *   weight_storage [dev] caller-owned, >= moeshard_weight_storage_size bytes;
+ *     the library repacks the shards into it (K-major: W_i^T, W_o^T per
+ *     expert) and keeps using it until destroy or a reload of that layer.
+ * The repack is enqueued on `stream`; the inputs may be freed after it. */
+int moeshard_load_expert_shards(moeshard_ctx* ctx, int layer, const void* w_in_shard,
+                                const void* w_out_shard, void* weight_storage, size_t bytes,
+                                void* stream);
+
+/* The MoEShard forward of one MoE layer (Alg. 1).
+ *   hidden       [dev] [n_local][h] this rank's tokens (dtype of the config)
+ *   router_w     [dev] [h][E] replicated router weight
+ *   hidden_out   [dev] [n_local][h] MoE FFN output for this rank's tokens
+ *                (no residual: Alg. 1 returns the aggregated tokens)
+ *   forced_expert [dev] nullable [n_local] int32: the paper's replaced router
+ *                (PAPER.md:368-372): e_t is taken from here, g_t is still
+ *                softmax(x_t W_r)[e_t]; the router kernel still runs. Ids
+ *                outside [0, E) are clamped and raise the sticky device error
+ *                reported by moeshard_check().
+ * n_local must satisfy 0 <= n_local <= max_tokens_per_rank and be equal on
+ * all ranks (v1). Enqueue-only on `stream`. Errors: BOUNDS, NOT_LOADED,
+ * INVALID_ARG, CUDA, NCCL. */
+int moeshard_forward(moeshard_ctx* ctx, int layer, const void* hidden, int n_local,
+                     const void* router_w, void* hidden_out, const int32_t* forced_expert,
+                     void* stream);
+
+/* Routing of the most recent forward (Steps 1-2), copied on `stream` into
+ * caller device buffers (any may be NULL):
+ *   expert_all [dev] int32 [world*n_local]  e_t for all global tokens t = r*n + i
+ *   gate_all   [dev] fp32  [world*n_local]  g_t
+ *   counts     [dev] int32 [E]              m_sizes summed over ranks
+ *   offsets    [dev] int32 [E+1]            exclusive scan of counts
+ *   perm       [dev] int32 [world*n_local]  global token ids grouped by expert,
+ *                                           ascending inside each expert */
+int moeshard_get_routing(moeshard_ctx* ctx, int32_t* expert_all, float* gate_all, int32_t* counts,
+                         int32_t* offsets, int32_t* perm, void* stream);
+
+/* Per-forward work counters of the most recent forward ([host] out, syncs
+ * the stream): tokens seen, grouped-GEMM tiles executed by the up and down
+ * products, and rows executed (tile padding included). */
+typedef struct {
+  int64_t n_tokens_global;
+  int64_t tiles_up;
+  int64_t tiles_down;
+  int64_t rows_executed_up;   /* sum over tiles of the MMA N (tokens) actually issued */
+} moeshard_stats;
+int moeshard_get_stats(moeshard_ctx* ctx, moeshard_stats* out, void* stream);
+
+/* Synchronise `stream` and report the sticky device error (forced id out of
+ * range) and any asynchronous CUDA/NCCL error. */
+int moeshard_check(moeshard_ctx* ctx, void* stream);
+
+/* Text of the last error on this context (or of the last failed call made
+ * with a NULL context, e.g. moeshard_init). Never NULL. */
+const char* moeshard_last_error(const moeshard_ctx* ctx);
+const char* moeshard_status_string(int status);
+
+/* Release the communicator and the context. Caller memory is untouched. */
+int moeshard_destroy(moeshard_ctx* ctx);
+
+/* Library version string, e.g. "moeshard-b200 0.1 sm_100a". */
+const char* moeshard_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOESHARD_H */

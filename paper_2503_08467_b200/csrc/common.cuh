@@ -1,0 +1,85 @@
+// common.cuh - shared device helpers for the moeshard kernels (sm_100a only).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "moeshard kernels target sm_100a (B200) only"
+#endif
+
+namespace moeshard {
+
+constexpr int kMaxExperts = 256;      // router instantiations cover E <= 256
+constexpr int kHistChunk = 1024;      // tokens per block in the histogram / scatter kernels
+constexpr int kTcTokTile = 256;       // max tokens per tcgen05 tile (UMMA N <= 256)
+constexpr int kTcFeatTile = 128;      // weight rows per tcgen05 tile (UMMA M)
+constexpr int kSimtTokTile = 64;      // tokens per SIMT tile
+constexpr int kSimtFeatTile = 64;     // output features per SIMT tile
+
+// Routing record of one token, gathered across ranks in one NCCL AllGather
+// (Step 2 metadata folded into the token exchange): expert id + gate bits.
+struct __align__(8) RouteRec {
+  int32_t expert;
+  float gate;
+};
+
+// Device-side per-forward tables written by the scan kernel.
+struct Tables {
+  int32_t* counts;         // [E]
+  int32_t* offsets;        // [E+1]
+  int32_t* tc_chunk_pref;  // [E+1] cumulative tcgen05 token chunks
+  int32_t* tc_chunk_size;  // [E]
+  int32_t* simt_chunk_pref;  // [E+1]
+  int32_t* stats;          // [8]: 0 tiles_up, 1 tiles_down, 2 rows_up, 3 error flag
+};
+
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+__host__ __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ int round_up(int a, int b) { return ceil_div(a, b) * b; }
+
+// Token chunking of one expert's segment for the tcgen05 tiles: split n_e
+// tokens into ceil(n_e/256) near-equal chunks of a multiple of 16 tokens.
+__host__ __device__ __forceinline__ void tc_chunking(int n_e, int* n_chunks, int* chunk) {
+  if (n_e <= 0) { *n_chunks = 0; *chunk = 0; return; }
+  int c0 = ceil_div(n_e, kTcTokTile);
+  int cs = round_up(ceil_div(n_e, c0), 16);
+  *chunk = cs;
+  *n_chunks = ceil_div(n_e, cs);
+}
+
+}  // namespace moeshard
+
+// ---------------------------------------------------------------------------
+// Host-side launcher declarations (implemented in the .cu files)
+// ---------------------------------------------------------------------------
+namespace moeshard {
+
+void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int E,
+                   const int32_t* forced, RouteRec* out, int32_t* err_flag, cudaStream_t s);
+
+void launch_group(const RouteRec* route, int N, int E, int32_t* block_hist, int32_t* block_base,
+                  Tables tb, int n_out_up, int n_out_down, int32_t* perm, cudaStream_t s);
+
+void launch_gather_rows(const void* x_all, const int32_t* perm, int N, int row_bytes, void* x_perm,
+                        cudaStream_t s);
+
+void launch_transpose(int dtype, const void* src, void* dst, int batch, int rows, int cols,
+                      cudaStream_t s);
+
+// SIMT grouped GEMMs (fp32 validation mode, and bf16 ablation).
+void launch_simt_up(int dtype, const void* x_perm, const void* wt_in, int K, int F, int E, Tables tb,
+                    void* H, int num_sms, cudaStream_t s);
+void launch_simt_down(int dtype, const void* H, const void* wt_out, int K, int h, int E, Tables tb,
+                      const int32_t* perm, const RouteRec* route, void* out, int num_sms,
+                      cudaStream_t s);
+
+}  // namespace moeshard

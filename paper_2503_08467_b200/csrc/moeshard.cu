@@ -1,0 +1,523 @@
+// moeshard.cu - host orchestrator behind the C ABI (include/moeshard.h).
+//
+// Owns: the context, the carve-up of the caller's workspace, the per-layer
+// K-major weight views and their TMA descriptors, and (world > 1) an NCCL
+// communicator (libnccl is dlopen'ed; with torch loaded this is the same
+// library torch.distributed uses). moeshard_forward enqueues Alg. 1
+// on the caller's stream:
+//
+//   1 router kernel (local tokens)                          Step 1
+//   2 ncclGroup{ AllGather(tokens), AllGather(route recs) }  Steps 2+3 (metadata folded
+//                                                           into the token exchange)
+//   3 group_hist / group_scan / group_scatter / gather_rows Step 2 grouping + Sec. 3.3
+//                                                           cross-GPU per-expert concat
+//   4 grouped GEMM up (+ReLU), grouped GEMM down (+gate,    Step 4 (Sec. 3.3 fusion)
+//     +un-permute scatter)
+//   5 ncclReduceScatter(sum)                                Step 5 gather + aggregateTokens
+//
+// No host synchronisation and no allocation inside forward.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/moeshard.h"
+#include "common.cuh"
+#include "gemm_tc.cuh"
+
+using namespace moeshard;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  const char* env = getenv("MOESHARD_NCCL_LIB");
+  if (!h && env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+#define LOAD(name, sym)                                          \
+  api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, sym)); \
+  if (!api.name) return api;
+  LOAD(GetUniqueId, "ncclGetUniqueId");
+  LOAD(CommInitRank, "ncclCommInitRank");
+  LOAD(CommDestroy, "ncclCommDestroy");
+  LOAD(CommGetAsyncError, "ncclCommGetAsyncError");
+  LOAD(AllGather, "ncclAllGather");
+  LOAD(ReduceScatter, "ncclReduceScatter");
+  LOAD(GroupStart, "ncclGroupStart");
+  LOAD(GroupEnd, "ncclGroupEnd");
+  LOAD(GetErrorString, "ncclGetErrorString");
+#undef LOAD
+  api.ok = true;
+  return api;
+}
+
+// ------------------------------------------------------------------ TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [outer][inner] (inner contiguous), box [box_outer][64], 128-B swizzle.
+bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+               uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+// Workspace carve-up, shared by moeshard_workspace_size and moeshard_init.
+struct Layout {
+  size_t route, block_hist, block_base, ints, perm, x_all, x_perm, H, partial, total;
+  int n_ints;
+};
+
+Layout make_layout(const moeshard_config& c, int world) {
+  const bool coll = world > 1 || (c.flags & MOESHARD_FLAG_FORCE_COLLECTIVES);
+  const size_t elt = c.dtype == MOESHARD_BF16 ? 2 : 4;
+  const size_t Nmax = static_cast<size_t>(world) * c.max_tokens_per_rank;
+  const size_t nb = std::max<size_t>(1, (Nmax + kHistChunk - 1) / kHistChunk);
+  const size_t E = c.n_experts, h = c.d_model, F = c.d_ff / world;
+  Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  L.route = take(Nmax * sizeof(RouteRec));
+  L.block_hist = take(nb * E * 4);
+  L.block_base = take(nb * E * 4);
+  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8);
+  L.ints = take(L.n_ints * 4);
+  L.perm = take(Nmax * 4);
+  L.x_all = coll ? take(Nmax * h * elt) : 0;
+  L.x_perm = take(Nmax * h * elt);
+  L.H = take(Nmax * F * elt);
+  L.partial = coll ? take(Nmax * h * elt) : 0;
+  L.total = off;
+  return L;
+}
+
+}  // namespace
+
+struct LayerW {
+  bool loaded = false;
+  void* wt_in = nullptr;   // [E][F][h]  (W_i^T shard, K-major for the up product)
+  void* wt_out = nullptr;  // [E][h][F]  (W_o^T shard, K-major for the down product)
+  CUtensorMap tm_in{}, tm_out{};
+};
+
+struct moeshard_ctx {
+  moeshard_config cfg{};
+  int rank = 0, world = 1, device = 0, num_sms = 148;
+  int h = 0, F = 0, E = 0, elt = 2;
+  bool coll = false, use_tc = true;
+  Layout L{};
+  char* ws = nullptr;
+  RouteRec* route = nullptr;
+  int32_t *block_hist = nullptr, *block_base = nullptr, *perm = nullptr;
+  Tables tb{};
+  void *x_all = nullptr, *x_perm = nullptr, *H = nullptr, *partial = nullptr;
+  CUtensorMap tm_xperm{}, tm_H{};
+  std::vector<LayerW> layers;
+  ncclComm_t comm = nullptr;
+  int last_n = 0;
+  std::string err = "no error";
+};
+
+namespace {
+
+int fail(moeshard_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(ctx, expr)                                                            \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return fail(ctx, MOESHARD_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                                  \
+  do {                                                                                       \
+    ncclResult_t _r = (expr);                                                                \
+    if (_r != ncclSuccess)                                                                   \
+      return fail(ctx, MOESHARD_ERR_NCCL, "%s failed: %s", #expr, nccl().GetErrorString(_r)); \
+  } while (0)
+
+int validate(const moeshard_config* c, int world) {
+  if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "config is NULL");
+  if (world < 1) return fail(nullptr, MOESHARD_ERR_BOUNDS, "world=%d must be >= 1", world);
+  if (c->dtype != MOESHARD_BF16 && c->dtype != MOESHARD_FP32)
+    return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "dtype=%d is not BF16(0)/FP32(1)", c->dtype);
+  if (c->n_experts < 1 || c->n_experts > 256)
+    return fail(nullptr, MOESHARD_ERR_CONFIG, "n_experts=%d outside [1, 256]", c->n_experts);
+  if (c->d_model < 128 || c->d_model % 128)
+    return fail(nullptr, MOESHARD_ERR_CONFIG, "d_model=%d must be a positive multiple of 128",
+                c->d_model);
+  if (c->d_ff < 1 || c->d_ff % world)
+    return fail(nullptr, MOESHARD_ERR_DIVISIBILITY,
+                "d_ff=%d is not divisible by world=%d (PAPER.md:169, 329-330)", c->d_ff, world);
+  if ((c->d_ff / world) % 128)
+    return fail(nullptr, MOESHARD_ERR_CONFIG, "d_ff/world=%d must be a multiple of 128",
+                c->d_ff / world);
+  if (c->n_layers < 1) return fail(nullptr, MOESHARD_ERR_CONFIG, "n_layers=%d < 1", c->n_layers);
+  if (c->max_tokens_per_rank < 0 ||
+      static_cast<long long>(c->max_tokens_per_rank) * world > (1LL << 30))
+    return fail(nullptr, MOESHARD_ERR_CONFIG, "max_tokens_per_rank=%d out of range",
+                c->max_tokens_per_rank);
+  return MOESHARD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* moeshard_version(void) { return "moeshard-b200 0.1 sm_100a"; }
+
+const char* moeshard_status_string(int s) {
+  switch (s) {
+    case MOESHARD_OK: return "MOESHARD_OK";
+    case MOESHARD_ERR_INVALID_ARG: return "MOESHARD_ERR_INVALID_ARG";
+    case MOESHARD_ERR_SHAPE: return "MOESHARD_ERR_SHAPE";
+    case MOESHARD_ERR_DIVISIBILITY: return "MOESHARD_ERR_DIVISIBILITY";
+    case MOESHARD_ERR_BOUNDS: return "MOESHARD_ERR_BOUNDS";
+    case MOESHARD_ERR_CONFIG: return "MOESHARD_ERR_CONFIG";
+    case MOESHARD_ERR_NOT_LOADED: return "MOESHARD_ERR_NOT_LOADED";
+    case MOESHARD_ERR_PROTOCOL: return "MOESHARD_ERR_PROTOCOL";
+    case MOESHARD_ERR_CUDA: return "MOESHARD_ERR_CUDA";
+    case MOESHARD_ERR_NCCL: return "MOESHARD_ERR_NCCL";
+    default: return "MOESHARD_ERR_UNKNOWN";
+  }
+}
+
+const char* moeshard_last_error(const moeshard_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_err.c_str();
+}
+
+int moeshard_get_unique_id(uint8_t out[128]) {
+  if (!out) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "out is NULL");
+  if (!nccl().ok) return fail(nullptr, MOESHARD_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  NCCL_TRY(nullptr, nccl().GetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out, &id, 128);
+  return MOESHARD_OK;
+}
+
+int moeshard_workspace_size(const moeshard_config* cfg, int world, size_t* bytes) {
+  int st = validate(cfg, world);
+  if (st) return st;
+  if (!bytes) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "bytes is NULL");
+  *bytes = make_layout(*cfg, world).total;
+  return MOESHARD_OK;
+}
+
+int moeshard_weight_storage_size(const moeshard_config* cfg, int world, size_t* bytes) {
+  int st = validate(cfg, world);
+  if (st) return st;
+  if (!bytes) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "bytes is NULL");
+  const size_t elt = cfg->dtype == MOESHARD_BF16 ? 2 : 4;
+  *bytes = 2 * static_cast<size_t>(cfg->n_experts) * cfg->d_model * (cfg->d_ff / world) * elt;
+  return MOESHARD_OK;
+}
+
+int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int world,
+                  const uint8_t uid[128], void* workspace, size_t ws_bytes, int device) {
+  if (!out) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  int st = validate(cfg, world);
+  if (st) return st;
+  if (rank < 0 || rank >= world)
+    return fail(nullptr, MOESHARD_ERR_BOUNDS, "rank=%d not in [0, world=%d)", rank, world);
+  Layout L = make_layout(*cfg, world);
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255))
+    return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "workspace NULL or not 256-B aligned");
+  if (ws_bytes < L.total)
+    return fail(nullptr, MOESHARD_ERR_SHAPE, "workspace has %zu bytes, needs %zu", ws_bytes,
+                L.total);
+  int ndev = 0;
+  CUDA_TRY(nullptr, cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return fail(nullptr, MOESHARD_ERR_BOUNDS, "device=%d not in [0, %d)", device, ndev);
+  CUDA_TRY(nullptr, cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(nullptr, cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(nullptr, MOESHARD_ERR_CONFIG,
+                "device %d is sm_%d%d; this library is built for sm_100a (B200) only", device,
+                prop.major, prop.minor);
+
+  auto* c = new moeshard_ctx();
+  c->cfg = *cfg;
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  c->h = cfg->d_model;
+  c->F = cfg->d_ff / world;
+  c->E = cfg->n_experts;
+  c->elt = cfg->dtype == MOESHARD_BF16 ? 2 : 4;
+  c->coll = world > 1 || (cfg->flags & MOESHARD_FLAG_FORCE_COLLECTIVES);
+  c->use_tc = cfg->dtype == MOESHARD_BF16 && !(cfg->flags & MOESHARD_FLAG_SIMT_GEMM);
+  c->L = L;
+  c->ws = static_cast<char*>(workspace);
+  c->route = reinterpret_cast<RouteRec*>(c->ws + L.route);
+  c->block_hist = reinterpret_cast<int32_t*>(c->ws + L.block_hist);
+  c->block_base = reinterpret_cast<int32_t*>(c->ws + L.block_base);
+  int32_t* ints = reinterpret_cast<int32_t*>(c->ws + L.ints);
+  const int E = c->E;
+  c->tb.counts = ints;
+  c->tb.offsets = ints + E;
+  c->tb.tc_chunk_pref = c->tb.offsets + (E + 1);
+  c->tb.tc_chunk_size = c->tb.tc_chunk_pref + (E + 1);
+  c->tb.simt_chunk_pref = c->tb.tc_chunk_size + E;
+  c->tb.stats = c->tb.simt_chunk_pref + (E + 1);
+  c->perm = reinterpret_cast<int32_t*>(c->ws + L.perm);
+  c->x_all = c->coll ? c->ws + L.x_all : nullptr;
+  c->x_perm = c->ws + L.x_perm;
+  c->H = c->ws + L.H;
+  c->partial = c->coll ? c->ws + L.partial : nullptr;
+  c->layers.resize(cfg->n_layers);
+  cudaError_t e = cudaMemset(ints, 0, L.n_ints * 4);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(nullptr, MOESHARD_ERR_CUDA, "cudaMemset: %s", cudaGetErrorString(e));
+  }
+  const int Nmax = world * cfg->max_tokens_per_rank;
+  if (c->use_tc && Nmax > 0) {
+    if (!make_tmap(&c->tm_xperm, c->x_perm, c->h, Nmax, 32) ||
+        !make_tmap(&c->tm_H, c->H, c->F, Nmax, 32)) {
+      delete c;
+      return fail(nullptr, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
+    }
+  }
+  if (c->coll) {
+    if (!uid) {
+      delete c;
+      return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "uid is NULL but a communicator is needed");
+    }
+    if (!nccl().ok) {
+      delete c;
+      return fail(nullptr, MOESHARD_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    }
+    ncclUniqueId id;
+    memcpy(&id, uid, 128);
+    ncclResult_t r = nccl().CommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      return fail(nullptr, MOESHARD_ERR_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
+    }
+  }
+  *out = c;
+  return MOESHARD_OK;
+}
+
+int moeshard_load_expert_shards(moeshard_ctx* c, int layer, const void* w_in_shard,
+                                const void* w_out_shard, void* storage, size_t bytes,
+                                void* stream) {
+  if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "ctx is NULL");
+  if (layer < 0 || layer >= c->cfg.n_layers)
+    return fail(c, MOESHARD_ERR_BOUNDS, "layer=%d not in [0, %d)", layer, c->cfg.n_layers);
+  if (!w_in_shard || !w_out_shard || !storage)
+    return fail(c, MOESHARD_ERR_INVALID_ARG, "NULL shard or storage pointer");
+  if (reinterpret_cast<uintptr_t>(storage) & 255)
+    return fail(c, MOESHARD_ERR_INVALID_ARG, "weight storage must be 256-B aligned");
+  const size_t per = static_cast<size_t>(c->E) * c->h * c->F * c->elt;
+  if (bytes < 2 * per)
+    return fail(c, MOESHARD_ERR_SHAPE, "weight storage has %zu bytes, needs %zu", bytes, 2 * per);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  LayerW& lw = c->layers[layer];
+  lw.wt_in = storage;
+  lw.wt_out = static_cast<char*>(storage) + per;
+  // W_i^r [E][h][F] -> [E][F][h];  W_o^r [E][F][h] -> [E][h][F]
+  launch_transpose(c->cfg.dtype, w_in_shard, lw.wt_in, c->E, c->h, c->F, s);
+  launch_transpose(c->cfg.dtype, w_out_shard, lw.wt_out, c->E, c->F, c->h, s);
+  CUDA_TRY(c, cudaGetLastError());
+  if (c->use_tc) {
+    if (!make_tmap(&lw.tm_in, lw.wt_in, c->h, static_cast<uint64_t>(c->E) * c->F, 128) ||
+        !make_tmap(&lw.tm_out, lw.wt_out, c->F, static_cast<uint64_t>(c->E) * c->h, 128))
+      return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for weights");
+  }
+  lw.loaded = true;
+  return MOESHARD_OK;
+}
+
+int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, const void* router_w,
+                     void* hidden_out, const int32_t* forced, void* stream) {
+  if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "ctx is NULL");
+  if (layer < 0 || layer >= c->cfg.n_layers)
+    return fail(c, MOESHARD_ERR_BOUNDS, "layer=%d not in [0, %d)", layer, c->cfg.n_layers);
+  if (!c->layers[layer].loaded)
+    return fail(c, MOESHARD_ERR_NOT_LOADED, "layer %d has no expert shards loaded", layer);
+  if (n < 0 || n > c->cfg.max_tokens_per_rank)
+    return fail(c, MOESHARD_ERR_BOUNDS, "n_local=%d not in [0, max_tokens_per_rank=%d]", n,
+                c->cfg.max_tokens_per_rank);
+  if (n > 0 && (!hidden || !router_w || !hidden_out))
+    return fail(c, MOESHARD_ERR_INVALID_ARG, "NULL hidden/router_w/hidden_out");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const LayerW& lw = c->layers[layer];
+  const int h = c->h, F = c->F, E = c->E;
+  const int N = c->coll ? c->world * n : n;
+  c->last_n = n;
+  if (n == 0) return MOESHARD_OK;
+  const ncclDataType_t ndt = c->cfg.dtype == MOESHARD_BF16 ? ncclBfloat16 : ncclFloat32;
+  int32_t* err_flag = c->tb.stats + 3;
+
+  // Step 1: route local tokens
+  RouteRec* my_route = c->route + (c->coll ? static_cast<size_t>(c->rank) * n : 0);
+  launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, err_flag, s);
+  // Steps 2+3: metadata + token scatter (replicate all tokens on all GPUs)
+  const void* x_all = hidden;
+  if (c->coll) {
+    NCCL_TRY(c, nccl().GroupStart());
+    NCCL_TRY(c, nccl().AllGather(hidden, c->x_all, static_cast<size_t>(n) * h, ndt, c->comm, s));
+    NCCL_TRY(c, nccl().AllGather(my_route, c->route, static_cast<size_t>(n) * 2, ncclInt32,
+                                 c->comm, s));
+    NCCL_TRY(c, nccl().GroupEnd());
+    x_all = c->x_all;
+  }
+  // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs
+  launch_group(c->route, N, E, c->block_hist, c->block_base, c->tb, F / kTcFeatTile,
+               h / kTcFeatTile, c->perm, s);
+  launch_gather_rows(x_all, c->perm, N, h * c->elt, c->x_perm, s);
+  // Step 4: expert computation, one grouped product per projection
+  void* P = c->coll ? c->partial : hidden_out;
+  if (c->use_tc) {
+    TcParams up{h, F / kTcFeatTile, F, E, c->tb, static_cast<__nv_bfloat16*>(c->H), F, nullptr,
+                nullptr};
+    CUDA_TRY(c, launch_tc_gemm(false, lw.tm_in, c->tm_xperm, up, c->num_sms, s));
+    TcParams dn{F, h / kTcFeatTile, h, E, c->tb, static_cast<__nv_bfloat16*>(P), h, c->perm,
+                c->route};
+    CUDA_TRY(c, launch_tc_gemm(true, lw.tm_out, c->tm_H, dn, c->num_sms, s));
+  } else {
+    launch_simt_up(c->cfg.dtype, c->x_perm, lw.wt_in, h, F, E, c->tb, c->H, c->num_sms, s);
+    launch_simt_down(c->cfg.dtype, c->H, lw.wt_out, F, h, E, c->tb, c->perm, c->route, P,
+                     c->num_sms, s);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  // Step 5: gather partial outputs to their owner and sum (aggregateTokens)
+  if (c->coll)
+    NCCL_TRY(c, nccl().ReduceScatter(P, hidden_out, static_cast<size_t>(n) * h, ndt, ncclSum,
+                                     c->comm, s));
+  return MOESHARD_OK;
+}
+
+int moeshard_get_routing(moeshard_ctx* c, int32_t* expert_all, float* gate_all, int32_t* counts,
+                         int32_t* offsets, int32_t* perm, void* stream) {
+  if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "ctx is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t N = static_cast<size_t>(c->coll ? c->world : 1) * c->last_n;
+  if (N > 0) {
+    if (expert_all)
+      CUDA_TRY(c, cudaMemcpy2DAsync(expert_all, 4, &c->route[0].expert, sizeof(RouteRec), 4, N,
+                                    cudaMemcpyDeviceToDevice, s));
+    if (gate_all)
+      CUDA_TRY(c, cudaMemcpy2DAsync(gate_all, 4, &c->route[0].gate, sizeof(RouteRec), 4, N,
+                                    cudaMemcpyDeviceToDevice, s));
+    if (perm) CUDA_TRY(c, cudaMemcpyAsync(perm, c->perm, N * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  if (counts)
+    CUDA_TRY(c, cudaMemcpyAsync(counts, c->tb.counts, c->E * 4, cudaMemcpyDeviceToDevice, s));
+  if (offsets)
+    CUDA_TRY(c, cudaMemcpyAsync(offsets, c->tb.offsets, (c->E + 1) * 4, cudaMemcpyDeviceToDevice,
+                                s));
+  return MOESHARD_OK;
+}
+
+int moeshard_get_stats(moeshard_ctx* c, moeshard_stats* out, void* stream) {
+  if (!c || !out) return fail(c, MOESHARD_ERR_INVALID_ARG, "NULL ctx or out");
+  int32_t st[8];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(c, cudaMemcpyAsync(st, c->tb.stats, sizeof(st), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  out->n_tokens_global = static_cast<int64_t>(c->coll ? c->world : 1) * c->last_n;
+  out->tiles_up = c->last_n ? st[0] : 0;
+  out->tiles_down = c->last_n ? st[1] : 0;
+  out->rows_executed_up = c->last_n ? st[2] : 0;
+  return MOESHARD_OK;
+}
+
+int moeshard_check(moeshard_ctx* c, void* stream) {
+  if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "ctx is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  CUDA_TRY(c, cudaGetLastError());
+  int32_t flag = 0;
+  CUDA_TRY(c, cudaMemcpy(&flag, c->tb.stats + 3, 4, cudaMemcpyDeviceToHost));
+  if (c->comm) {
+    ncclResult_t ar = ncclSuccess;
+    NCCL_TRY(c, nccl().CommGetAsyncError(c->comm, &ar));
+    if (ar != ncclSuccess)
+      return fail(c, MOESHARD_ERR_NCCL, "NCCL async error: %s", nccl().GetErrorString(ar));
+  }
+  if (flag) {
+    cudaMemset(c->tb.stats + 3, 0, 4);
+    return fail(c, MOESHARD_ERR_BOUNDS, "forced_expert contained ids outside [0, %d)", c->E);
+  }
+  return MOESHARD_OK;
+}
+
+int moeshard_destroy(moeshard_ctx* c) {
+  if (!c) return MOESHARD_OK;
+  if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  delete c;
+  return MOESHARD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,150 @@
+"""Torch-facing wrapper of the C ABI: one object per rank serving n_layers MoE layers.
+
+Marshalling only - buffers are torch tensors, pointers and the current CUDA
+stream are passed through to libmoeshard.so. For world > 1 rank 0 creates
+the NCCL unique id and it is broadcast with torch.distributed (CS3 in
+SURVEY.md §3; collective contract of moeshard_init).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Tuple
+
+import torch
+
+from . import moeshard as C
+
+_DTYPES = {torch.bfloat16: C.MOESHARD_BF16, torch.float32: C.MOESHARD_FP32}
+
+
+def shard_columns(d_ff: int, world: int, rank: int) -> Tuple[int, int]:
+    """This rank's contiguous slice of W_i's columns / W_o's rows."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} not in [0, {world})")
+    if d_ff % world:
+        raise ValueError(f"d_ff={d_ff} is not divisible by world={world} (PAPER.md:169)")
+    F = d_ff // world
+    return rank * F, (rank + 1) * F
+
+
+def local_token_range(n_global: int, world: int, rank: int) -> Tuple[int, int]:
+    """Tokens of rank r in the global rank-major order t = r*n + i (equal split, v1)."""
+    if n_global % world:
+        raise ValueError(f"global token count {n_global} not divisible by world {world}")
+    n = n_global // world
+    return rank * n, (rank + 1) * n
+
+
+def broadcast_uid(uid: Optional[bytes], rank: int, group=None) -> bytes:
+    """Rank 0's 128-byte NCCL id to every rank over torch.distributed (any backend)."""
+    import torch.distributed as dist
+    obj: List[Optional[bytes]] = [uid if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    assert obj[0] is not None and len(obj[0]) == 128
+    return obj[0]
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class MoEShardLayer:
+    """Sharded Switch-MoE FFN layers on one GPU of a `world`-GPU job."""
+
+    def __init__(self, d_model: int, d_ff: int, n_experts: int, *, n_layers: int = 1,
+                 max_tokens_per_rank: int, dtype=torch.bfloat16, rank: int = 0, world: int = 1,
+                 device: Optional[int] = None, flags: int = 0, group=None):
+        if dtype not in _DTYPES:
+            raise ValueError(f"dtype must be bf16 or fp32, got {dtype}")
+        self.device = torch.cuda.current_device() if device is None else device
+        self.dtype, self.rank, self.world = dtype, rank, world
+        self.h, self.d_ff, self.E = d_model, d_ff, n_experts
+        self.F = d_ff // world
+        self.cfg = C.moeshard_config(d_model, d_ff, n_experts, n_layers, max_tokens_per_rank,
+                                     _DTYPES[dtype], flags)
+        ws = C.moeshard_workspace_size(self.cfg, world)
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=f"cuda:{self.device}")
+        self._wbytes = C.moeshard_weight_storage_size(self.cfg, world)
+        self._storage: List[Optional[torch.Tensor]] = [None] * n_layers
+        uid = None
+        if world > 1 or (flags & C.MOESHARD_FLAG_FORCE_COLLECTIVES):
+            uid = C.moeshard_get_unique_id() if rank == 0 else None
+            if world > 1:
+                uid = broadcast_uid(uid, rank, group)
+        self.ctx = C.moeshard_init(self.cfg, rank, world, uid, self.workspace.data_ptr(), ws,
+                                   self.device)
+
+    @staticmethod
+    def _stream() -> int:
+        return torch.cuda.current_stream().cuda_stream
+
+    def load_expert_shards(self, layer: int, w_in_shard: torch.Tensor, w_out_shard: torch.Tensor):
+        """w_in_shard [E, h, d_ff/world], w_out_shard [E, d_ff/world, h] (this rank's slices)."""
+        exp_in, exp_out = (self.E, self.h, self.F), (self.E, self.F, self.h)
+        if tuple(w_in_shard.shape) != exp_in or tuple(w_out_shard.shape) != exp_out:
+            raise C.MoEShardError(-2, f"shards {tuple(w_in_shard.shape)}/{tuple(w_out_shard.shape)}"
+                                      f" vs expected {exp_in}/{exp_out}")
+        w_in_shard = w_in_shard.to(device=f"cuda:{self.device}", dtype=self.dtype).contiguous()
+        w_out_shard = w_out_shard.to(device=f"cuda:{self.device}", dtype=self.dtype).contiguous()
+        st = torch.empty(self._wbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        C.moeshard_load_expert_shards(self.ctx, layer, w_in_shard.data_ptr(),
+                                      w_out_shard.data_ptr(), st.data_ptr(), self._wbytes,
+                                      self._stream())
+        torch.cuda.current_stream().synchronize()  # inputs may be freed by the caller afterwards
+        self._storage[layer] = st
+
+    def forward(self, layer: int, hidden: torch.Tensor, router_w: torch.Tensor,
+                forced_expert: Optional[torch.Tensor] = None,
+                out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        n = hidden.shape[0]
+        if hidden.dtype != self.dtype or router_w.dtype != self.dtype:
+            raise C.MoEShardError(-1, f"hidden/router_w must be {self.dtype}")
+        if hidden.dim() != 2 or hidden.shape[1] != self.h or tuple(router_w.shape) != (self.h, self.E):
+            raise C.MoEShardError(-2, f"hidden {tuple(hidden.shape)} / router_w {tuple(router_w.shape)}"
+                                      f" vs expected [n, {self.h}] / [{self.h}, {self.E}]")
+        if not (hidden.is_contiguous() and router_w.is_contiguous()):
+            raise C.MoEShardError(-1, "hidden and router_w must be contiguous")
+        if out is None:
+            out = torch.empty_like(hidden)
+        if forced_expert is not None:
+            if forced_expert.dtype != torch.int32 or forced_expert.shape != (n,):
+                raise C.MoEShardError(-2, f"forced_expert must be int32 [{n}]")
+        C.moeshard_forward(self.ctx, layer, hidden.data_ptr(), n, router_w.data_ptr(),
+                           out.data_ptr(), _ptr(forced_expert), self._stream())
+        return out
+
+    __call__ = forward
+
+    def routing(self, n_local: int) -> dict:
+        N = n_local * (self.world if self._collective() else 1)
+        dev = f"cuda:{self.device}"
+        r = {
+            "expert": torch.empty(N, dtype=torch.int32, device=dev),
+            "gate": torch.empty(N, dtype=torch.float32, device=dev),
+            "counts": torch.empty(self.E, dtype=torch.int32, device=dev),
+            "offsets": torch.empty(self.E + 1, dtype=torch.int32, device=dev),
+            "perm": torch.empty(N, dtype=torch.int32, device=dev),
+        }
+        C.moeshard_get_routing(self.ctx, r["expert"].data_ptr(), r["gate"].data_ptr(),
+                               r["counts"].data_ptr(), r["offsets"].data_ptr(),
+                               r["perm"].data_ptr(), self._stream())
+        return r
+
+    def _collective(self) -> bool:
+        return self.world > 1 or bool(self.cfg.flags & C.MOESHARD_FLAG_FORCE_COLLECTIVES)
+
+    def stats(self) -> dict:
+        return C.moeshard_get_stats(self.ctx, self._stream())
+
+    def check(self):
+        C.moeshard_check(self.ctx, self._stream())
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None:
+            C.moeshard_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
