@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""bench.py - MoE-layer tokens/s of the B200 MoEShard sharded Switch-MoE layer.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c5]
+                    [--impl ours|reference]
+
+One step = one full MoE-layer forward through the C ABI (all SURVEY.md §8(a)
+rows: router, token/metadata AllGather, grouping + permute, grouped GEMM up,
+grouped GEMM down, ReduceScatter) on N_global tokens split evenly over the N
+ranks (strong scaling: BASELINE.json configs read as global token counts,
+DESIGN.md R8). Default workload: BASELINE.json configs[1], Switch-Base-64
+(E=64, d_model=768, d_ff=3072, 8192 tokens), bf16.
+
+Rank 0 prints ONE JSON line. Under torchrun every rank runs the layer and the
+time is the max over ranks. --impl reference times the CPU oracle (the
+reference arm of this tier) on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c2": dict(name="Switch-Base-64 MoE layer (BASELINE.json configs[1])", E=64, h=768, d_ff=3072,
+               N=8192),
+    "c3": dict(name="Switch-Base-128 MoE layer, batch 32 x seq 512 (BASELINE.json configs[2])",
+               E=128, h=768, d_ff=3072, N=16384),
+    "c4": dict(name="Switch-Base-256 MoE layer, batch 32 x seq 512 (BASELINE.json configs[3])",
+               E=256, h=768, d_ff=3072, N=16384),
+    "c5": dict(name="Switch-Large-128 MoE layer, batch 64 x seq 512 (BASELINE.json configs[4])",
+               E=128, h=1024, d_ff=4096, N=32768),
+}
+SEED = {"c2": 2, "c3": 3, "c4": 4, "c5": 5}
+L2_BYTES = 126 * 2**20
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks (NVML, during timed region)
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+def _oracle_weights(cfg, seed, device):
+    import torch
+    import workload as W
+    x = W.make_tokens(seed, cfg["N"], cfg["h"], device=device)
+    w_r = W.make_router_weight(seed, cfg["h"], cfg["E"], device=device)
+    wi, wo = W.make_expert_weights(seed, cfg["E"], cfg["h"], cfg["d_ff"], device=device)
+    to64 = lambda t: t.double().cpu().numpy()
+    return to64(x), to64(w_r), to64(wi), to64(wo)
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if info:
+            return int(max(i["num_threads"] for i in info))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def cpu_baseline(cfg, seed, budget_s=12.0, device="cpu"):
+    """The oracle as it stands, timed on the host cores on a bounded prefix of
+    the same workload (natural router), doubling the sample until ~budget."""
+    import oracle
+    x, w_r, wi, wo = _oracle_weights(cfg, seed, device)
+    n_s, spent, best = 256, 0.0, None
+    while True:
+        t0 = time.perf_counter()
+        oracle.moe_layer(x[:n_s], w_r, wi, wo)
+        dt = time.perf_counter() - t0
+        spent += dt
+        best = (n_s, dt)
+        if n_s >= cfg["N"] or spent + 2.2 * dt > budget_s:
+            break
+        n_s = min(cfg["N"], 2 * n_s)
+    n_s, dt = best
+    return {"value": n_s / dt, "unit": "tokens/s", "cores": _blas_threads(), "kind": "oracle",
+            "sample": f"first {n_s} of {cfg['N']} tokens of the same layer (all {cfg['E']} experts' "
+                      f"weights), fp64 numpy oracle.moe_layer, one call {dt:.2f} s",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args, cfg, seed):
+    """--impl reference: the CPU oracle, rank 0 only, K timed steps of a bounded sample."""
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    x, w_r, wi, wo = _oracle_weights(cfg, seed, dev)
+    # size the per-step sample so W+K steps take ~2 minutes at most
+    t0 = time.perf_counter()
+    oracle.moe_layer(x[:64], w_r, wi, wo)
+    t64 = time.perf_counter() - t0
+    per_step_budget = 120.0 / max(1, args.steps + args.warmup)
+    n_s = 64
+    while n_s < cfg["N"] and t64 * (2 * n_s) / 64 * 0.6 < per_step_budget:
+        n_s *= 2
+    n_s = min(n_s, cfg["N"])
+    N = cfg["N"]
+    for w in range(args.warmup):
+        o = (w * n_s) % N
+        oracle.moe_layer(x[o:o + n_s], w_r, wi, wo)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        o = (k * n_s) % N
+        oracle.moe_layer(x[o:o + n_s], w_r, wi, wo)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = n_s / dt
+    line = {
+        "impl": "reference", "metric": "MoE-layer tokens/s", "value": v, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based normals, workload/)",
+        "config": _config_json(cfg, args, args.gpus),
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": _blas_threads(), "kind": "oracle",
+                         "sample": f"{n_s} consecutive tokens per step of the {N}-token layer"},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_json(cfg, args, G):
+    return {"workload": cfg["name"], "d_model": cfg["h"], "d_ff": cfg["d_ff"], "experts": cfg["E"],
+            "tokens_global": cfg["N"], "tokens_per_rank": cfg["N"] // G, "top_k": 1,
+            "parallelism": f"moeshard expert-sharding x{G} (each rank: 1/{G} of every expert)",
+            "routing": "natural learned-style router (near-uniform); skewed = Zipf(1.2) forced"}
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = CONFIGS[args.config]
+    seed = SEED[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, seed)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import workload as W
+    from paper_2503_08467_b200 import MoEShardLayer, local_token_range, shard_columns
+    from paper_2503_08467_b200.moeshard import PHASES
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
+    G = world
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    if G > 1:
+        dist.init_process_group("nccl", device_id=torch.device(dev))
+    E, h, d_ff, N = cfg["E"], cfg["h"], cfg["d_ff"], cfg["N"]
+    n = N // G
+    t0, t1 = local_token_range(N, G, rank)
+    c0, c1 = shard_columns(d_ff, G, rank)
+    F = d_ff // G
+
+    # weight sets: rotate so a step's weights were evicted from L2 by the previous steps
+    per_set = 2 * E * h * F * 2
+    NW = max(1, math.ceil(3 * L2_BYTES / per_set))
+    layer = MoEShardLayer(h, d_ff, E, n_layers=NW, max_tokens_per_rank=n, dtype=torch.bfloat16,
+                          rank=rank, world=G, device=local)
+    for l in range(NW):
+        wi, wo = W.make_expert_weights(seed, E, h, d_ff, cols=(c0, c1), device=dev, layer=l)
+        layer.load_expert_shards(l, wi, wo)
+        del wi, wo
+    x = W.make_tokens(seed, n, h, device=dev, token_offset=t0)
+    w_r = W.make_router_weight(seed, h, E, device=dev)
+    zipf = W.draw_experts(seed, N, E, "zipf", device=dev, s=1.2)[t0:t1].contiguous()
+    out = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if G > 1:
+            dist.barrier()
+
+    def timed(fn, steps, warmup, sampler=None):
+        for w in range(warmup):
+            fn(w)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if sampler:
+            sampler.__enter__()
+        st.record(stream)
+        for k in range(steps):
+            fn(k)
+        en.record(stream)
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__exit__()
+        barrier()
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en)
+        if G > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms / steps
+
+    fwd = lambda k: layer.forward(k % NW, x, w_r, out=out)
+    fwd_skew = lambda k: layer.forward(k % NW, x, w_r, forced_expert=zipf, out=out)
+
+    # --- main timed region (natural router, near-uniform routing)
+    launches0 = layer.stats()["kernel_launches"]
+    clk = ClockSampler(local)
+    ms = timed(fwd, args.steps, args.warmup, sampler=clk)
+    launches = layer.stats()["kernel_launches"] - launches0
+    st_uniform = layer.stats()
+    r = layer.routing(n)
+    counts = r["counts"].cpu()
+    e_active_u = int((counts > 0).sum())
+    max_tok_u = int(counts.max())
+
+    # --- skewed routing (Zipf 1.2, paper's replaced-router hook)
+    ms_skew = timed(fwd_skew, args.steps, args.warmup)
+    counts_z = layer.routing(n)["counts"].cpu()
+    st_skew = layer.stats()
+
+    # --- per-kernel phase times (separate pass, phase events on the launch stream)
+    layer.profile(True)
+    for k in range(min(args.steps, 1000)):
+        fwd(k)
+    ph, cnt = layer.phase_ms()
+    layer.profile(False)
+    ph_us = {k: 1e3 * v / max(cnt, 1) for k, v in ph.items()}
+
+    # --- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        x_host = x.cpu().pin_memory()
+        y_host = torch.empty_like(x_host).pin_memory()
+        x_dev = torch.empty_like(x)
+        fe = lambda k: layer.forward_host(k % NW, x_host, w_r, x_dev, out, y_host)
+        ms_e2e = timed(fe, args.steps, args.warmup)
+        e2e = {"value": N / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": n * h * 2 * G, "d2h_bytes_per_step": n * h * 2 * G,
+               "path": "MoEShardLayer.forward_host: pinned H2D + moeshard_forward + D2H, per rank"}
+
+    hbm, tf_burst, tf_sust, peak_src = peaks()
+    # algorithmic bytes per launch
+    def gemm_bytes(e_act):
+        w = e_act * h * F * 2
+        return {"gemm_up": w + N * h * 2 + N * F * 2, "gemm_down": w + N * F * 2 + N * h * 2}
+    gb = gemm_bytes(e_active_u)
+    alg = {
+        "router": n * h * 2 + h * E * 2 + n * 8,
+        "grouping": 3 * N * 8 + 2 * N * 4,
+        "gather_rows": 2 * N * h * 2,
+        "gemm_up": gb["gemm_up"],
+        "gemm_down": gb["gemm_down"],
+    }
+    flops = {"gemm_up": 2 * N * h * F, "gemm_down": 2 * N * h * F}
+    kernels = {}
+    for k, us in ph_us.items():
+        d = {"us": round(us, 3)}
+        if k in alg and us > 0:
+            d["GB_s"] = round(alg[k] / (us * 1e-6) / 1e9, 1)
+            d["frac_hbm"] = round(d["GB_s"] / hbm, 4)
+        if k in flops and us > 0:
+            d["TFLOP_s"] = round(flops[k] / (us * 1e-6) / 1e12, 1)
+        kernels[k] = d
+    dom = max(("gemm_up", "gemm_down"), key=lambda k: ph_us[k])
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    achieved = alg[dom] / (ph_us[dom] * 1e-6) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
+                "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)", "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": traffic,
+                "algorithmic_bytes": alg[dom], "launch_us": round(ph_us[dom], 3)}
+    # whole-layer roofline: T_TC, T_HBM (weights + x + partial), T_NV
+    t_tc = 4 * N * h * F / (tf_burst * 1e12) * 1e6
+    t_hbm = (e_active_u * 2 * h * F * 2 + N * h * 2 + N * h * 2) / (hbm * 1e9) * 1e6
+    t_nv = (G - 1) / G * N * h * 4 / 770e9 * 1e6 if G > 1 else 0.0
+    roof3 = max(t_tc, t_hbm, t_nv)
+    layer_roof = {"T_tc_us": round(t_tc, 2), "T_hbm_us": round(t_hbm, 2), "T_nv_us": round(t_nv, 2),
+                  "roof_us": round(roof3, 2), "roof_ns_us": round(max(t_tc, t_nv), 2),
+                  "frac": round(roof3 / (ms * 1e3), 4),
+                  "note": "roof = max(T_tc at bf16 burst peak, T_hbm weights+x+out at measured HBM, "
+                          "T_nv AG+RS bf16 at 770 GB/s measured peer bw); roof_ns = north-star two-term"}
+
+    line = {
+        "metric": "MoE-layer tokens/s", "value": N / (ms * 1e-3), "unit": "tokens/s",
+        "n_gpus": G, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded counter-based normals, workload/); random-init weights",
+        "config": dict(_config_json(cfg, args, G),
+                       l2=f"{NW} rotating weight set(s) of {per_set / 2**20:.0f} MiB/rank "
+                          f"(>= 3x the 126 MB L2 between reuses)"),
+        "routing_uniform": {"experts_active": e_active_u, "max_tokens_per_expert": max_tok_u,
+                            "tiles_up": st_uniform["tiles_up"], "tiles_down": st_uniform["tiles_down"]},
+        "skewed": {"routing": "Zipf(s=1.2) forced", "value": N / (ms_skew * 1e-3),
+                   "ms_per_step": ms_skew, "skew_over_uniform_time": round(ms_skew / ms, 4),
+                   "experts_active": int((counts_z > 0).sum()),
+                   "max_tokens_per_expert": int(counts_z.max()),
+                   "tiles_up": st_skew["tiles_up"], "tiles_down": st_skew["tiles_down"]},
+        "roofline": roofline,
+        "layer_roofline": layer_roof,
+        "kernels_us": kernels,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg, seed, device=dev)
+        except Exception as ex:  # report, never hide
+            line["cpu_baseline"] = {"error": repr(ex)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if G > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

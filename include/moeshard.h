@@ -73,7 +73,7 @@ typedef enum {
 typedef struct {
   int32_t d_model;             /* h; multiple of 128 */
   int32_t d_ff;                /* FULL expert hidden width; d_ff/world multiple of 128 */
-  int32_t n_experts;           /* E, 1 <= E <= 1024 */
+  int32_t n_experts;           /* E, 1 <= E <= 256 */
   int32_t n_layers;            /* number of weight slots (MoE layers) this context serves */
   int32_t max_tokens_per_rank; /* upper bound on n_local */
   int32_t dtype;               /* moeshard_dtype */
@@ -155,8 +155,21 @@ typedef struct {
   int64_t tiles_up;
   int64_t tiles_down;
   int64_t rows_executed_up;   /* sum over tiles of the MMA N (tokens) actually issued */
+  int64_t kernel_launches;    /* cumulative count of this context's kernel launches */
 } moeshard_stats;
 int moeshard_get_stats(moeshard_ctx* ctx, moeshard_stats* out, void* stream);
+
+/* Phase timing (measurement only). enable != 0 starts recording CUDA events
+ * at the phase boundaries of every moeshard_forward (ring of 1024 forwards)
+ * and resets the accumulators; enable == 0 stops. moeshard_get_phase_ms
+ * synchronises and writes into out[0..n) the total milliseconds spent, over
+ * all forwards recorded since enabling, in the phases
+ *   0 router, 1 token/metadata AllGather, 2 grouping (hist+scan+scatter),
+ *   3 row gather (permute), 4 grouped GEMM up, 5 grouped GEMM down,
+ *   6 ReduceScatter
+ * and returns the number of forwards in *count. */
+int moeshard_profile(moeshard_ctx* ctx, int enable);
+int moeshard_get_phase_ms(moeshard_ctx* ctx, float* out, int n, int* count);
 
 /* Synchronise `stream` and report the sticky device error (forced id out of
  * range) and any asynchronous CUDA/NCCL error. */

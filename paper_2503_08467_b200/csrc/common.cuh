@@ -47,11 +47,13 @@ __host__ __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b -
 __host__ __device__ __forceinline__ int round_up(int a, int b) { return ceil_div(a, b) * b; }
 
 // Token chunking of one expert's segment for the tcgen05 tiles: split n_e
-// tokens into ceil(n_e/256) near-equal chunks of a multiple of 16 tokens.
+// tokens into ceil(n_e/256) near-equal chunks of a multiple of 32 tokens
+// (the CTA-pair kernel splits a chunk's rows evenly over the two SMs in
+// 16-row TMA boxes).
 __host__ __device__ __forceinline__ void tc_chunking(int n_e, int* n_chunks, int* chunk) {
   if (n_e <= 0) { *n_chunks = 0; *chunk = 0; return; }
   int c0 = ceil_div(n_e, kTcTokTile);
-  int cs = round_up(ceil_div(n_e, c0), 16);
+  int cs = round_up(ceil_div(n_e, c0), 32);
   *chunk = cs;
   *n_chunks = ceil_div(n_e, cs);
 }

@@ -14,8 +14,9 @@
 //         epilogue: out[perm[t]][c] = bf16(gate[perm[t]] * D)   (gate + un-permute fused, R2)
 //
 // Persistent kernel, one CTA per SM, warp-specialised:
-//   warp 0      TMA producer (one elected lane), STAGES-deep smem ring
-//   warp 1      MMA issuer (one elected lane), double-buffered TMEM accumulator
+//   warp 0      TMA producer of the weight tiles (one lane), A_STAGES-deep ring
+//   warp 3      TMA producer of the token tiles (one lane), B_STAGES-deep ring
+//   warp 1      MMA issuer (one lane), double-buffered TMEM accumulator
 //   warp 2      TMEM allocator
 //   warps 4-7   epilogue: tcgen05.ld -> registers -> global (lane quadrant = warp % 4)
 // Work units (expert e, 128-feature tile mt, token chunk c) are decoded on
@@ -27,6 +28,9 @@
 #include "gemm_tc.cuh"
 #include "ptx.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace moeshard {
 namespace {
 
@@ -36,7 +40,6 @@ constexpr int BM = kTcFeatTile;  // 128
 constexpr int BK = 64;           // 64 bf16 = 128 B = one swizzle atom row
 constexpr int BN_MAX = kTcTokTile;
 constexpr int B_BOX = 32;        // TMA box rows for the token operand
-constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;       // 16 KB
 constexpr int B_BYTES = BN_MAX * BK * 2;   // 32 KB
 constexpr int B_BOX_BYTES = B_BOX * BK * 2;  // 4 KB
@@ -67,19 +70,82 @@ __device__ __forceinline__ Unit decode(int u, int n_mt, int E, const int32_t* pr
   return w;
 }
 
+// Epilogue of one tile: TMEM accumulator (lane = output feature of this
+// warp's 32-feature slice, column = token) -> fused ReLU (up) or gate x (down)
+// -> bf16 -> a per-warp 1 KB shared staging buffer [16 tokens][32 features]
+// -> 16-B vector stores (up: row tok0+j of H; down: un-permute scatter to row
+// perm[tok0+j] of the output). One 16-token chunk at a time.
 template <bool kDown>
+__device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok, int nmma,
+                                           int fbase, uint32_t taddr, int lane, uint64_t pol_keep,
+                                           __nv_bfloat16* stage) {
+  uint16_t* st16 = reinterpret_cast<uint16_t*>(stage);
+  for (int c0 = 0; c0 < nmma; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(taddr + c0, r);
+    tmem_ld_wait();
+    int row = 0;
+    if (kDown) {
+      float g = 0.f;
+      const int tk = c0 + (lane & 15);
+      if (tk < ntok) {
+        row = p.perm[tok0 + tk];
+        g = p.route[row].gate;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float gj = __shfl_sync(0xffffffffu, g, j);
+        const __nv_bfloat16 v = __float2bfloat16_rn(gj * __uint_as_float(r[j]));
+        st16[j * 32 + lane] = *reinterpret_cast<const uint16_t*>(&v);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const __nv_bfloat16 v = __float2bfloat16_rn(fmaxf(__uint_as_float(r[j]), 0.f));
+        st16[j * 32 + lane] = *reinterpret_cast<const uint16_t*>(&v);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int q = lane + 32 * i;  // 64 vectors of 16 B: 16 tokens x 4 parts
+      const int j = q >> 2, part = q & 3;
+      const uint4 v = reinterpret_cast<const uint4*>(stage)[q];
+      if (kDown) {
+        const int rj = __shfl_sync(0xffffffffu, row, j);
+        if (c0 + j < ntok)
+          *reinterpret_cast<uint4*>(p.out + (size_t)rj * p.ld_out + fbase + part * 8) = v;
+      } else if (c0 + j < ntok) {
+        st_v4_hint(p.out + (size_t)(tok0 + c0 + j) * p.ld_out + fbase + part * 8, v, pol_keep);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// kMode (experiments only, MOESHARD_TC_VARIANT 5-10): 0 = normal; 1 = stream A+B, no MMA and
+// no epilogue; 2 = stream A only; 3 = MMA + TMEM reads, no global stores; 4 = MMA, no epilogue;
+// 5 = normal + per-role blocked-time counters printed by CTA 0.
+#define TWAIT(acc, stmt)                        \
+  do {                                          \
+    const long long _t0 = clock64();            \
+    stmt;                                       \
+    acc += clock64() - _t0;                     \
+  } while (0)
+template <bool kDown, int A_STAGES, int B_STAGES, int kMode = 0>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    TcParams p) {
+    tc_grouped_gemm(const __grid_constant__ CUtensorMap tmB, TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for the 128-B swizzle atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sB = smem + A_STAGES * A_BYTES;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + B_STAGES * B_BYTES);
+  uint64_t* emptyA = fullA + A_STAGES;
+  uint64_t* fullB = emptyA + A_STAGES;
+  uint64_t* emptyB = fullB + B_STAGES;
+  uint64_t* tfull = emptyB + B_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int32_t* s_pref = reinterpret_cast<int32_t*>(tmem_slot + 4);
@@ -92,14 +158,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     s_off[i] = p.tb.offsets[i];
     if (i < p.E) s_cs[i] = p.tb.tc_chunk_size[i];
   }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-  }
+  if (warp == 3 && lane == 0) tma_prefetch_desc(&tmB);
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < A_STAGES; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < B_STAGES; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -118,101 +185,136 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nkb = p.K / BK;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ TMA producer
+    {
+      // ------------------------------------------------------------ weight producer
       const uint64_t pol_w = policy_evict_first();  // weights: streamed, shared only by siblings
-      const uint64_t pol_x = policy_evict_last();   // activations: re-read by n_mt tiles
       int stage = 0;
       uint32_t phase = 0;
+      long long t_blk = 0, t_all = clock64();
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
         const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_cs);
-        const int nb = (w.ntok + B_BOX - 1) / B_BOX;
-        const uint32_t bytes = A_BYTES + nb * B_BOX_BYTES;
-        const int arow = w.e * p.rows_per_e + w.mt * BM;
+        const __nv_bfloat16* tiles =
+            p.a_tiles + (static_cast<size_t>(w.e) * n_mt + w.mt) * nkb * (BM * BK);
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_2d(&tmA, &full[stage], sA + stage * A_BYTES, kb * BK, arow, pol_w);
-          for (int i = 0; i < nb; ++i)
-            tma_load_2d(&tmB, &full[stage], sB + stage * B_BYTES + i * B_BOX_BYTES, kb * BK,
-                        w.tok0 + i * B_BOX, pol_x);
-          if (++stage == STAGES) {
+          TWAIT(t_blk, mbar_wait(&emptyA[stage], phase ^ 1));
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&fullA[stage], A_BYTES);
+            bulk_load(sA + stage * A_BYTES, tiles + static_cast<size_t>(kb) * (BM * BK), A_BYTES,
+                      &fullA[stage], pol_w);
+          }
+          __syncwarp();
+          if (++stage == A_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
+      if (kMode == 5 && blockIdx.x == 0 && lane == 0)
+        printf("[A producer] total %lld blocked-on-empty %lld\n", clock64() - t_all, t_blk);
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
+  } else if (warp == 3) {
+    if (kMode != 2) {
+      // ------------------------------------------------------------ token producer
+      const uint64_t pol_x = policy_evict_last();   // activations: re-read by n_mt tiles
       int stage = 0;
       uint32_t phase = 0;
+      long long t_blk = 0, t_all = clock64();
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_cs);
+        const int nb = (w.ntok + B_BOX - 1) / B_BOX;
+        for (int kb = 0; kb < nkb; ++kb) {
+          TWAIT(t_blk, mbar_wait(&emptyB[stage], phase ^ 1));
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&fullB[stage], nb * B_BOX_BYTES);
+            for (int i = 0; i < nb; ++i)
+              tma_load_2d(&tmB, &fullB[stage], sB + stage * B_BYTES + i * B_BOX_BYTES, kb * BK,
+                          w.tok0 + i * B_BOX, pol_x);
+          }
+          __syncwarp();
+          if (++stage == B_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (kMode == 5 && blockIdx.x == 0 && lane == 0)
+        printf("[B producer] total %lld blocked-on-empty %lld\n", clock64() - t_all, t_blk);
+    }
+  } else if (warp == 1) {
+    {
+      // ------------------------------------------------------------ MMA issuer
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
       int as = 0;
       uint32_t aphase = 0;
+      long long t_a = 0, t_b = 0, t_t = 0, t_all = clock64();
+      int units = 0;
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
         const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_cs);
         const int nmma = (w.ntok + 15) & ~15;
         const uint32_t idesc = idesc_bf16_f32(BM, nmma);
-        mbar_wait(&tempty[as], aphase ^ 1);
+        ++units;
+        if (kMode == 0 || kMode == 3 || kMode == 5) TWAIT(t_t, mbar_wait(&tempty[as], aphase ^ 1));
         tc_fence_after();
         const uint32_t d = tmem_base + as * BN_MAX;
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
+          if (kMode != 2) TWAIT(t_b, mbar_wait(&fullB[sb], pb));
+          TWAIT(t_a, mbar_wait(&fullA[sa], pa));
           tc_fence_after();
-          const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + stage * A_BYTES));
-          const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + stage * B_BYTES));
+          const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
+          const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B_BYTES));
+          if (elect_one()) {
+            if (kMode == 0 || kMode >= 3) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma_bf16_ss(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-          mma_commit(&empty[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+              for (int k = 0; k < BK / 16; ++k)
+                mma_bf16_ss(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            }
+            mma_commit(&emptyA[sa]);
+            if (kMode != 2) mma_commit(&emptyB[sb]);
+          }
+          __syncwarp();
+          if (++sa == A_STAGES) {
+            sa = 0;
+            pa ^= 1;
+          }
+          if (++sb == B_STAGES) {
+            sb = 0;
+            pb ^= 1;
           }
         }
-        mma_commit(&tfull[as]);
+        if ((kMode == 0 || kMode == 3 || kMode == 5) && elect_one()) mma_commit(&tfull[as]);
+        __syncwarp();
         as ^= 1;
         if (as == 0) aphase ^= 1;
       }
+      if (kMode == 5 && blockIdx.x == 0 && lane == 0)
+        printf("[MMA] units %d total %lld waitA %lld waitB %lld waitTMEM %lld\n", units,
+               clock64() - t_all, t_a, t_b, t_t);
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && (kMode == 0 || kMode == 3 || kMode == 5)) {
     // -------------------------------------------------------------- epilogue
     const int wq = warp & 3;
+    __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(
+        (reinterpret_cast<uintptr_t>(s_cs + p.E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
+    const uint64_t pol_keep = policy_evict_last();  // H is re-read by the down product
     int as = 0;
     uint32_t aphase = 0;
+    long long t_w = 0, t_all = clock64();
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
       const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_cs);
-      mbar_wait(&tfull[as], aphase);
+      TWAIT(t_w, mbar_wait(&tfull[as], aphase));
       tc_fence_after();
       const int f = w.mt * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * BN_MAX;
-      const int nmma = (w.ntok + 15) & ~15;
-      for (int c0 = 0; c0 < nmma; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(taddr + c0, r);
-        tmem_ld_wait();
-        if (kDown) {
-          int row = 0;
-          float g = 0.f;
-          const int tk = c0 + (lane & 15);
-          if (tk < w.ntok) {
-            row = p.perm[w.tok0 + tk];
-            g = p.route[row].gate;
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int rj = __shfl_sync(0xffffffffu, row, j);
-            const float gj = __shfl_sync(0xffffffffu, g, j);
-            if (c0 + j < w.ntok)
-              p.out[(size_t)rj * p.ld_out + f] = __float2bfloat16_rn(gj * __uint_as_float(r[j]));
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < w.ntok)
-              p.out[(size_t)(w.tok0 + c0 + j) * p.ld_out + f] =
-                  __float2bfloat16_rn(fmaxf(__uint_as_float(r[j]), 0.f));
+      if (kMode == 0 || kMode == 5) {
+        store_tile<kDown>(p, w.tok0, w.ntok, (w.ntok + 15) & ~15, w.mt * BM + wq * 32, taddr, lane,
+                          pol_keep, stage);
+      } else {
+        for (int c0 = 0; c0 < ((w.ntok + 15) & ~15); c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(taddr + c0, r);
+          tmem_ld_wait();
+          if (r[0] == 0x7fc00001u) p.out[f] = __float2bfloat16_rn(0.f);  // keep the loads live
         }
       }
       tc_fence_before();
@@ -221,6 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       as ^= 1;
       if (as == 0) aphase ^= 1;
     }
+    if (kMode == 5 && blockIdx.x == 0 && lane == 0)
+      printf("[epilogue w%d] total %lld waitFull %lld\n", warp, clock64() - t_all, t_w);
   }
 
   tc_fence_before();
@@ -229,31 +333,326 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem_base, TMEM_COLS);
 }
 
-size_t smem_bytes(int E) {
-  return 1024 + STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16 + (3 * E + 2) * 4;
+
+// ===========================================================================
+// CTA-pair variant (cta_group::2): the two CTAs of a cluster own adjacent
+// 128-feature tiles (2p, 2p+1) of the same (expert, token chunk) and run ONE
+// M=256 MMA per k-step issued by the leader. Each CTA stages its own 16 KB
+// weight tile but only HALF of the token tile (N/2 rows): the token bytes an
+// SM must ingest per weight byte are halved, which is what bounds the
+// one-CTA kernel (weights from HBM + tokens from L2 share the per-SM fill
+// bandwidth). Weights are fetched with TMA (no swizzle: the packed tiles are
+// already the swizzled smem image) so the follower's loads can complete on
+// the leader's barriers.
+// ===========================================================================
+constexpr int B2_BOX = 16;                       // token rows per TMA box (2 KB)
+constexpr int B2_BYTES = (BN_MAX / 2) * BK * 2;  // 16 KB: half of a 256-token tile
+
+template <bool kDown, int AS, int BS, bool kTiming = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_grouped_gemm_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + AS * A_BYTES;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + BS * B2_BYTES);
+  uint64_t* emptyA = fullA + AS;
+  uint64_t* fullB = emptyA + AS;
+  uint64_t* emptyB = fullB + BS;
+  uint64_t* tfull = emptyB + BS;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int32_t* s_pref = reinterpret_cast<int32_t*>(tmem_slot + 4);
+  int32_t* s_off = s_pref + (p.E + 1);
+  int32_t* s_cs = s_off + (p.E + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  for (int i = threadIdx.x; i <= p.E; i += kThreads) {
+    s_pref[i] = p.tb.tc_chunk_pref[i];
+    s_off[i] = p.tb.offsets[i];
+    if (i < p.E) s_cs[i] = p.tb.tc_chunk_size[i];
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(&fullA[s], 2);   // leader arrive.expect_tx + follower arrive
+      mbar_init(&emptyA[s], 1);  // leader's multicast commit
+    }
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(&fullB[s], 2);
+      mbar_init(&emptyB[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (in the leader)
+    }
+    fence_mbar_init();
+  }
+  cluster_sync_all();
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_mt = p.n_mt, n_mp = n_mt / 2;
+  const int total = s_pref[p.E] * n_mp;
+  const int nkb = p.K / BK;
+  const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
+
+  if (warp == 0) {
+    {
+      // ------------------------------------------------------------ weight producer (both CTAs)
+      const uint64_t pol_w = policy_evict_first();
+      const uint32_t leader_full = mapa_shared(smem_u32(fullA), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      long long t_blk = 0, t_all = clock64();
+      for (int u = cid; u < total; u += ncl) {
+        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_cs);
+        const int mt = 2 * w.mt + static_cast<int>(rank);
+        const int row0 = ((w.e * n_mt + mt) * nkb) * BM;
+        for (int kb = 0; kb < nkb; ++kb) {
+          TWAIT(t_blk, mbar_wait(&emptyA[stage], phase ^ 1));
+          const uint32_t fb = leader_full + stage * 8;
+          if (elect_one()) {
+            if (leader) mbar_arrive_expect_tx(&fullA[stage], 2 * A_BYTES);
+            else mbar_arrive_cluster(fb);
+            tma_load_2d_2sm(&tmA, fb, sA + stage * A_BYTES, 0, row0 + kb * BM, pol_w);
+          }
+          __syncwarp();
+          if (++stage == AS) { stage = 0; phase ^= 1; }
+        }
+      }
+      if (kTiming && cid == 0 && lane == 0)
+        printf("[2sm A producer r%u] total %lld blocked %lld\n", rank, clock64() - t_all, t_blk);
+    }
+  } else if (warp == 3) {
+    {
+      // ------------------------------------------------------------ token producer (both CTAs)
+      const uint64_t pol_x = policy_evict_last();
+      const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cid; u < total; u += ncl) {
+        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_cs);
+        const int half = ((w.ntok + 31) & ~31) / 2;     // rows per CTA
+        const int nb = half / B2_BOX;
+        const int r0 = w.tok0 + static_cast<int>(rank) * half;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&emptyB[stage], phase ^ 1);
+          const uint32_t fb = leader_full + stage * 8;
+          if (elect_one()) {
+            if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * nb * B2_BOX * BK * 2);
+            else mbar_arrive_cluster(fb);
+            for (int i = 0; i < nb; ++i)
+              tma_load_2d_2sm(&tmB, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
+                              r0 + i * B2_BOX, pol_x);
+          }
+          __syncwarp();
+          if (++stage == BS) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ------------------------------------------------------------ MMA issuer (leader only)
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      int as = 0;
+      uint32_t aphase = 0;
+      long long t_a = 0, t_b = 0, t_t = 0, t_all = clock64();
+      int units = 0;
+      for (int u = cid; u < total; u += ncl) {
+        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_cs);
+        const int nmma = (w.ntok + 31) & ~31;
+        const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
+        ++units;
+        TWAIT(t_t, mbar_wait(&tempty[as], aphase ^ 1));
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * BN_MAX;
+        for (int kb = 0; kb < nkb; ++kb) {
+          TWAIT(t_b, mbar_wait(&fullB[sb], pb));
+          TWAIT(t_a, mbar_wait(&fullA[sa], pa));
+          tc_fence_after();
+          const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
+          const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B2_BYTES));
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_ss_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            mma_commit_2sm(&emptyA[sa], 0x3);
+            mma_commit_2sm(&emptyB[sb], 0x3);
+          }
+          __syncwarp();
+          if (++sa == AS) { sa = 0; pa ^= 1; }
+          if (++sb == BS) { sb = 0; pb ^= 1; }
+        }
+        if (elect_one()) mma_commit_2sm(&tfull[as], 0x3);
+        __syncwarp();
+        as ^= 1;
+        if (as == 0) aphase ^= 1;
+      }
+      if (kTiming && cid == 0 && lane == 0)
+        printf("[2sm MMA] units %d total %lld waitA %lld waitB %lld waitTMEM %lld\n", units,
+               clock64() - t_all, t_a, t_b, t_t);
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue (both CTAs)
+    const int wq = warp & 3;
+    __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(
+        (reinterpret_cast<uintptr_t>(s_cs + p.E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
+    const uint64_t pol_keep = policy_evict_last();
+    const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
+    int as = 0;
+    uint32_t aphase = 0;
+    long long t_w = 0, t_all = clock64();
+    for (int u = cid; u < total; u += ncl) {
+      const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_cs);
+      TWAIT(t_w, mbar_wait(&tfull[as], aphase));
+      tc_fence_after();
+      const int mt = 2 * w.mt + static_cast<int>(rank);
+      const int f = mt * BM + wq * 32 + lane;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * BN_MAX;
+      store_tile<kDown>(p, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
+                        pol_keep, stage);
+      (void)f;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty + as * 8);
+      as ^= 1;
+      if (as == 0) aphase ^= 1;
+    }
+    if (kTiming && cid == 0 && lane == 0 && wq == 0)
+      printf("[2sm epilogue r%u] total %lld waitFull %lld\n", rank, clock64() - t_all, t_w);
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2sm(tmem_base, TMEM_COLS);
 }
 
-template <bool kDown>
-cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcParams& p, int grid,
-                     cudaStream_t s) {
-  const size_t sm = smem_bytes(p.E);
+size_t smem_bytes(int E, int as, int bs) {
+  return 1024 + as * A_BYTES + bs * B_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (3 * E + 2) * 4 +
+         16 + 4 * 1024;
+}
+
+template <bool kDown, int AS, int BS, int kMode = 0>
+cudaError_t launch_v(const CUtensorMap& tmB, const TcParams& p, int grid, cudaStream_t s) {
+  const size_t sm = smem_bytes(p.E, AS, BS);
   static bool attr_set = false;  // per template instance; the library is single-device
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_grouped_gemm<kDown>,
+    cudaError_t e = cudaFuncSetAttribute(tc_grouped_gemm<kDown, AS, BS, kMode>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_bytes(kMaxExperts)));
+                                         static_cast<int>(smem_bytes(kMaxExperts, AS, BS)));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  tc_grouped_gemm<kDown><<<grid, kThreads, sm, s>>>(tmA, tmB, p);
+  tc_grouped_gemm<kDown, AS, BS, kMode><<<grid, kThreads, sm, s>>>(tmB, p);
   return cudaGetLastError();
+}
+
+// ring depths (A stages x 16 KB, B stages x 32 KB); MOESHARD_TC_VARIANT selects for experiments
+int variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOESHARD_TC_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+size_t smem_bytes_2sm(int E, int as, int bs) {
+  return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (3 * E + 2) * 4 +
+         16 + 4 * 1024;
+}
+
+template <bool kDown, int AS, int BS, bool kT = false>
+cudaError_t launch_2sm(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcParams& p, int grid,
+                       cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_grouped_gemm_2sm<kDown, AS, BS, kT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem_bytes_2sm(kMaxExperts, AS, BS)));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  tc_grouped_gemm_2sm<kDown, AS, BS, kT><<<grid & ~1, kThreads, smem_bytes_2sm(p.E, AS, BS), s>>>(
+      tmA, tmB, p);
+  return cudaGetLastError();
+}
+
+template <bool kDown>
+cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmB2,
+                     const TcParams& p, int grid, cudaStream_t s) {
+  if (p.n_mt % 2 == 0 && variant() == 0) return launch_2sm<kDown, 6, 6>(tmA, tmB2, p, grid, s);
+  if (p.n_mt % 2 == 0 && variant() == 11) return launch_2sm<kDown, 6, 6, true>(tmA, tmB2, p, grid, s);
+  if (p.n_mt % 2 == 0 && variant() == 12) return launch_2sm<kDown, 8, 4>(tmA, tmB2, p, grid, s);
+  if (p.n_mt % 2 == 0 && variant() == 13) return launch_2sm<kDown, 9, 3>(tmA, tmB2, p, grid, s);
+  if (p.n_mt % 2 == 0 && variant() == 14) return launch_2sm<kDown, 7, 5>(tmA, tmB2, p, grid, s);
+  if (p.n_mt % 2 == 0 && variant() == 15) return launch_2sm<kDown, 10, 2>(tmA, tmB2, p, grid, s);
+  switch (variant()) {
+    case 1: return launch_v<kDown, 4, 3>(tmB, p, grid, s);
+    case 2: return launch_v<kDown, 4, 4>(tmB, p, grid, s);
+    case 3: return launch_v<kDown, 2, 5>(tmB, p, grid, s);
+    case 4: return launch_v<kDown, 9, 2>(tmB, p, grid, s);
+    case 5: return launch_v<kDown, 4, 4, 1>(tmB, p, grid, s);
+    case 6: return launch_v<kDown, 4, 4, 2>(tmB, p, grid, s);
+    case 8: return launch_v<kDown, 4, 4, 3>(tmB, p, grid, s);
+    case 9: return launch_v<kDown, 4, 4, 4>(tmB, p, grid, s);
+    case 10: return launch_v<kDown, 4, 4, 5>(tmB, p, grid, s);
+    default: return launch_v<kDown, 4, 4>(tmB, p, grid, s);
+  }
 }
 
 }  // namespace
 
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                           const TcParams& p, int grid, cudaStream_t s) {
-  return down ? launch_t<true>(tmA, tmB, p, grid, s) : launch_t<false>(tmA, tmB, p, grid, s);
+                           const CUtensorMap& tmB2, const TcParams& p, int grid, cudaStream_t s) {
+  return down ? launch_t<true>(tmA, tmB, tmB2, p, grid, s)
+              : launch_t<false>(tmA, tmB, tmB2, p, grid, s);
+}
+
+namespace {
+// One CTA per 128 x 64 tile: coalesced read of src[e][kb*64 .. +64][mt*128 .. +128]
+// (rows of M), transpose through shared memory, write the swizzled 16 KB block.
+__global__ void __launch_bounds__(256) pack_a_tiles(const __nv_bfloat16* __restrict__ src,
+                                                    __nv_bfloat16* __restrict__ dst, int K, int M) {
+  __shared__ __nv_bfloat16 t[64][128 + 8];
+  const int mt = blockIdx.x, kb = blockIdx.y, e = blockIdx.z;
+  const int n_mt = M / BM, nkb = K / BK;
+  const __nv_bfloat16* s = src + static_cast<size_t>(e) * K * M;
+  for (int q = threadIdx.x; q < 64 * 16; q += 256) {      // 64 k-rows x 16 chunks of 8 m
+    const int kk = q / 16, c = q % 16;
+    const uint4 v = *reinterpret_cast<const uint4*>(s + static_cast<size_t>(kb * BK + kk) * M +
+                                                    mt * BM + c * 8);
+    *reinterpret_cast<uint4*>(&t[kk][c * 8]) = v;
+  }
+  __syncthreads();
+  __nv_bfloat16* d = dst + ((static_cast<size_t>(e) * n_mt + mt) * nkb + kb) * (BM * BK);
+  for (int q = threadIdx.x; q < BM * 8; q += 256) {       // 128 rows x 8 chunks of 8 k
+    const int r = q / 8, j = q % 8;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = t[j * 8 + i][r];
+    *reinterpret_cast<uint4*>(d + r * BK + ((j ^ (r & 7)) * 8)) = *reinterpret_cast<uint4*>(v);
+  }
+}
+}  // namespace
+
+void launch_pack_a_tiles(const void* src, void* dst, int E, int K, int M, cudaStream_t s) {
+  dim3 grid(M / BM, K / BK, E);
+  pack_a_tiles<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(src),
+                                    static_cast<__nv_bfloat16*>(dst), K, M);
 }
 
 }  // namespace moeshard

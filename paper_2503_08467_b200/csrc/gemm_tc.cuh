@@ -7,10 +7,21 @@
 
 namespace moeshard {
 
+// Weight storage of the tcgen05 path ("A" operand): for every expert e, every
+// 128-row tile mt of the output features and every 64-wide k-block kb, the
+// 128 x 64 bf16 tile A[e][mt*128 + r][kb*64 + c] is stored as one contiguous
+// 16 KB block, rows of 128 B with the 128-B swizzle already applied
+// (16-B chunk j of row r stored at chunk j ^ (r % 8)) - i.e. byte-for-byte
+// the shared-memory image the MMA descriptor expects. Blocks are ordered
+// [e][mt][kb], so one (e, mt) tile row streams as K/64 * 16 KB contiguous
+// bytes: sequential HBM reads, fetched with plain bulk copies.
+//   src [E][K][M] row-major  (w_in_shard: K = h, M = F;  w_out_shard: K = F, M = h)
+void launch_pack_a_tiles(const void* src, void* dst, int E, int K, int M, cudaStream_t s);
+
 struct TcParams {
   int K;              // reduction length: h (up) or F = d_ff/G (down); multiple of 64
   int n_mt;           // output tiles of 128 features: F/128 (up) or h/128 (down)
-  int rows_per_e;     // weight rows per expert in the A tensor map (= n_mt * 128)
+  const __nv_bfloat16* a_tiles;  // packed weight tiles (launch_pack_a_tiles)
   int E;              // experts
   Tables tb;          // device segment tables of the current forward
   __nv_bfloat16* out; // up: H [N][F]; down: out [N or n][h] in global token order
@@ -19,8 +30,20 @@ struct TcParams {
   const RouteRec* route;   // down: gate per global token
 };
 
+// tcgen05 router (router.cu): transposes router_w [h][E] -> wt_r [EP][h] (zero
+// rows E..EP-1), then logits/softmax/top-1 per 128-token CTA.
+// tmX: x [n][h] box {64, 128}; tmW: wt_r [EP][h] box {64, EP}.
+size_t router_tc_smem_bytes(int EP);
+cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, const void* w_r,
+                             void* wt_r, int n, int h, int E, int EP, const int32_t* forced,
+                             RouteRec* out, int32_t* err_flag, cudaStream_t s);
+
 // grid = number of persistent CTAs (normally the SM count).
+//   tmA:  packed weight tiles as a [rows][64] bf16 tensor, box {64, 128}, no swizzle
+//   tmB:  activations [N][K], box {64, 32}, 128-B swizzle   (one-CTA kernel)
+//   tmB2: activations [N][K], box {64, 16}, 128-B swizzle   (CTA-pair kernel)
+// The CTA-pair (cta_group::2) kernel is used when n_mt is even.
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                           const TcParams& p, int grid, cudaStream_t s);
+                           const CUtensorMap& tmB2, const TcParams& p, int grid, cudaStream_t s);
 
 }  // namespace moeshard

@@ -97,7 +97,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D bf16 tensor [outer][inner] (inner contiguous), box [box_outer][64], 128-B swizzle.
 bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-               uint32_t box_outer) {
+               uint32_t box_outer, bool swizzle = true) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -105,7 +105,8 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
   cuuint32_t box[2] = {64, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -114,7 +115,7 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 // Workspace carve-up, shared by moeshard_workspace_size and moeshard_init.
 struct Layout {
-  size_t route, block_hist, block_base, ints, perm, x_all, x_perm, H, partial, total;
+  size_t wt_r, route, block_hist, block_base, ints, perm, x_all, x_perm, H, partial, total;
   int n_ints;
 };
 
@@ -131,6 +132,7 @@ Layout make_layout(const moeshard_config& c, int world) {
     off += align256(bytes);
     return o;
   };
+  L.wt_r = take(static_cast<size_t>(round_up(c.n_experts, 16)) * h * elt);  // W_r^T, padded
   L.route = take(Nmax * sizeof(RouteRec));
   L.block_hist = take(nb * E * 4);
   L.block_base = take(nb * E * 4);
@@ -149,9 +151,9 @@ Layout make_layout(const moeshard_config& c, int world) {
 
 struct LayerW {
   bool loaded = false;
+  CUtensorMap tm_in{}, tm_out{};  // packed weight tiles viewed as [rows][64], box 128 rows
   void* wt_in = nullptr;   // [E][F][h]  (W_i^T shard, K-major for the up product)
   void* wt_out = nullptr;  // [E][h][F]  (W_o^T shard, K-major for the down product)
-  CUtensorMap tm_in{}, tm_out{};
 };
 
 struct moeshard_ctx {
@@ -165,11 +167,22 @@ struct moeshard_ctx {
   int32_t *block_hist = nullptr, *block_base = nullptr, *perm = nullptr;
   Tables tb{};
   void *x_all = nullptr, *x_perm = nullptr, *H = nullptr, *partial = nullptr;
-  CUtensorMap tm_xperm{}, tm_H{};
+  CUtensorMap tm_xperm{}, tm_H{}, tm_xperm16{}, tm_H16{}, tm_wt_r{};
+  void* wt_r = nullptr;
+  int EP = 16;
   std::vector<LayerW> layers;
   ncclComm_t comm = nullptr;
   int last_n = 0;
+  int64_t launches = 0;  // cumulative kernel launches of this context
+  // phase profiling (measurement only)
+  bool prof = false;
+  static constexpr int kRing = 1024, kEv = 8;
+  std::vector<cudaEvent_t> ev;  // kRing * kEv
+  int prof_count = 0;
   std::string err = "no error";
+  void mark(int phase, cudaStream_t s) {
+    if (prof) cudaEventRecord(ev[(prof_count % kRing) * kEv + phase], s);
+  }
 };
 
 namespace {
@@ -317,6 +330,8 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->L = L;
   c->ws = static_cast<char*>(workspace);
   c->route = reinterpret_cast<RouteRec*>(c->ws + L.route);
+  c->wt_r = c->ws + L.wt_r;
+  c->EP = round_up(c->E, 16);
   c->block_hist = reinterpret_cast<int32_t*>(c->ws + L.block_hist);
   c->block_base = reinterpret_cast<int32_t*>(c->ws + L.block_base);
   int32_t* ints = reinterpret_cast<int32_t*>(c->ws + L.ints);
@@ -341,7 +356,10 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   const int Nmax = world * cfg->max_tokens_per_rank;
   if (c->use_tc && Nmax > 0) {
     if (!make_tmap(&c->tm_xperm, c->x_perm, c->h, Nmax, 32) ||
-        !make_tmap(&c->tm_H, c->H, c->F, Nmax, 32)) {
+        !make_tmap(&c->tm_H, c->H, c->F, Nmax, 32) ||
+        !make_tmap(&c->tm_xperm16, c->x_perm, c->h, Nmax, 16) ||
+        !make_tmap(&c->tm_H16, c->H, c->F, Nmax, 16) ||
+        !make_tmap(&c->tm_wt_r, c->wt_r, c->h, c->EP, c->EP)) {
       delete c;
       return fail(nullptr, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
     }
@@ -385,15 +403,20 @@ int moeshard_load_expert_shards(moeshard_ctx* c, int layer, const void* w_in_sha
   LayerW& lw = c->layers[layer];
   lw.wt_in = storage;
   lw.wt_out = static_cast<char*>(storage) + per;
-  // W_i^r [E][h][F] -> [E][F][h];  W_o^r [E][F][h] -> [E][h][F]
-  launch_transpose(c->cfg.dtype, w_in_shard, lw.wt_in, c->E, c->h, c->F, s);
-  launch_transpose(c->cfg.dtype, w_out_shard, lw.wt_out, c->E, c->F, c->h, s);
-  CUDA_TRY(c, cudaGetLastError());
   if (c->use_tc) {
-    if (!make_tmap(&lw.tm_in, lw.wt_in, c->h, static_cast<uint64_t>(c->E) * c->F, 128) ||
-        !make_tmap(&lw.tm_out, lw.wt_out, c->F, static_cast<uint64_t>(c->E) * c->h, 128))
-      return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for weights");
+    // swizzled contiguous 128 x 64 tiles of W_i^T [E][F][h] and W_o^T [E][h][F]
+    launch_pack_a_tiles(w_in_shard, lw.wt_in, c->E, c->h, c->F, s);
+    launch_pack_a_tiles(w_out_shard, lw.wt_out, c->E, c->F, c->h, s);
+    const uint64_t rows = static_cast<uint64_t>(c->E) * c->F * c->h / 64;
+    if (!make_tmap(&lw.tm_in, lw.wt_in, 64, rows, 128, false) ||
+        !make_tmap(&lw.tm_out, lw.wt_out, 64, rows, 128, false))
+      return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for weight tiles");
+  } else {
+    // W_i^r [E][h][F] -> [E][F][h];  W_o^r [E][F][h] -> [E][h][F]
+    launch_transpose(c->cfg.dtype, w_in_shard, lw.wt_in, c->E, c->h, c->F, s);
+    launch_transpose(c->cfg.dtype, w_out_shard, lw.wt_out, c->E, c->F, c->h, s);
   }
+  CUDA_TRY(c, cudaGetLastError());
   lw.loaded = true;
   return MOESHARD_OK;
 }
@@ -419,9 +442,21 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   const ncclDataType_t ndt = c->cfg.dtype == MOESHARD_BF16 ? ncclBfloat16 : ncclFloat32;
   int32_t* err_flag = c->tb.stats + 3;
 
+  c->mark(0, s);
   // Step 1: route local tokens
   RouteRec* my_route = c->route + (c->coll ? static_cast<size_t>(c->rank) * n : 0);
-  launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, err_flag, s);
+  if (c->use_tc) {
+    CUtensorMap tm_x;
+    if (!make_tmap(&tm_x, hidden, h, n, 128))
+      return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden");
+    CUDA_TRY(c, launch_router_tc(tm_x, c->tm_wt_r, router_w, c->wt_r, n, h, E, c->EP, forced,
+                                 my_route, err_flag, s));
+    c->launches += 2;
+  } else {
+    launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, err_flag, s);
+    c->launches += 1;
+  }
+  c->mark(1, s);
   // Steps 2+3: metadata + token scatter (replicate all tokens on all GPUs)
   const void* x_all = hidden;
   if (c->coll) {
@@ -432,29 +467,39 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     NCCL_TRY(c, nccl().GroupEnd());
     x_all = c->x_all;
   }
+  c->mark(2, s);
   // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs
   launch_group(c->route, N, E, c->block_hist, c->block_base, c->tb, F / kTcFeatTile,
                h / kTcFeatTile, c->perm, s);
+  c->mark(3, s);
   launch_gather_rows(x_all, c->perm, N, h * c->elt, c->x_perm, s);
+  c->launches += N <= 65536 ? 2 : 4;
+  c->mark(4, s);
   // Step 4: expert computation, one grouped product per projection
   void* P = c->coll ? c->partial : hidden_out;
   if (c->use_tc) {
-    TcParams up{h, F / kTcFeatTile, F, E, c->tb, static_cast<__nv_bfloat16*>(c->H), F, nullptr,
-                nullptr};
-    CUDA_TRY(c, launch_tc_gemm(false, lw.tm_in, c->tm_xperm, up, c->num_sms, s));
-    TcParams dn{F, h / kTcFeatTile, h, E, c->tb, static_cast<__nv_bfloat16*>(P), h, c->perm,
-                c->route};
-    CUDA_TRY(c, launch_tc_gemm(true, lw.tm_out, c->tm_H, dn, c->num_sms, s));
+    TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
+                static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
+    CUDA_TRY(c, launch_tc_gemm(false, lw.tm_in, c->tm_xperm, c->tm_xperm16, up, c->num_sms, s));
+    c->mark(5, s);
+    TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
+                static_cast<__nv_bfloat16*>(P), h, c->perm, c->route};
+    CUDA_TRY(c, launch_tc_gemm(true, lw.tm_out, c->tm_H, c->tm_H16, dn, c->num_sms, s));
   } else {
     launch_simt_up(c->cfg.dtype, c->x_perm, lw.wt_in, h, F, E, c->tb, c->H, c->num_sms, s);
+    c->mark(5, s);
     launch_simt_down(c->cfg.dtype, c->H, lw.wt_out, F, h, E, c->tb, c->perm, c->route, P,
                      c->num_sms, s);
   }
   CUDA_TRY(c, cudaGetLastError());
+  c->launches += 2;
+  c->mark(6, s);
   // Step 5: gather partial outputs to their owner and sum (aggregateTokens)
   if (c->coll)
     NCCL_TRY(c, nccl().ReduceScatter(P, hidden_out, static_cast<size_t>(n) * h, ndt, ncclSum,
                                      c->comm, s));
+  c->mark(7, s);
+  if (c->prof) c->prof_count++;
   return MOESHARD_OK;
 }
 
@@ -490,6 +535,36 @@ int moeshard_get_stats(moeshard_ctx* c, moeshard_stats* out, void* stream) {
   out->tiles_up = c->last_n ? st[0] : 0;
   out->tiles_down = c->last_n ? st[1] : 0;
   out->rows_executed_up = c->last_n ? st[2] : 0;
+  out->kernel_launches = c->launches;
+  return MOESHARD_OK;
+}
+
+int moeshard_profile(moeshard_ctx* c, int enable) {
+  if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "ctx is NULL");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (enable && c->ev.empty()) {
+    c->ev.resize(moeshard_ctx::kRing * moeshard_ctx::kEv);
+    for (auto& e : c->ev) CUDA_TRY(c, cudaEventCreate(&e));
+  }
+  c->prof = enable != 0;
+  c->prof_count = 0;
+  return MOESHARD_OK;
+}
+
+int moeshard_get_phase_ms(moeshard_ctx* c, float* out, int n, int* count) {
+  if (!c || !out || n < 0) return fail(c, MOESHARD_ERR_INVALID_ARG, "NULL ctx/out or n < 0");
+  const int kEv = moeshard_ctx::kEv;
+  for (int i = 0; i < n; ++i) out[i] = 0.f;
+  const int m = std::min(c->prof_count, moeshard_ctx::kRing);
+  if (count) *count = m;
+  if (m == 0) return MOESHARD_OK;
+  CUDA_TRY(c, cudaEventSynchronize(c->ev[((c->prof_count - 1) % moeshard_ctx::kRing) * kEv + kEv - 1]));
+  for (int f = 0; f < m; ++f)
+    for (int p = 0; p + 1 < kEv && p < n; ++p) {
+      float ms = 0.f;
+      CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev[f * kEv + p], c->ev[f * kEv + p + 1]));
+      out[p] += ms;
+    }
   return MOESHARD_OK;
 }
 
@@ -516,6 +591,7 @@ int moeshard_check(moeshard_ctx* c, void* stream) {
 int moeshard_destroy(moeshard_ctx* c) {
   if (!c) return MOESHARD_OK;
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  for (auto& e : c->ev) cudaEventDestroy(e);
   delete c;
   return MOESHARD_OK;
 }

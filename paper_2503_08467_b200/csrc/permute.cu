@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(1024) group_scan(const int32_t* __restrict__ b
     int nc, cs;
     tc_chunking(run, &nc, &cs);
     s_tc[e] = nc;
-    s_rows[e] = nc > 0 ? (run / cs) * cs + round_up(run % cs, 16) : 0;  // sum of MMA N over chunks
+    s_rows[e] = nc > 0 ? (run / cs) * cs + round_up(run % cs, 32) : 0;  // sum of MMA N over chunks
     s_simt[e] = ceil_div(run, kSimtTokTile);
     tb.counts[e] = run;
     tb.tc_chunk_size[e] = cs;
@@ -222,10 +222,164 @@ __global__ void transpose_kernel(const T* __restrict__ src, T* __restrict__ dst,
   }
 }
 
+
+// Single-CTA fused grouping (N <= kFusedMaxTokens): the three phases of
+// hist / scan / scatter in one launch. 32 warps; warp w owns the contiguous
+// token range [w*span, (w+1)*span) so the stable order is warp-major.
+constexpr int kFusedMaxTokens = 65536;
+
+__device__ __forceinline__ int block_excl_scan_1024(int v, int* s_warp, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int w = s_warp[lane];
+    int wi = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += o;
+    }
+    s_warp[lane] = wi - w;
+    if (lane == 31) s_warp[32] = wi;
+  }
+  __syncthreads();
+  const int res = s_warp[warp] + incl - v;
+  total = s_warp[32];
+  __syncthreads();
+  return res;
+}
+
+__global__ void __launch_bounds__(1024, 1) group_fused(const RouteRec* __restrict__ route, int N,
+                                                       int E, Tables tb, int n_mt_up_tc,
+                                                       int n_mt_down_tc, int32_t* __restrict__ perm) {
+  __shared__ int32_t whist[32][kMaxExperts];
+  __shared__ int32_t s_warp[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 32 * E; i += 1024) whist[i / E][i % E] = 0;
+  __syncthreads();
+  const int span = ceil_div(ceil_div(N, 32), 32) * 32;   // multiple of 32 tokens per warp
+  const int t_begin = warp * span, t_end = min(N, t_begin + span);
+  constexpr int U = 8;  // rounds of 32 tokens loaded together (memory-level parallelism)
+  // phase 1: per-warp histograms (warp-aggregated: one update per distinct expert per round)
+  for (int t0 = t_begin; t0 < t_end; t0 += 32 * U) {
+    int es[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u * 32 + lane;
+      es[u] = t < t_end ? __ldg(&route[t].expert) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned peers = __match_any_sync(0xffffffffu, es[u]);
+      if (es[u] >= 0 && lane == __ffs(peers) - 1) whist[warp][es[u]] += __popc(peers);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // phase 2: totals, tile tables, offsets, per-warp bases
+  const int e = threadIdx.x;
+  int cnt = 0, nc = 0, cs = 0, rows = 0, sc = 0;
+  if (e < E) {
+    for (int w = 0; w < 32; ++w) cnt += whist[w][e];
+    tc_chunking(cnt, &nc, &cs);
+    rows = nc > 0 ? (cnt / cs) * cs + round_up(cnt % cs, 32) : 0;
+    sc = ceil_div(cnt, kSimtTokTile);
+    tb.counts[e] = cnt;
+    tb.tc_chunk_size[e] = cs;
+  }
+  int tot_cnt, tot_tc, tot_sc, tot_rows;
+  const int off = block_excl_scan_1024(cnt, s_warp, tot_cnt);
+  const int tcp = block_excl_scan_1024(nc, s_warp, tot_tc);
+  const int smp = block_excl_scan_1024(sc, s_warp, tot_sc);
+  block_excl_scan_1024(rows, s_warp, tot_rows);
+  if (e < E) {
+    tb.offsets[e] = off;
+    tb.tc_chunk_pref[e] = tcp;
+    tb.simt_chunk_pref[e] = smp;
+    int run = off;
+    for (int w = 0; w < 32; ++w) {
+      const int v = whist[w][e];
+      whist[w][e] = run;
+      run += v;
+    }
+  }
+  if (threadIdx.x == 0) {
+    tb.offsets[E] = tot_cnt;
+    tb.tc_chunk_pref[E] = tot_tc;
+    tb.simt_chunk_pref[E] = tot_sc;
+    tb.stats[0] = tot_tc * n_mt_up_tc;
+    tb.stats[1] = tot_tc * n_mt_down_tc;
+    tb.stats[2] = tot_rows * n_mt_up_tc;
+  }
+  __syncthreads();
+  // phase 3: stable ranks -> perm
+  const unsigned lt = lanemask_lt();
+  for (int t0 = t_begin; t0 < t_end; t0 += 32 * U) {
+    int es[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u * 32 + lane;
+      es[u] = t < t_end ? __ldg(&route[t].expert) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int ee = es[u];
+      const unsigned peers = __match_any_sync(0xffffffffu, ee);
+      if (ee >= 0) perm[whist[warp][ee] + __popc(peers & lt)] = t0 + u * 32 + lane;
+      __syncwarp();
+      if (ee >= 0 && lane == __ffs(peers) - 1) whist[warp][ee] += __popc(peers);
+      __syncwarp();
+    }
+  }
+}
+
+// One warp per destination row, rows_per_warp rows in flight per iteration.
+template <int VPL>  // 16-B vectors per lane per row
+__global__ void __launch_bounds__(256) gather_rows_warp(const uint4* __restrict__ src,
+                                                        const int32_t* __restrict__ perm, int N,
+                                                        int row_vecs, uint4* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int j0 = gw * 2; j0 < N; j0 += nw * 2) {
+    uint4 v[2][VPL];
+    int rows[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int j = j0 + r;
+      rows[r] = j < N ? __ldg(perm + j) : -1;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        if (rows[r] >= 0 && c < row_vecs) v[r][i] = __ldg(src + (size_t)rows[r] * row_vecs + c);
+      }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        if (rows[r] >= 0 && c < row_vecs) dst[(size_t)(j0 + r) * row_vecs + c] = v[r][i];
+      }
+  }
+}
 }  // namespace
 
 void launch_group(const RouteRec* route, int N, int E, int32_t* block_hist, int32_t* block_base,
                   Tables tb, int n_mt_up_tc, int n_mt_down_tc, int32_t* perm, cudaStream_t s) {
+  if (N <= kFusedMaxTokens) {
+    group_fused<<<1, 1024, 0, s>>>(route, N, E, tb, n_mt_up_tc, n_mt_down_tc, perm);
+    return;
+  }
   const int nb = ceil_div(N, kHistChunk);
   if (nb > 0) group_hist<<<nb, kGroupThreads, 0, s>>>(route, N, E, block_hist);
   group_scan<<<1, 1024, 0, s>>>(block_hist, nb, E, block_base, tb, n_mt_up_tc, n_mt_down_tc);
@@ -236,6 +390,21 @@ void launch_gather_rows(const void* x_all, const int32_t* perm, int N, int row_b
                         cudaStream_t s) {
   if (N <= 0) return;
   const int row_vecs = row_bytes / 16;
+  if (row_vecs <= 32 * 8) {
+    const int vpl = ceil_div(row_vecs, 32);
+    int grid = ceil_div(ceil_div(N, 2), 8);            // 8 warps per block, 2 rows per warp
+    if (grid > 148 * 8) grid = 148 * 8;
+    auto* sp = static_cast<const uint4*>(x_all);
+    auto* dp = static_cast<uint4*>(x_perm);
+    switch (vpl) {
+      case 1: gather_rows_warp<1><<<grid, 256, 0, s>>>(sp, perm, N, row_vecs, dp); return;
+      case 2: gather_rows_warp<2><<<grid, 256, 0, s>>>(sp, perm, N, row_vecs, dp); return;
+      case 3: gather_rows_warp<3><<<grid, 256, 0, s>>>(sp, perm, N, row_vecs, dp); return;
+      case 4: gather_rows_warp<4><<<grid, 256, 0, s>>>(sp, perm, N, row_vecs, dp); return;
+      case 5: case 6: gather_rows_warp<6><<<grid, 256, 0, s>>>(sp, perm, N, row_vecs, dp); return;
+      default: gather_rows_warp<8><<<grid, 256, 0, s>>>(sp, perm, N, row_vecs, dp); return;
+    }
+  }
   const long long total = (long long)N * row_vecs;
   int grid = (int)((total + 4LL * 256 - 1) / (4LL * 256));
   if (grid > 148 * 16) grid = 148 * 16;

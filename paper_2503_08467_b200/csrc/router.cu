@@ -4,6 +4,12 @@
 // probability of the chosen expert (R2). Optional forced expert ids (the
 // paper's replaced router).
 //
+// Two implementations:
+//  * router_tc_kernel (bf16, the product path; bottom of this file): tcgen05
+//    logits on the tensor cores, token on the TMEM lane axis;
+//  * router_kernel (fp32 validation mode, and bf16 with MOESHARD_FLAG_SIMT_GEMM):
+//    FFMA on CUDA cores, described next.
+//
 // Layout: x [n][h] row-major (bf16 or fp32), W_r [h][E] row-major.
 // One CTA = 64 tokens x all E experts. 256 threads = 16 token groups (ty) x
 // 16 expert lanes (tx); thread (ty, tx) owns tokens ty*4+i and experts
@@ -169,6 +175,194 @@ void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int 
   else
     launch_router_t(static_cast<const float*>(x), n, h, static_cast<const float*>(w_r), E, forced,
                     out, err_flag, s);
+}
+
+}  // namespace moeshard
+
+// ===========================================================================
+// tcgen05 router (bf16): logits for 128 tokens x EP experts per CTA on the
+// tensor cores. A = x tile [128 tok][h] (TMA, K-major, 128-B swizzle),
+// B = W_r^T [EP][h] (transposed + zero-padded once per forward into the
+// workspace by router_transpose, TMA). D[t][e] lives in TMEM with the token
+// on the lane axis, so each epilogue thread owns one token's whole logit row
+// and computes max / argmax (lowest index) / sum-exp sequentially - no
+// cross-thread reduction at all.
+// ===========================================================================
+#include "ptx.cuh"
+
+namespace moeshard {
+namespace {
+
+constexpr int RTC_STAGES = 3;
+constexpr int RTC_A_BYTES = 128 * 128;  // 128 tokens x 64 k x 2 B
+
+__global__ void router_transpose(const __nv_bfloat16* __restrict__ w_r, int h, int E, int EP,
+                                 __nv_bfloat16* __restrict__ wt) {
+  __shared__ __nv_bfloat16 tile[32][34];
+  const int k0 = blockIdx.x * 32, e0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int k = k0 + i, e = e0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < h && e < E) ? w_r[(size_t)k * E + e] : __float2bfloat16_rn(0.f);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int e = e0 + i, k = k0 + threadIdx.x;
+    if (e < EP && k < h) wt[(size_t)e * h + k] = tile[threadIdx.x][i];
+  }
+}
+
+__global__ void __launch_bounds__(192, 1)
+    router_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                     int n, int h, int E, int EP, const int32_t* __restrict__ forced,
+                     RouteRec* __restrict__ out, int32_t* __restrict__ err_flag) {
+  using namespace ptx;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int b_bytes = EP * 128;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + RTC_STAGES * RTC_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + RTC_STAGES * b_bytes);
+  uint64_t* empty = full + RTC_STAGES;
+  uint64_t* done = empty + RTC_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ncols = EP <= 32 ? 32 : EP <= 64 ? 64 : EP <= 128 ? 128 : 256;
+
+  if (warp == 4 && lane == 0) {
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmW);
+    for (int s = 0; s < RTC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, ncols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int tok0 = blockIdx.x * 128;
+  const int nkb = h / 64;
+
+  if (warp == 4) {
+    {  // TMA producer (warp-uniform loop, one elected lane issues)
+      const uint64_t pol_x = policy_evict_first();
+      const uint64_t pol_w = policy_evict_last();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&full[s], RTC_A_BYTES + b_bytes);
+          tma_load_2d(&tmX, &full[s], sA + s * RTC_A_BYTES, kb * 64, tok0, pol_x);
+          tma_load_2d(&tmW, &full[s], sB + s * b_bytes, kb * 64, 0, pol_w);  // box = EP rows
+        }
+        __syncwarp();
+        if (++s == RTC_STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 5) {
+    {  // MMA issuer (warp-uniform loop, one elected lane issues)
+      const uint32_t idesc = idesc_bf16_f32(128, EP);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + s * RTC_A_BYTES));
+        const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + s * b_bytes));
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          mma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == RTC_STAGES) { s = 0; ph ^= 1; }
+      }
+      if (elect_one()) mma_commit(done);
+      __syncwarp();
+    }
+  } else {
+    // epilogue: warps 0-3, thread = token (TMEM lane 32*warp + lane)
+    const int t = tok0 + warp * 32 + lane;
+    int sel = -1;
+    bool bad = false;
+    if (forced != nullptr && t < n) {
+      sel = forced[t];
+      if (sel < 0 || sel >= E) {
+        bad = true;
+        sel = sel < 0 ? 0 : E - 1;
+      }
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    float best = -INFINITY, lsel = 0.f;
+    int best_e = 0;
+    for (int c0 = 0; c0 < EP; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld16(taddr + c0, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int e = c0 + j;
+        const float v = __uint_as_float(r[j]);
+        if (e < E && v > best) {  // strict: the lowest index wins ties (R4)
+          best = v;
+          best_e = e;
+        }
+        if (e == sel) lsel = v;
+      }
+    }
+    float sum = 0.f;
+    for (int c0 = 0; c0 < EP; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld16(taddr + c0, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < E) sum += expf(__uint_as_float(r[j]) - best);
+    }
+    if (t < n) {
+      RouteRec rec;
+      rec.expert = sel >= 0 ? sel : best_e;
+      rec.gate = (sel >= 0 ? expf(lsel - best) : 1.f) / sum;
+      out[t] = rec;
+      if (bad) atomicExch(err_flag, 1);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem, ncols);
+}
+
+}  // namespace
+
+size_t router_tc_smem_bytes(int EP) {
+  return 1024 + RTC_STAGES * (RTC_A_BYTES + EP * 128) + (2 * RTC_STAGES + 1) * 8 + 16;
+}
+
+cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, const void* w_r,
+                             void* wt_r, int n, int h, int E, int EP, const int32_t* forced,
+                             RouteRec* out, int32_t* err_flag, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
+  router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,
+                                     static_cast<__nv_bfloat16*>(wt_r));
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(router_tc_smem_bytes(256)));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  router_tc_kernel<<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP), s>>>(tmX, tmW, n, h, E, EP,
+                                                                        forced, out, err_flag);
+  return cudaGetLastError();
 }
 
 }  // namespace moeshard

@@ -135,6 +135,22 @@ class MoEShardLayer:
     def stats(self) -> dict:
         return C.moeshard_get_stats(self.ctx, self._stream())
 
+    def profile(self, enable: bool = True):
+        C.moeshard_profile(self.ctx, enable)
+
+    def phase_ms(self):
+        return C.moeshard_get_phase_ms(self.ctx)
+
+    def forward_host(self, layer: int, hidden_host: torch.Tensor, router_w: torch.Tensor,
+                     dev_in: torch.Tensor, dev_out: torch.Tensor, host_out: torch.Tensor,
+                     forced_expert: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """End-to-end call with HOST buffers: H2D copy of the tokens (pinned),
+        the forward, D2H copy of the result - all enqueued on the current stream."""
+        dev_in.copy_(hidden_host, non_blocking=True)
+        self.forward(layer, dev_in, router_w, forced_expert=forced_expert, out=dev_out)
+        host_out.copy_(dev_out, non_blocking=True)
+        return host_out
+
     def check(self):
         C.moeshard_check(self.ctx, self._stream())
 

@@ -33,8 +33,10 @@ EXPORTS = [
     "moeshard_get_unique_id", "moeshard_workspace_size", "moeshard_weight_storage_size",
     "moeshard_init", "moeshard_load_expert_shards", "moeshard_forward", "moeshard_get_routing",
     "moeshard_get_stats", "moeshard_check", "moeshard_last_error", "moeshard_status_string",
-    "moeshard_destroy", "moeshard_version",
+    "moeshard_destroy", "moeshard_version", "moeshard_profile", "moeshard_get_phase_ms",
 ]
+PHASES = ["router", "allgather", "grouping", "gather_rows", "gemm_up", "gemm_down",
+          "reduce_scatter"]
 
 
 class MoEShardError(RuntimeError):
@@ -53,7 +55,8 @@ class moeshard_config(ctypes.Structure):
 
 class moeshard_stats(ctypes.Structure):
     _fields_ = [("n_tokens_global", ctypes.c_int64), ("tiles_up", ctypes.c_int64),
-                ("tiles_down", ctypes.c_int64), ("rows_executed_up", ctypes.c_int64)]
+                ("tiles_down", ctypes.c_int64), ("rows_executed_up", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64)]
 
 
 def _nccl_lib_path() -> Optional[str]:
@@ -91,6 +94,9 @@ def load_library() -> ctypes.CDLL:
         "moeshard_status_string": ([i32], ctypes.c_char_p),
         "moeshard_destroy": ([vp], i32),
         "moeshard_version": ([], ctypes.c_char_p),
+        "moeshard_profile": ([vp, i32], i32),
+        "moeshard_get_phase_ms": ([vp, ctypes.POINTER(ctypes.c_float), i32,
+                                   ctypes.POINTER(ctypes.c_int)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -169,3 +175,15 @@ def moeshard_destroy(ctx):
 
 def moeshard_last_error(ctx=None) -> str:
     return _lib.moeshard_last_error(ctx).decode()
+
+
+def moeshard_profile(ctx, enable: bool):
+    _check(_lib.moeshard_profile(ctx, 1 if enable else 0), ctx)
+
+
+def moeshard_get_phase_ms(ctx):
+    """({phase: total ms}, number of forwards) since profiling was enabled."""
+    buf = (ctypes.c_float * len(PHASES))()
+    cnt = ctypes.c_int()
+    _check(_lib.moeshard_get_phase_ms(ctx, buf, len(PHASES), ctypes.byref(cnt)), ctx)
+    return {k: float(buf[i]) for i, k in enumerate(PHASES)}, cnt.value

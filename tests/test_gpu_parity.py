@@ -112,8 +112,8 @@ def test_bf16_tcgen05_parity(N, h, d_ff, E, routing):
     _check_layer(inp, y, r, tol=BF16_TOL)
     st = L.stats()
     assert st["n_tokens_global"] == N
-    # tile accounting: tokens padded to multiples of 16 per chunk, never more than 15 per chunk
-    assert N <= st["rows_executed_up"] // (d_ff // 128) <= N + 15 * st["tiles_up"] // (d_ff // 128)
+    # tile accounting: tokens padded to multiples of 32 per chunk, never more than 31 per chunk
+    assert N <= st["rows_executed_up"] // (d_ff // 128) <= N + 31 * st["tiles_up"] // (d_ff // 128)
 
 
 def test_bf16_natural_routing_with_ambiguity_rule():
