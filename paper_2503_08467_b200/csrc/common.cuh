@@ -12,7 +12,6 @@
 namespace moeshard {
 
 constexpr int kMaxExperts = 256;      // router instantiations cover E <= 256
-constexpr int kHistChunk = 1024;      // tokens per block in the histogram / scatter kernels
 constexpr int kTcTokTile = 256;       // max tokens per tcgen05 tile (UMMA N <= 256)
 constexpr int kTcFeatTile = 128;      // weight rows per tcgen05 tile (UMMA M)
 constexpr int kSimtTokTile = 64;      // tokens per SIMT tile
@@ -65,14 +64,16 @@ __host__ __device__ __forceinline__ void tc_chunking(int n_e, int* n_chunks, int
 // ---------------------------------------------------------------------------
 namespace moeshard {
 
+// SIMT router (fp32 mode / ablation): 64-token CTAs; hist_out [ceil(n/64)][E] per-block counts.
 void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int E,
-                   const int32_t* forced, RouteRec* out, int32_t* err_flag, cudaStream_t s);
+                   const int32_t* forced, RouteRec* out, int32_t* hist_out, int32_t* err_flag,
+                   cudaStream_t s);
 
-void launch_group(const RouteRec* route, int N, int E, int32_t* block_hist, int32_t* block_base,
-                  Tables tb, int n_out_up, int n_out_down, int32_t* perm, cudaStream_t s);
-
-void launch_gather_rows(const void* x_all, const int32_t* perm, int N, int row_bytes, void* x_perm,
-                        cudaStream_t s);
+// Step 2 from the routers' per-block histograms, one launch: one CTA per
+// hist-block of HB <= 128 tokens (offsets, stable scatter, row gather).
+void launch_group_blocks(const int32_t* hist, int NB, int E, Tables tb, int n_mt_up_tc,
+                         int n_mt_down_tc, const RouteRec* route, const void* x_all, int n, int nbr,
+                         int HB, int row_bytes, int32_t* perm, void* x_perm, cudaStream_t s);
 
 void launch_transpose(int dtype, const void* src, void* dst, int batch, int rows, int cols,
                       cudaStream_t s);

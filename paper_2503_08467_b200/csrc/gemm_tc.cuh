@@ -30,13 +30,16 @@ struct TcParams {
   const RouteRec* route;   // down: gate per global token
 };
 
-// tcgen05 router (router.cu): transposes router_w [h][E] -> wt_r [EP][h] (zero
-// rows E..EP-1), then logits/softmax/top-1 per 128-token CTA.
-// tmX: x [n][h] box {64, 128}; tmW: wt_r [EP][h] box {64, EP}.
-size_t router_tc_smem_bytes(int EP);
-cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, const void* w_r,
-                             void* wt_r, int n, int h, int E, int EP, const int32_t* forced,
-                             RouteRec* out, int32_t* err_flag, cudaStream_t s);
+// tcgen05 router (router.cu): logits/softmax/top-1 per 128-token CTA, plus the
+// CTA's per-expert token histogram hist_out[blockIdx][E].
+// tmX: x [n][h] box {64, 128}. mn_major: tmW = router_w [h][E] box {64 experts, 64 k}
+// (E % 8 == 0); else router_w is first transposed to wt_r [EP][h] (zero rows E..EP-1)
+// and tmW = wt_r box {64, EP}.
+size_t router_tc_smem_bytes(int EP, bool mn_major);
+cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
+                             const void* w_r, void* wt_r, int n, int h, int E, int EP,
+                             const int32_t* forced, RouteRec* out, int32_t* hist_out,
+                             int32_t* err_flag, cudaStream_t s);
 
 // grid = number of persistent CTAs (normally the SM count).
 //   tmA:  packed weight tiles as a [rows][64] bf16 tensor, box {64, 128}, no swizzle

@@ -9,7 +9,8 @@
 //   1 router kernel (local tokens)                          Step 1
 //   2 ncclGroup{ AllGather(tokens), AllGather(route recs) }  Steps 2+3 (metadata folded
 //                                                           into the token exchange)
-//   3 group_hist / group_scan / group_scatter / gather_rows Step 2 grouping + Sec. 3.3
+//   3 group_scatter_gather (router-emitted per-block         Step 2 grouping + Sec. 3.3
+//     histograms -> offsets, stable perm, X_perm)
 //                                                           cross-GPU per-expert concat
 //   4 grouped GEMM up (+ReLU), grouped GEMM down (+gate,    Step 4 (Sec. 3.3 fusion)
 //     +un-permute scatter)
@@ -123,7 +124,8 @@ Layout make_layout(const moeshard_config& c, int world) {
   const bool coll = world > 1 || (c.flags & MOESHARD_FLAG_FORCE_COLLECTIVES);
   const size_t elt = c.dtype == MOESHARD_BF16 ? 2 : 4;
   const size_t Nmax = static_cast<size_t>(world) * c.max_tokens_per_rank;
-  const size_t nb = std::max<size_t>(1, (Nmax + kHistChunk - 1) / kHistChunk);
+  // hist-blocks: >= 64 tokens each (128 for the tcgen05 router), per rank
+  const size_t nb = std::max<size_t>(1, world * ((c.max_tokens_per_rank + 63) / 64));
   const size_t E = c.n_experts, h = c.d_model, F = c.d_ff / world;
   Layout L{};
   size_t off = 0;
@@ -436,7 +438,6 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const LayerW& lw = c->layers[layer];
   const int h = c->h, F = c->F, E = c->E;
-  const int N = c->coll ? c->world * n : n;
   c->last_n = n;
   if (n == 0) return MOESHARD_OK;
   const ncclDataType_t ndt = c->cfg.dtype == MOESHARD_BF16 ? ncclBfloat16 : ncclFloat32;
@@ -445,15 +446,21 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   c->mark(0, s);
   // Step 1: route local tokens
   RouteRec* my_route = c->route + (c->coll ? static_cast<size_t>(c->rank) * n : 0);
+  const int HB = c->use_tc ? 128 : 64;                 // tokens per hist-block
+  const int nbr = (n + HB - 1) / HB;                    // hist-blocks per rank
+  const int NB = (c->coll ? c->world : 1) * nbr;
+  int32_t* my_hist = c->block_hist + (c->coll ? static_cast<size_t>(c->rank) * nbr * E : 0);
   if (c->use_tc) {
-    CUtensorMap tm_x;
-    if (!make_tmap(&tm_x, hidden, h, n, 128))
-      return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden");
-    CUDA_TRY(c, launch_router_tc(tm_x, c->tm_wt_r, router_w, c->wt_r, n, h, E, c->EP, forced,
-                                 my_route, err_flag, s));
-    c->launches += 2;
+    CUtensorMap tm_x, tm_w;
+    const bool mn = (E % 8) == 0;
+    if (!make_tmap(&tm_x, hidden, h, n, 128) ||
+        (mn && !make_tmap(&tm_w, router_w, E, h, 64)))
+      return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden/router_w");
+    CUDA_TRY(c, launch_router_tc(tm_x, mn ? tm_w : c->tm_wt_r, mn, router_w, c->wt_r, n, h, E,
+                                 c->EP, forced, my_route, my_hist, err_flag, s));
+    c->launches += mn ? 1 : 2;
   } else {
-    launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, err_flag, s);
+    launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, my_hist, err_flag, s);
     c->launches += 1;
   }
   c->mark(1, s);
@@ -464,16 +471,17 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     NCCL_TRY(c, nccl().AllGather(hidden, c->x_all, static_cast<size_t>(n) * h, ndt, c->comm, s));
     NCCL_TRY(c, nccl().AllGather(my_route, c->route, static_cast<size_t>(n) * 2, ncclInt32,
                                  c->comm, s));
+    NCCL_TRY(c, nccl().AllGather(my_hist, c->block_hist, static_cast<size_t>(nbr) * E, ncclInt32,
+                                 c->comm, s));
     NCCL_TRY(c, nccl().GroupEnd());
     x_all = c->x_all;
   }
   c->mark(2, s);
   // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs
-  launch_group(c->route, N, E, c->block_hist, c->block_base, c->tb, F / kTcFeatTile,
-               h / kTcFeatTile, c->perm, s);
+  launch_group_blocks(c->block_hist, NB, E, c->tb, F / kTcFeatTile, h / kTcFeatTile, c->route,
+                      x_all, n, nbr, HB, h * c->elt, c->perm, c->x_perm, s);
+  c->launches += 1;
   c->mark(3, s);
-  launch_gather_rows(x_all, c->perm, N, h * c->elt, c->x_perm, s);
-  c->launches += N <= 65536 ? 2 : 4;
   c->mark(4, s);
   // Step 4: expert computation, one grouped product per projection
   void* P = c->coll ? c->partial : hidden_out;

@@ -50,12 +50,15 @@ __global__ void __launch_bounds__(256) router_kernel(const T* __restrict__ x, in
                                                      const T* __restrict__ w_r, int E,
                                                      const int32_t* __restrict__ forced,
                                                      RouteRec* __restrict__ out,
+                                                     int32_t* __restrict__ hist_out,
                                                      int32_t* __restrict__ err_flag) {
   constexpr int EP = EPT * 16;                 // padded expert count handled by this instantiation
   __shared__ __align__(16) float xs[RT_KC][RT_TOK + 4];
   __shared__ __align__(16) float ws[RT_KC][EP];
+  __shared__ int32_t s_hist[kMaxExperts];
 
   const int tid = threadIdx.x;
+  for (int e = tid; e < E; e += 256) s_hist[e] = 0;
   const int tx = tid & 15, ty = tid >> 4;
   const int tok0 = blockIdx.x * RT_TOK;
 
@@ -148,33 +151,37 @@ __global__ void __launch_bounds__(256) router_kernel(const T* __restrict__ x, in
       r.expert = sel;
       r.gate = expf(lsel - best) / sum;
       out[t] = r;
+      atomicAdd(&s_hist[sel], 1);
       if (bad) atomicExch(err_flag, 1);
     }
   }
+  __syncthreads();
+  for (int e = tid; e < E; e += 256) hist_out[(size_t)blockIdx.x * E + e] = s_hist[e];
 }
 
 template <typename T>
 void launch_router_t(const T* x, int n, int h, const T* w_r, int E, const int32_t* forced,
-                     RouteRec* out, int32_t* err, cudaStream_t s) {
+                     RouteRec* out, int32_t* hist, int32_t* err, cudaStream_t s) {
   if (n <= 0) return;
   dim3 grid(ceil_div(n, RT_TOK));
-  if (E <= 16) router_kernel<T, 1><<<grid, 256, 0, s>>>(x, n, h, w_r, E, forced, out, err);
-  else if (E <= 32) router_kernel<T, 2><<<grid, 256, 0, s>>>(x, n, h, w_r, E, forced, out, err);
-  else if (E <= 64) router_kernel<T, 4><<<grid, 256, 0, s>>>(x, n, h, w_r, E, forced, out, err);
-  else if (E <= 128) router_kernel<T, 8><<<grid, 256, 0, s>>>(x, n, h, w_r, E, forced, out, err);
-  else router_kernel<T, 16><<<grid, 256, 0, s>>>(x, n, h, w_r, E, forced, out, err);
+  if (E <= 16) router_kernel<T, 1><<<grid, 256, 0, s>>>(x, n, h, w_r, E, forced, out, hist, err);
+  else if (E <= 32) router_kernel<T, 2><<<grid, 256, 0, s>>>(x, n, h, w_r, E, forced, out, hist, err);
+  else if (E <= 64) router_kernel<T, 4><<<grid, 256, 0, s>>>(x, n, h, w_r, E, forced, out, hist, err);
+  else if (E <= 128) router_kernel<T, 8><<<grid, 256, 0, s>>>(x, n, h, w_r, E, forced, out, hist, err);
+  else router_kernel<T, 16><<<grid, 256, 0, s>>>(x, n, h, w_r, E, forced, out, hist, err);
 }
 
 }  // namespace
 
 void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int E,
-                   const int32_t* forced, RouteRec* out, int32_t* err_flag, cudaStream_t s) {
+                   const int32_t* forced, RouteRec* out, int32_t* hist_out, int32_t* err_flag,
+                   cudaStream_t s) {
   if (dtype == 0)
     launch_router_t(static_cast<const __nv_bfloat16*>(x), n, h,
-                    static_cast<const __nv_bfloat16*>(w_r), E, forced, out, err_flag, s);
+                    static_cast<const __nv_bfloat16*>(w_r), E, forced, out, hist_out, err_flag, s);
   else
     launch_router_t(static_cast<const float*>(x), n, h, static_cast<const float*>(w_r), E, forced,
-                    out, err_flag, s);
+                    out, hist_out, err_flag, s);
 }
 
 }  // namespace moeshard
@@ -188,12 +195,17 @@ void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int 
 // and computes max / argmax (lowest index) / sum-exp sequentially - no
 // cross-thread reduction at all.
 // ===========================================================================
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
 #include "ptx.cuh"
 
 namespace moeshard {
 namespace {
 
-constexpr int RTC_STAGES = 3;
+constexpr int RTC_MAX_STAGES = 8;
+constexpr int RTC_SMEM_BUDGET = 200 * 1024;
 constexpr int RTC_A_BYTES = 128 * 128;  // 128 tokens x 64 k x 2 B
 
 __global__ void router_transpose(const __nv_bfloat16* __restrict__ w_r, int h, int E, int EP,
@@ -211,15 +223,23 @@ __global__ void router_transpose(const __nv_bfloat16* __restrict__ w_r, int h, i
   }
 }
 
+// kMN: B = router_w [h][E] read directly (MN-major, 64-expert x 64-k TMA boxes);
+// otherwise B = the transposed copy [EP][h] (K-major).
+template <bool kMN, bool kT = false>
 __global__ void __launch_bounds__(192, 1)
     router_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      int n, int h, int E, int EP, const int32_t* __restrict__ forced,
-                     RouteRec* __restrict__ out, int32_t* __restrict__ err_flag) {
+                     RouteRec* __restrict__ out, int32_t* __restrict__ hist_out,
+                     int32_t* __restrict__ err_flag) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  const int b_bytes = EP * 128;
+  const int n_atoms = (EP + 63) / 64;
+  const int b_bytes = kMN ? n_atoms * 8192 : EP * 128;
+  __shared__ int32_t s_hist[kMaxExperts];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
+  const int RTC_STAGES = min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (RTC_A_BYTES + b_bytes));
   uint8_t* sA = smem;
   uint8_t* sB = smem + RTC_STAGES * RTC_A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + RTC_STAGES * b_bytes);
@@ -239,11 +259,13 @@ __global__ void __launch_bounds__(192, 1)
     mbar_init(done, 1);
     fence_mbar_init();
   }
+  const long long t_start = clock64();
   if (warp == 0) tmem_alloc(tmem_slot, ncols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const long long t_setup = clock64();
   const int tok0 = blockIdx.x * 128;
   const int nkb = h / 64;
 
@@ -258,7 +280,12 @@ __global__ void __launch_bounds__(192, 1)
         if (elect_one()) {
           mbar_arrive_expect_tx(&full[s], RTC_A_BYTES + b_bytes);
           tma_load_2d(&tmX, &full[s], sA + s * RTC_A_BYTES, kb * 64, tok0, pol_x);
-          tma_load_2d(&tmW, &full[s], sB + s * b_bytes, kb * 64, 0, pol_w);  // box = EP rows
+          if (kMN) {
+            for (int a = 0; a < n_atoms; ++a)
+              tma_load_2d(&tmW, &full[s], sB + s * b_bytes + a * 8192, a * 64, kb * 64, pol_w);
+          } else {
+            tma_load_2d(&tmW, &full[s], sB + s * b_bytes, kb * 64, 0, pol_w);  // box = EP rows
+          }
         }
         __syncwarp();
         if (++s == RTC_STAGES) { s = 0; ph ^= 1; }
@@ -266,17 +293,20 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else if (warp == 5) {
     {  // MMA issuer (warp-uniform loop, one elected lane issues)
-      const uint32_t idesc = idesc_bf16_f32(128, EP);
+      const uint32_t idesc = idesc_bf16_f32(128, EP, kMN);
       int s = 0;
       uint32_t ph = 0;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + s * RTC_A_BYTES));
-        const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + s * b_bytes));
+        const uint64_t bd = kMN ? smem_desc_mn_sw128(smem_u32(sB + s * b_bytes), 8192)
+                                : smem_desc_k_sw128(smem_u32(sB + s * b_bytes));
+        const uint32_t bstep = kMN ? 128 : 2;   // K=16 step: 16 rows x 128 B (MN) or 32 B (K)
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          for (int k = 0; k < 4; ++k)
+            mma_bf16_ss(tmem, ad + 2 * k, bd + bstep * k, idesc, (kb | k) != 0);
           mma_commit(&empty[s]);
         }
         __syncwarp();
@@ -299,40 +329,56 @@ __global__ void __launch_bounds__(192, 1)
     }
     mbar_wait(done, 0);
     tc_fence_after();
+    const long long t_done = clock64();
     const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    float best = -INFINITY, lsel = 0.f;
+    // one pass over the logit row (32 columns per TMEM load): running max /
+    // argmax (strict '>' in ascending column order = lowest index on ties, R4)
+    // and online sum of exp(l - max), rescaled when the max moves.
+    constexpr float kLog2e = 1.4426950408889634f;
+    float best = -INFINITY, lsel = 0.f, sum = 0.f;
     int best_e = 0;
-    for (int c0 = 0; c0 < EP; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld16(taddr + c0, r);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int e = c0 + j;
-        const float v = __uint_as_float(r[j]);
-        if (e < E && v > best) {  // strict: the lowest index wins ties (R4)
-          best = v;
-          best_e = e;
-        }
-        if (e == sel) lsel = v;
+    for (int c0 = 0; c0 < EP; c0 += 32) {
+      uint32_t r[32];
+      if (c0 + 16 < EP) {
+        tmem_ld32(taddr + c0, r);
+      } else {
+        uint32_t (&r16)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[0]);
+        tmem_ld16(taddr + c0, r16);
       }
-    }
-    float sum = 0.f;
-    for (int c0 = 0; c0 < EP; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld16(taddr + c0, r);
       tmem_ld_wait();
+      const int w = min(32, EP - c0);
+      float cmax = -INFINITY;
+      int cidx = 0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (c0 + j < E) sum += expf(__uint_as_float(r[j]) - best);
+      for (int j = 0; j < 32; ++j) {
+        if (j < w && c0 + j < E) {
+          const float v = __uint_as_float(r[j]);
+          if (v > cmax) { cmax = v; cidx = c0 + j; }
+          if (c0 + j == sel) lsel = v;
+        }
+      }
+      if (cmax > best) {
+        sum *= exp2f((best - cmax) * kLog2e);   // best = -inf on the first chunk -> 0 * 0
+        best = cmax;
+        best_e = cidx;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < w && c0 + j < E) sum += exp2f((__uint_as_float(r[j]) - best) * kLog2e);
     }
     if (t < n) {
       RouteRec rec;
       rec.expert = sel >= 0 ? sel : best_e;
-      rec.gate = (sel >= 0 ? expf(lsel - best) : 1.f) / sum;
+      rec.gate = (sel >= 0 ? exp2f((lsel - best) * kLog2e) : 1.f) / sum;
       out[t] = rec;
+      atomicAdd(&s_hist[rec.expert], 1);
       if (bad) atomicExch(err_flag, 1);
     }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+    for (int e = threadIdx.x; e < E; e += 128) hist_out[(size_t)blockIdx.x * E + e] = s_hist[e];
+    if (kT && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 40))
+      printf("[router cta %d] setup %lld mainloop %lld epilogue %lld\n", blockIdx.x,
+             t_setup - t_start, t_done - t_setup, clock64() - t_done);
   }
   tc_fence_before();
   __syncthreads();
@@ -342,26 +388,44 @@ __global__ void __launch_bounds__(192, 1)
 
 }  // namespace
 
-size_t router_tc_smem_bytes(int EP) {
-  return 1024 + RTC_STAGES * (RTC_A_BYTES + EP * 128) + (2 * RTC_STAGES + 1) * 8 + 16;
+size_t router_tc_smem_bytes(int EP, bool mn) {
+  const int b = mn ? ((EP + 63) / 64) * 8192 : EP * 128;
+  const int st = std::min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (RTC_A_BYTES + b));
+  return 1024 + st * (RTC_A_BYTES + b) + (2 * st + 1) * 8 + 16;
 }
 
-cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, const void* w_r,
-                             void* wt_r, int n, int h, int E, int EP, const int32_t* forced,
-                             RouteRec* out, int32_t* err_flag, cudaStream_t s) {
+cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
+                             const void* w_r, void* wt_r, int n, int h, int E, int EP,
+                             const int32_t* forced, RouteRec* out, int32_t* hist_out,
+                             int32_t* err_flag, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
-  router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,
-                                     static_cast<__nv_bfloat16*>(wt_r));
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(router_tc_smem_bytes(256)));
+    cudaError_t e = cudaFuncSetAttribute(router_tc_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         RTC_SMEM_BUDGET + 2048);  // >= router_tc_smem_bytes(any EP)
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(router_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               RTC_SMEM_BUDGET + 2048);  // >= router_tc_smem_bytes(any EP)
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  router_tc_kernel<<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP), s>>>(tmX, tmW, n, h, E, EP,
-                                                                        forced, out, err_flag);
+  static const bool timing = getenv("MOESHARD_ROUTER_TIMING") != nullptr;
+  if (mn_major && timing) {
+    cudaFuncSetAttribute(router_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         RTC_SMEM_BUDGET + 2048);
+    router_tc_kernel<true, true><<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP, true), s>>>(
+        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
+  } else if (mn_major) {
+    router_tc_kernel<true><<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP, true), s>>>(
+        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
+  } else {
+    dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
+    router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,
+                                       static_cast<__nv_bfloat16*>(wt_r));
+    router_tc_kernel<false><<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP, false), s>>>(
+        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
+  }
   return cudaGetLastError();
 }
 
