@@ -265,12 +265,15 @@ def main():
         if G > 1:
             dist.barrier()
 
+    launch_count = {}
+
     def timed(fn, steps, warmup, sampler=None):
         for w in range(warmup):
             fn(w)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
+        l0 = layer.stats()["kernel_launches"]
         st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if sampler:
             sampler.__enter__()
@@ -281,6 +284,7 @@ def main():
         torch.cuda.synchronize()
         if sampler:
             sampler.__exit__()
+        launch_count["timed"] = layer.stats()["kernel_launches"] - l0
         barrier()
         torch.cuda.synchronize()
         ms = st.elapsed_time(en)
@@ -294,10 +298,9 @@ def main():
     fwd_skew = lambda k: layer.forward(k % NW, x, w_r, forced_expert=zipf, out=out)
 
     # --- main timed region (natural router, near-uniform routing)
-    launches0 = layer.stats()["kernel_launches"]
     clk = ClockSampler(local)
     ms = timed(fwd, args.steps, args.warmup, sampler=clk)
-    launches = layer.stats()["kernel_launches"] - launches0
+    launches = launch_count["timed"]
     st_uniform = layer.stats()
     r = layer.routing(n)
     counts = r["counts"].cpu()
@@ -335,10 +338,10 @@ def main():
         w = e_act * h * F * 2
         return {"gemm_up": w + N * h * 2 + N * F * 2, "gemm_down": w + N * F * 2 + N * h * 2}
     gb = gemm_bytes(e_active_u)
-    alg = {
-        "router": n * h * 2 + h * E * 2 + n * 8,
-        "grouping": 3 * N * 8 + 2 * N * 4,
-        "gather_rows": 2 * N * h * 2,
+    nb_hist = G * math.ceil(n / 128)
+    alg = {   # algorithmic HBM bytes per launch
+        "router": n * h * 2 + h * E * 2 + n * 8 + math.ceil(n / 128) * E * 4,
+        "grouping": N * 8 + N * 4 + 2 * N * h * 2 + nb_hist * E * 4,
         "gemm_up": gb["gemm_up"],
         "gemm_down": gb["gemm_down"],
     }
@@ -353,18 +356,22 @@ def main():
             d["TFLOP_s"] = round(flops[k] / (us * 1e-6) / 1e12, 1)
         kernels[k] = d
     dom = max(("gemm_up", "gemm_down"), key=lambda k: ph_us[k])
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config, {}).get(dom)
+            tj = json.load(open(tp))
+            traffic = tj.get(args.config, {}).get(dom)
+            traffic_src = tj.get("source")
         except Exception:
             traffic = None
     achieved = alg[dom] / (ph_us[dom] * 1e-6) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)", "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": traffic,
-                "algorithmic_bytes": alg[dom], "launch_us": round(ph_us[dom], 3)}
+                "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes": alg[dom], "launch_us": round(ph_us[dom], 3),
+                "timing": "phase CUDA events on the launch stream around the kernel, averaged over "
+                          f"{cnt} forwards of a separate profiled pass (includes ~2-3 us event gap)"}
     # whole-layer roofline: T_TC, T_HBM (weights + x + partial), T_NV
     t_tc = 4 * N * h * F / (tf_burst * 1e12) * 1e6
     t_hbm = (e_active_u * 2 * h * F * 2 + N * h * 2 + N * h * 2) / (hbm * 1e9) * 1e6

@@ -164,9 +164,9 @@ int moeshard_get_stats(moeshard_ctx* ctx, moeshard_stats* out, void* stream);
  * and resets the accumulators; enable == 0 stops. moeshard_get_phase_ms
  * synchronises and writes into out[0..n) the total milliseconds spent, over
  * all forwards recorded since enabling, in the phases
- *   0 router, 1 token/metadata AllGather, 2 grouping (hist+scan+scatter),
- *   3 row gather (permute), 4 grouped GEMM up, 5 grouped GEMM down,
- *   6 ReduceScatter
+ *   0 router, 1 token/metadata AllGather, 2 grouping (offsets, stable
+ *   permutation, row gather), 3 grouped GEMM up, 4 grouped GEMM down,
+ *   5 ReduceScatter
  * and returns the number of forwards in *count. */
 int moeshard_profile(moeshard_ctx* ctx, int enable);
 int moeshard_get_phase_ms(moeshard_ctx* ctx, float* out, int n, int* count);

@@ -178,7 +178,7 @@ struct moeshard_ctx {
   int64_t launches = 0;  // cumulative kernel launches of this context
   // phase profiling (measurement only)
   bool prof = false;
-  static constexpr int kRing = 1024, kEv = 8;
+  static constexpr int kRing = 1024, kEv = 7;
   std::vector<cudaEvent_t> ev;  // kRing * kEv
   int prof_count = 0;
   std::string err = "no error";
@@ -482,31 +482,30 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
                       x_all, n, nbr, HB, h * c->elt, c->perm, c->x_perm, s);
   c->launches += 1;
   c->mark(3, s);
-  c->mark(4, s);
   // Step 4: expert computation, one grouped product per projection
   void* P = c->coll ? c->partial : hidden_out;
   if (c->use_tc) {
     TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
                 static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
     CUDA_TRY(c, launch_tc_gemm(false, lw.tm_in, c->tm_xperm, c->tm_xperm16, up, c->num_sms, s));
-    c->mark(5, s);
+    c->mark(4, s);
     TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
                 static_cast<__nv_bfloat16*>(P), h, c->perm, c->route};
     CUDA_TRY(c, launch_tc_gemm(true, lw.tm_out, c->tm_H, c->tm_H16, dn, c->num_sms, s));
   } else {
     launch_simt_up(c->cfg.dtype, c->x_perm, lw.wt_in, h, F, E, c->tb, c->H, c->num_sms, s);
-    c->mark(5, s);
+    c->mark(4, s);
     launch_simt_down(c->cfg.dtype, c->H, lw.wt_out, F, h, E, c->tb, c->perm, c->route, P,
                      c->num_sms, s);
   }
   CUDA_TRY(c, cudaGetLastError());
   c->launches += 2;
-  c->mark(6, s);
+  c->mark(5, s);
   // Step 5: gather partial outputs to their owner and sum (aggregateTokens)
   if (c->coll)
     NCCL_TRY(c, nccl().ReduceScatter(P, hidden_out, static_cast<size_t>(n) * h, ndt, ncclSum,
                                      c->comm, s));
-  c->mark(7, s);
+  c->mark(6, s);
   if (c->prof) c->prof_count++;
   return MOESHARD_OK;
 }

@@ -35,8 +35,7 @@ EXPORTS = [
     "moeshard_get_stats", "moeshard_check", "moeshard_last_error", "moeshard_status_string",
     "moeshard_destroy", "moeshard_version", "moeshard_profile", "moeshard_get_phase_ms",
 ]
-PHASES = ["router", "allgather", "grouping", "gather_rows", "gemm_up", "gemm_down",
-          "reduce_scatter"]
+PHASES = ["router", "allgather", "grouping", "gemm_up", "gemm_down", "reduce_scatter"]
 
 
 class MoEShardError(RuntimeError):
