@@ -69,6 +69,7 @@ typedef enum {
 /* config.flags */
 #define MOESHARD_FLAG_FORCE_COLLECTIVES 0x1u /* run the AllGather/ReduceScatter path even at world = 1 */
 #define MOESHARD_FLAG_SIMT_GEMM 0x2u         /* bf16 mode: CUDA-core grouped GEMM (ablation / debug) */
+#define MOESHARD_FLAG_UNFUSED_GEMM 0x4u      /* bf16 mode: up and down products as two launches (ablation) */
 
 typedef struct {
   int32_t d_model;             /* h; multiple of 128 */

@@ -32,6 +32,7 @@ struct Tables {
   int32_t* tc_chunk_size;  // [E]
   int32_t* simt_chunk_pref;  // [E+1]
   int32_t* stats;          // [8]: 0 tiles_up, 1 tiles_down, 2 rows_up, 3 error flag
+  int32_t* done;           // [E] up-projection tiles completed per expert (fused GEMM), zeroed by Step 2
 };
 
 __device__ __forceinline__ float to_f32(float v) { return v; }
@@ -55,6 +56,25 @@ __host__ __device__ __forceinline__ void tc_chunking(int n_e, int* n_chunks, int
   int cs = round_up(ceil_div(n_e, c0), 32);
   *chunk = cs;
   *n_chunks = ceil_div(n_e, cs);
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while the previous kernel in the stream drains; it must call
+// griddepcontrol.wait before touching memory the predecessor writes or reads.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 }  // namespace moeshard

@@ -540,6 +540,236 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc_2sm(tmem_base, TMEM_COLS);
 }
 
+
+// ===========================================================================
+// Both projections in ONE persistent CTA-pair kernel. The work list is
+// [all up pair-units (expert-major), all down pair-units (expert-major)];
+// cluster c takes units c, c + #clusters, ... A down unit of expert e reads
+// H rows written by the up units of e (every feature tile), so its token
+// producer waits until done[e] == 2 * chunks(e) * n_mp_up (each CTA of each up
+// pair-unit releases one count after its H tile is stored) - acquire, then an
+// async-proxy fence before the TMA reads H. Units earlier in the list never
+// wait on later ones, so with all clusters resident there is no deadlock.
+// This removes the down-projection's wave-quantisation tail and the launch gap
+// between the two products.
+// ===========================================================================
+struct FusedParams {
+  TcParams up, dn;
+  int32_t* done;  // [E], zeroed by Step 2 before every forward
+};
+
+template <int AS, int BS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_moe_ffn_2sm(const __grid_constant__ CUtensorMap tmA_up, const __grid_constant__ CUtensorMap tmB_up,
+                   const __grid_constant__ CUtensorMap tmA_dn, const __grid_constant__ CUtensorMap tmB_dn,
+                   FusedParams fp) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int E = fp.up.E;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + AS * A_BYTES;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + BS * B2_BYTES);
+  uint64_t* emptyA = fullA + AS;
+  uint64_t* fullB = emptyA + AS;
+  uint64_t* emptyB = fullB + BS;
+  uint64_t* tfull = emptyB + BS;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int32_t* s_pref = reinterpret_cast<int32_t*>(tmem_slot + 4);
+  int32_t* s_off = s_pref + (E + 1);
+  int32_t* s_cs = s_off + (E + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA_up);
+    tma_prefetch_desc(&tmA_dn);
+  }
+  if (warp == 3 && lane == 0) {
+    tma_prefetch_desc(&tmB_up);
+    tma_prefetch_desc(&tmB_dn);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(&fullA[s], 2);
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(&fullB[s], 2);
+      mbar_init(&emptyB[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_mbar_init();
+  }
+  cluster_sync_all();
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+  // PDL: everything above overlapped the grouping kernel's tail
+  griddep_wait();
+  for (int i = threadIdx.x; i <= E; i += kThreads) {
+    s_pref[i] = fp.up.tb.tc_chunk_pref[i];
+    s_off[i] = fp.up.tb.offsets[i];
+    if (i < E) s_cs[i] = fp.up.tb.tc_chunk_size[i];
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();
+
+  const int n_mp_up = fp.up.n_mt / 2, n_mp_dn = fp.dn.n_mt / 2;
+  const int chunks = s_pref[E];
+  const int total_up = chunks * n_mp_up;
+  const int total = total_up + chunks * n_mp_dn;
+  const int nkb_up = fp.up.K / BK, nkb_dn = fp.dn.K / BK;
+  const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
+
+  if (warp == 0) {
+    // -------------------------------------------------------------- weight producer (both CTAs)
+    const uint64_t pol_w = policy_evict_first();
+    const uint32_t leader_full = mapa_shared(smem_u32(fullA), 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = cid; u < total; u += ncl) {
+      const bool down = u >= total_up;
+      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_cs);
+      const int n_mt = down ? fp.dn.n_mt : fp.up.n_mt;
+      const int nkb = down ? nkb_dn : nkb_up;
+      const CUtensorMap* tm = down ? &tmA_dn : &tmA_up;
+      const int mt = 2 * w.mt + static_cast<int>(rank);
+      const int row0 = ((w.e * n_mt + mt) * nkb) * BM;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&emptyA[stage], phase ^ 1);
+        const uint32_t fb = leader_full + stage * 8;
+        if (elect_one()) {
+          if (leader) mbar_arrive_expect_tx(&fullA[stage], 2 * A_BYTES);
+          else mbar_arrive_cluster(fb);
+          tma_load_2d_2sm(tm, fb, sA + stage * A_BYTES, 0, row0 + kb * BM, pol_w);
+        }
+        __syncwarp();
+        if (++stage == AS) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 3) {
+    // -------------------------------------------------------------- token producer (both CTAs)
+    const uint64_t pol_x = policy_evict_last();
+    const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = cid; u < total; u += ncl) {
+      const bool down = u >= total_up;
+      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_cs);
+      const int nkb = down ? nkb_dn : nkb_up;
+      const CUtensorMap* tm = down ? &tmB_dn : &tmB_up;
+      if (down) {   // H rows of expert e complete? (acquire), then order the TMA after it
+        const int target = 2 * (s_pref[w.e + 1] - s_pref[w.e]) * n_mp_up;
+        if (elect_one()) {
+          while (ld_acquire_gpu(fp.done + w.e) < target) __nanosleep(128);
+          fence_proxy_async_global();
+        }
+        __syncwarp();
+      }
+      const int half = ((w.ntok + 31) & ~31) / 2;
+      const int nb = half / B2_BOX;
+      const int r0 = w.tok0 + static_cast<int>(rank) * half;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&emptyB[stage], phase ^ 1);
+        const uint32_t fb = leader_full + stage * 8;
+        if (elect_one()) {
+          if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * nb * B2_BOX * BK * 2);
+          else mbar_arrive_cluster(fb);
+          for (int i = 0; i < nb; ++i)
+            tma_load_2d_2sm(tm, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
+                            r0 + i * B2_BOX, pol_x);
+        }
+        __syncwarp();
+        if (++stage == BS) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ------------------------------------------------------------ MMA issuer (leader only)
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      int as = 0;
+      uint32_t aphase = 0;
+      for (int u = cid; u < total; u += ncl) {
+        const bool down = u >= total_up;
+        const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_cs);
+        const int nkb = down ? nkb_dn : nkb_up;
+        const int nmma = (w.ntok + 31) & ~31;
+        const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * BN_MAX;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&fullB[sb], pb);
+          mbar_wait(&fullA[sa], pa);
+          tc_fence_after();
+          const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
+          const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B2_BYTES));
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_ss_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            mma_commit_2sm(&emptyA[sa], 0x3);
+            mma_commit_2sm(&emptyB[sb], 0x3);
+          }
+          __syncwarp();
+          if (++sa == AS) { sa = 0; pa ^= 1; }
+          if (++sb == BS) { sb = 0; pb ^= 1; }
+        }
+        if (elect_one()) mma_commit_2sm(&tfull[as], 0x3);
+        __syncwarp();
+        as ^= 1;
+        if (as == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue (both CTAs)
+    const int wq = warp & 3;
+    __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(
+        (reinterpret_cast<uintptr_t>(s_cs + E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
+    const uint64_t pol_keep = policy_evict_last();
+    const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
+    int as = 0;
+    uint32_t aphase = 0;
+    for (int u = cid; u < total; u += ncl) {
+      const bool down = u >= total_up;
+      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_cs);
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
+      const int mt = 2 * w.mt + static_cast<int>(rank);
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * BN_MAX;
+      if (down)
+        store_tile<true>(fp.dn, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
+                         pol_keep, stage);
+      else
+        store_tile<false>(fp.up, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
+                          pol_keep, stage);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty + as * 8);
+      if (!down) {   // publish this CTA's H tile of expert e
+        __threadfence();
+        asm volatile("bar.sync 2, 128;" ::: "memory");   // the 4 epilogue warps
+        if (wq == 0 && lane == 0) red_release_gpu_add(fp.done + w.e, 1);
+      }
+      as ^= 1;
+      if (as == 0) aphase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+}
+
 size_t smem_bytes(int E, int as, int bs) {
   return 1024 + as * A_BYTES + bs * B_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (3 * E + 2) * 4 +
          16 + 4 * 1024;
@@ -615,6 +845,24 @@ cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUten
 }
 
 }  // namespace
+
+cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
+                              const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
+                              const TcParams& up, const TcParams& dn, int32_t* done, int grid,
+                              cudaStream_t s) {
+  constexpr int AS = 6, BS = 6;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem_bytes_2sm(kMaxExperts, AS, BS)));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  FusedParams fp{up, dn, done};
+  return launch_pdl(tc_moe_ffn_2sm<AS, BS>, dim3(grid & ~1), dim3(kThreads),
+                    smem_bytes_2sm(up.E, AS, BS), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
+}
 
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const CUtensorMap& tmB2, const TcParams& p, int grid, cudaStream_t s) {

@@ -46,6 +46,13 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
 //   tmB:  activations [N][K], box {64, 32}, 128-B swizzle   (one-CTA kernel)
 //   tmB2: activations [N][K], box {64, 16}, 128-B swizzle   (CTA-pair kernel)
 // The CTA-pair (cta_group::2) kernel is used when n_mt is even.
+// Both projections in one persistent CTA-pair launch (needs F/128 and h/128 even).
+// done: [E] int32 zeroed before the launch (Step 2 does it).
+cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
+                              const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
+                              const TcParams& up, const TcParams& dn, int32_t* done, int grid,
+                              cudaStream_t s);
+
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const CUtensorMap& tmB2, const TcParams& p, int grid, cudaStream_t s);
 

@@ -138,7 +138,7 @@ Layout make_layout(const moeshard_config& c, int world) {
   L.route = take(Nmax * sizeof(RouteRec));
   L.block_hist = take(nb * E * 4);
   L.block_base = take(nb * E * 4);
-  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8);
+  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E);
   L.ints = take(L.n_ints * 4);
   L.perm = take(Nmax * 4);
   L.x_all = coll ? take(Nmax * h * elt) : 0;
@@ -344,6 +344,7 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->tb.tc_chunk_size = c->tb.tc_chunk_pref + (E + 1);
   c->tb.simt_chunk_pref = c->tb.tc_chunk_size + E;
   c->tb.stats = c->tb.simt_chunk_pref + (E + 1);
+  c->tb.done = c->tb.stats + 8;
   c->perm = reinterpret_cast<int32_t*>(c->ws + L.perm);
   c->x_all = c->coll ? c->ws + L.x_all : nullptr;
   c->x_perm = c->ws + L.x_perm;
@@ -484,7 +485,18 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   c->mark(3, s);
   // Step 4: expert computation, one grouped product per projection
   void* P = c->coll ? c->partial : hidden_out;
-  if (c->use_tc) {
+  const bool fused = c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_UNFUSED_GEMM) &&
+                     (F / kTcFeatTile) % 2 == 0 && (h / kTcFeatTile) % 2 == 0;
+  if (fused) {
+    TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
+                static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
+    TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
+                static_cast<__nv_bfloat16*>(P), h, c->perm, c->route};
+    CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, c->tm_xperm16, lw.tm_out, c->tm_H16, up, dn,
+                                  c->tb.done, c->num_sms, s));
+    c->mark(4, s);
+    c->launches += 1;
+  } else if (c->use_tc) {
     TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
                 static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
     CUDA_TRY(c, launch_tc_gemm(false, lw.tm_in, c->tm_xperm, c->tm_xperm16, up, c->num_sms, s));
@@ -492,14 +504,15 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
                 static_cast<__nv_bfloat16*>(P), h, c->perm, c->route};
     CUDA_TRY(c, launch_tc_gemm(true, lw.tm_out, c->tm_H, c->tm_H16, dn, c->num_sms, s));
+    c->launches += 2;
   } else {
     launch_simt_up(c->cfg.dtype, c->x_perm, lw.wt_in, h, F, E, c->tb, c->H, c->num_sms, s);
     c->mark(4, s);
     launch_simt_down(c->cfg.dtype, c->H, lw.wt_out, F, h, E, c->tb, c->perm, c->route, P,
                      c->num_sms, s);
+    c->launches += 2;
   }
   CUDA_TRY(c, cudaGetLastError());
-  c->launches += 2;
   c->mark(5, s);
   // Step 5: gather partial outputs to their owner and sum (aggregateTokens)
   if (c->coll)

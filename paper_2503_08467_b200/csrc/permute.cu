@@ -12,6 +12,7 @@
 // Also: a batched transpose used once at load time to repack expert shards
 // K-major (loadShard).
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace moeshard {
 namespace {
@@ -42,6 +43,37 @@ __global__ void transpose_kernel(const T* __restrict__ src, T* __restrict__ dst,
   }
 }
 
+
+// Exclusive scan over the CTA (kThreads <= 1024, one value per thread); total in `total`.
+template <int kThreads>
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
+  constexpr int kWarps = kThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int w = lane < kWarps ? s_warp[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += o;
+    }
+    if (lane < kWarps) s_warp[lane] = wi - w;
+    if (lane == 31) s_warp[32] = wi;
+  }
+  __syncthreads();
+  const int res = s_warp[warp] + incl - v;
+  total = s_warp[32];
+  __syncthreads();
+  return res;
+}
 
 __device__ __forceinline__ int block_excl_scan_1024(int v, int* s_warp, int& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -91,11 +123,16 @@ __device__ __forceinline__ int block_excl_scan_1024(int v, int* s_warp, int& tot
 //     (match_any) -> j = offsets[e] + earlier[e] + rank, perm[j] = t;
 //  3. all 32 warps copy the block's rows to X_perm[j] (16-B vectors, 4 rows
 //     per warp with every load in flight before the stores).
-template <int VPL>
-__global__ void __launch_bounds__(1024, 1) group_scatter_gather(
+// kSplit CTAs share one hist-block: all compute its ranks, each copies
+// 128/kSplit of its rows (spreads the row traffic over more SMs).
+template <int VPL, int kSplit>
+__global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     const int32_t* __restrict__ hist, int NB, int E, Tables tb, int n_mt_up_tc, int n_mt_down_tc,
     const RouteRec* __restrict__ route, const uint4* __restrict__ x_all, int n, int nbr, int HB,
     int32_t* __restrict__ perm, int row_vecs, uint4* __restrict__ x_perm) {
+  constexpr int kThreads = 1024 / kSplit;
+  constexpr int kRowsPerWarp = 4;                 // rows copied per warp
+  static_assert(kThreads >= 128, "ranks need 128 threads");
   __shared__ int32_t s_tot[kMaxExperts];
   __shared__ int32_t s_pre[kMaxExperts];
   __shared__ int32_t s_base[kMaxExperts];
@@ -103,16 +140,19 @@ __global__ void __launch_bounds__(1024, 1) group_scatter_gather(
   __shared__ int32_t s_j[128];
   __shared__ int32_t s_warp[33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int b = blockIdx.x;
+  const int b = blockIdx.x / kSplit, part = blockIdx.x % kSplit;
   const int r = b / nbr, i = b - r * nbr;
   const int t0 = r * n + i * HB;
   const int t1 = min(t0 + HB, (r + 1) * n);
-  // issue this block's row loads first: the sources are known, only the
+  const int row_base = part * (128 / kSplit);     // this CTA's rows of the block
+  ptx::griddep_wait();            // the router's records and histograms
+  ptx::griddep_launch_dependents();
+  // issue this CTA's row loads first: the sources are known, only the
   // destinations depend on the scan below
-  uint4 v[4][VPL];
+  uint4 v[kRowsPerWarp][VPL];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int tt = t0 + warp * 4 + u;
+  for (int u = 0; u < kRowsPerWarp; ++u) {
+    const int tt = t0 + row_base + warp * kRowsPerWarp + u;
 #pragma unroll
     for (int c = 0; c < VPL; ++c) {
       const int col = lane + 32 * c;
@@ -124,15 +164,15 @@ __global__ void __launch_bounds__(1024, 1) group_scatter_gather(
     t = t0 + threadIdx.x;
     e = (t < t1) ? __ldg(&route[t].expert) : -1;
   }
-  for (int k = threadIdx.x; k < E; k += 1024) {
+  for (int k = threadIdx.x; k < E; k += kThreads) {
     s_tot[k] = 0;
     s_pre[k] = 0;
   }
-  for (int k = threadIdx.x; k < 4 * E; k += 1024) whist[k / E][k % E] = 0;
+  for (int k = threadIdx.x; k < 4 * E; k += kThreads) whist[k / E][k % E] = 0;
   __syncthreads();
   // 1. totals and earlier-block counts (consecutive threads -> consecutive experts)
   const int total = NB * E;
-  for (int idx = threadIdx.x; idx < total; idx += 1024) {
+  for (int idx = threadIdx.x; idx < total; idx += kThreads) {
     const int bb = idx / E, e = idx - bb * E;
     const int v = __ldg(hist + idx);
     if (v) {
@@ -151,14 +191,15 @@ __global__ void __launch_bounds__(1024, 1) group_scatter_gather(
       sc = ceil_div(cnt, kSimtTokTile);
     }
     int tot_cnt;
-    const int off = block_excl_scan_1024(cnt, s_warp, tot_cnt);
+    const int off = block_excl_scan<kThreads>(cnt, s_warp, tot_cnt);
     if (e < E) s_base[e] = off + s_pre[e];
-    if (b == 0) {  // publish the tables the grouped GEMMs read
+    if (blockIdx.x == 0) {  // publish the tables the grouped GEMMs read
       int tot_tc, tot_sc, tot_rows;
-      const int tcp = block_excl_scan_1024(nc, s_warp, tot_tc);
-      const int smp = block_excl_scan_1024(sc, s_warp, tot_sc);
-      block_excl_scan_1024(rows, s_warp, tot_rows);
+      const int tcp = block_excl_scan<kThreads>(nc, s_warp, tot_tc);
+      const int smp = block_excl_scan<kThreads>(sc, s_warp, tot_sc);
+      block_excl_scan<kThreads>(rows, s_warp, tot_rows);
       if (e < E) {
+        tb.done[e] = 0;
         tb.counts[e] = cnt;
         tb.tc_chunk_size[e] = cs;
         tb.offsets[e] = off;
@@ -187,19 +228,19 @@ __global__ void __launch_bounds__(1024, 1) group_scatter_gather(
       int before = 0;
       for (int w = 0; w < warp; ++w) before += whist[w][e];
       const int j = s_base[e] + before + rank_w;
-      perm[j] = t;
+      if (part == 0) perm[j] = t;
       s_j[threadIdx.x] = j;
     } else {
       s_j[threadIdx.x] = -1;
     }
   }
   __syncthreads();
-  // 3. row stores: warp w moves rows 4w .. 4w+3 of the block (loaded at the top)
-  int jj[4];
+  // 3. row stores (rows loaded at the top)
+  int jj[kRowsPerWarp];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) jj[u] = s_j[warp * 4 + u];
+  for (int u = 0; u < kRowsPerWarp; ++u) jj[u] = s_j[row_base + warp * kRowsPerWarp + u];
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < kRowsPerWarp; ++u)
 #pragma unroll
     for (int c = 0; c < VPL; ++c) {
       const int col = lane + 32 * c;
@@ -217,9 +258,10 @@ void launch_group_blocks(const int32_t* hist, int NB, int E, Tables tb, int n_mt
   const int vpl = ceil_div(row_vecs, 32);
   auto* xs = static_cast<const uint4*>(x_all);
   auto* xd = static_cast<uint4*>(x_perm);
-#define SG(V)                                                                                \
-  group_scatter_gather<V><<<NB, 1024, 0, s>>>(hist, NB, E, tb, n_mt_up_tc, n_mt_down_tc, route, \
-                                              xs, n, nbr, HB, perm, row_vecs, xd)
+  // each hist-block's rows are copied by kSplit = 4 CTAs of 256 threads
+#define SG(V)                                                                                    \
+  launch_pdl(group_scatter_gather<V, 4>, dim3(NB * 4), dim3(256), 0, s, hist, NB, E, tb,          \
+             n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm, row_vecs, xd)
   switch (vpl) {
     case 1: SG(1); break;
     case 2: SG(2); break;

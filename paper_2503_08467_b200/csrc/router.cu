@@ -265,6 +265,10 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: x may come from the previous kernel, and the previous forward's FFN
+  // still reads the route records this kernel overwrites
+  griddep_wait();
+  griddep_launch_dependents();
   const long long t_setup = clock64();
   const int tok0 = blockIdx.x * 128;
   const int nkb = h / 64;
@@ -417,8 +421,9 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
     router_tc_kernel<true, true><<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP, true), s>>>(
         tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
   } else if (mn_major) {
-    router_tc_kernel<true><<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP, true), s>>>(
-        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
+    return launch_pdl(router_tc_kernel<true>, dim3(ceil_div(n, 128)), dim3(192),
+                      router_tc_smem_bytes(EP, true), s, tmX, tmW, n, h, E, EP, forced, out,
+                      hist_out, err_flag);
   } else {
     dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
     router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,

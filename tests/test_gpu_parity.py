@@ -130,6 +130,31 @@ def test_bf16_simt_ablation_matches_oracle():
     _check_layer(inp, y, r, tol=BF16_TOL)
 
 
+def test_unfused_two_launch_gemm_ablation_matches_oracle():
+    # the up and down products as two CTA-pair launches instead of the fused kernel
+    from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_UNFUSED_GEMM
+    inp = W.make_layer_inputs(18, 2100, 256, 512, 32, dtype=torch.bfloat16, routing="zipf")
+    L, y, r = _run(inp, dtype=torch.bfloat16, flags=MOESHARD_FLAG_UNFUSED_GEMM,
+                   forced=inp.forced.cuda().contiguous())
+    _check_layer(inp, y, r, tol=BF16_TOL)
+
+
+def test_fused_and_unfused_gemm_agree_bitwise():
+    # same arithmetic in both schedules: outputs must be identical bit for bit
+    from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_UNFUSED_GEMM
+    inp = W.make_layer_inputs(19, 3000, 512, 1024, 64, dtype=torch.bfloat16, routing="zipf")
+    f = inp.forced.cuda().contiguous()
+    ys = []
+    for flags in (0, MOESHARD_FLAG_UNFUSED_GEMM):
+        L = MoEShardLayer(512, 1024, 64, max_tokens_per_rank=3000, dtype=torch.bfloat16, flags=flags)
+        L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
+        ys.append(L.forward(0, inp.x.cuda(), inp.w_r.cuda(), forced_expert=f))
+        torch.cuda.synchronize()
+        L.close()
+    assert torch.equal(ys[0], ys[1])
+
+
 def test_forced_collectives_path_world1():
     # exercises AllGather / partial buffer / ReduceScatter through NCCL with one rank
     from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_FORCE_COLLECTIVES
