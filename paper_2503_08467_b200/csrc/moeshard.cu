@@ -25,6 +25,8 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -176,6 +178,7 @@ struct moeshard_ctx {
   ncclComm_t comm = nullptr;
   int last_n = 0;
   int64_t launches = 0;  // cumulative kernel launches of this context
+  long long pf_bytes = 0;  // experimental L2 weight prefetch during routing (MOESHARD_L2_PREFETCH_MB)
   // phase profiling (measurement only)
   bool prof = false;
   static constexpr int kRing = 1024, kEv = 7;
@@ -319,6 +322,7 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
 
   auto* c = new moeshard_ctx();
   c->cfg = *cfg;
+  if (const char* fl = getenv("MOESHARD_FLAGS")) c->cfg.flags |= static_cast<uint32_t>(atoi(fl));
   c->rank = rank;
   c->world = world;
   c->device = device;
@@ -327,8 +331,9 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->F = cfg->d_ff / world;
   c->E = cfg->n_experts;
   c->elt = cfg->dtype == MOESHARD_BF16 ? 2 : 4;
-  c->coll = world > 1 || (cfg->flags & MOESHARD_FLAG_FORCE_COLLECTIVES);
-  c->use_tc = cfg->dtype == MOESHARD_BF16 && !(cfg->flags & MOESHARD_FLAG_SIMT_GEMM);
+  c->coll = world > 1 || (c->cfg.flags & MOESHARD_FLAG_FORCE_COLLECTIVES);
+  c->use_tc = cfg->dtype == MOESHARD_BF16 && !(c->cfg.flags & MOESHARD_FLAG_SIMT_GEMM);
+  if (const char* pf = getenv("MOESHARD_L2_PREFETCH_MB")) c->pf_bytes = atoll(pf) << 20;
   c->L = L;
   c->ws = static_cast<char*>(workspace);
   c->route = reinterpret_cast<RouteRec*>(c->ws + L.route);
@@ -457,8 +462,14 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     if (!make_tmap(&tm_x, hidden, h, n, 128) ||
         (mn && !make_tmap(&tm_w, router_w, E, h, 64)))
       return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden/router_w");
+    // L2 prefetch of the first up-projection tiles on the SMs the router leaves idle
+    const int tiles = (n + 127) / 128;
+    const int pf_ctas = c->pf_bytes > 0 ? std::max(0, std::min(c->num_sms - tiles, 96)) : 0;
+    const long long pf_bytes =
+        std::min<long long>(c->pf_bytes, static_cast<long long>(E) * F * h * c->elt);
     CUDA_TRY(c, launch_router_tc(tm_x, mn ? tm_w : c->tm_wt_r, mn, router_w, c->wt_r, n, h, E,
-                                 c->EP, forced, my_route, my_hist, err_flag, s));
+                                 c->EP, forced, my_route, my_hist, err_flag, lw.wt_in, pf_bytes,
+                                 pf_ctas, s));
     c->launches += mn ? 1 : 2;
   } else {
     launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, my_hist, err_flag, s);

@@ -75,33 +75,6 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
   return res;
 }
 
-__device__ __forceinline__ int block_excl_scan_1024(int v, int* s_warp, int& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int o = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += o;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const int w = s_warp[lane];
-    int wi = w;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int o = __shfl_up_sync(0xffffffffu, wi, off);
-      if (lane >= off) wi += o;
-    }
-    s_warp[lane] = wi - w;
-    if (lane == 31) s_warp[32] = wi;
-  }
-  __syncthreads();
-  const int res = s_warp[warp] + incl - v;
-  total = s_warp[32];
-  __syncthreads();
-  return res;
-}
 
 
 // ===========================================================================

@@ -99,6 +99,12 @@ __device__ __forceinline__ void red_release_gpu_add(int32_t* p, int v) {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+// Prefetch [p, p + bytes) into L2 (bytes multiple of 16), no shared-memory destination.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)),
+               "r"(bytes)
+               : "memory");
+}
 // L2 cache-policy descriptors (createpolicy.fractional)
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;

@@ -205,6 +205,13 @@ namespace moeshard {
 namespace {
 
 constexpr int RTC_MAX_STAGES = 8;
+
+// 2^x on the SFU (ex2.approx.ftz: ~2 ulp; exp2(-inf) = +0)
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 constexpr int RTC_SMEM_BUDGET = 200 * 1024;
 constexpr int RTC_A_BYTES = 128 * 128;  // 128 tokens x 64 k x 2 B
 
@@ -230,7 +237,20 @@ __global__ void __launch_bounds__(192, 1)
     router_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      int n, int h, int E, int EP, const int32_t* __restrict__ forced,
                      RouteRec* __restrict__ out, int32_t* __restrict__ hist_out,
-                     int32_t* __restrict__ err_flag) {
+                     int32_t* __restrict__ err_flag, const uint8_t* __restrict__ pf,
+                     long long pf_bytes) {
+  // CTAs beyond the token tiles run on otherwise idle SMs and pull the first
+  // weight tiles the FFN kernel will stream into L2 while routing and grouping
+  // are latency-bound (the weights do not depend on the routing result).
+  const int n_tiles = (n + 127) / 128;
+  if (static_cast<int>(blockIdx.x) >= n_tiles) {
+    const int n_pf = gridDim.x - n_tiles, q = blockIdx.x - n_tiles;
+    const long long per = ((pf_bytes / n_pf) + 16383) & ~16383LL;
+    const long long beg = q * per, end = min(pf_bytes, beg + per);
+    for (long long o = beg + threadIdx.x * 16384LL; o < end; o += blockDim.x * 16384LL)
+      ptx::prefetch_l2_bulk(pf + o, static_cast<uint32_t>(min(16384LL, end - o)));
+    return;
+  }
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -335,9 +355,10 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     const long long t_done = clock64();
     const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    // one pass over the logit row (32 columns per TMEM load): running max /
-    // argmax (strict '>' in ascending column order = lowest index on ties, R4)
-    // and online sum of exp(l - max), rescaled when the max moves.
+    // one pass over the logit row, 32 columns per TMEM load: columns >= E are
+    // masked to -inf; chunk max by a tree, argmax = the smallest column attaining
+    // it (lowest index on ties, R4) by a tree of index minima, then a running
+    // (max, sum exp(l - max)) pair rescaled when the max moves.
     constexpr float kLog2e = 1.4426950408889634f;
     float best = -INFINITY, lsel = 0.f, sum = 0.f;
     int best_e = 0;
@@ -348,41 +369,67 @@ __global__ void __launch_bounds__(192, 1)
       } else {
         uint32_t (&r16)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[0]);
         tmem_ld16(taddr + c0, r16);
+#pragma unroll
+        for (int j = 16; j < 32; ++j) r[j] = 0xff800000u;  // -inf
       }
       tmem_ld_wait();
-      const int w = min(32, EP - c0);
-      float cmax = -INFINITY;
-      int cidx = 0;
+      float v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (j < w && c0 + j < E) {
-          const float v = __uint_as_float(r[j]);
-          if (v > cmax) { cmax = v; cidx = c0 + j; }
-          if (c0 + j == sel) lsel = v;
-        }
+      for (int j = 0; j < 32; ++j) v[j] = (c0 + j < E) ? __uint_as_float(r[j]) : -INFINITY;
+      float m[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) m[j] = fmaxf(v[j], v[j + 16]);
+#pragma unroll
+      for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+        for (int j = 0; j < w; ++j) m[j] = fmaxf(m[j], m[j + w]);
+      const float cmax = m[0];
+      int ix[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        ix[j] = min(v[j] == cmax ? j : 32, v[j + 16] == cmax ? j + 16 : 32);
+#pragma unroll
+      for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+        for (int j = 0; j < w; ++j) ix[j] = min(ix[j], ix[j + w]);
+      if (sel >= c0 && sel < c0 + 32) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j == sel) lsel = v[j];
       }
       if (cmax > best) {
-        sum *= exp2f((best - cmax) * kLog2e);   // best = -inf on the first chunk -> 0 * 0
+        sum *= fast_exp2((best - cmax) * kLog2e);   // best = -inf on the first chunk -> 0
         best = cmax;
-        best_e = cidx;
+        best_e = c0 + ix[0];
       }
+      const float mb = best * kLog2e;
+      float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < w && c0 + j < E) sum += exp2f((__uint_as_float(r[j]) - best) * kLog2e);
+      for (int j = 0; j < 32; j += 4) {
+        p0 += fast_exp2(fmaf(v[j], kLog2e, -mb));
+        p1 += fast_exp2(fmaf(v[j + 1], kLog2e, -mb));
+        p2 += fast_exp2(fmaf(v[j + 2], kLog2e, -mb));
+        p3 += fast_exp2(fmaf(v[j + 3], kLog2e, -mb));
+      }
+      sum += (p0 + p1) + (p2 + p3);
     }
+    const long long t_loop = clock64();
     if (t < n) {
       RouteRec rec;
       rec.expert = sel >= 0 ? sel : best_e;
-      rec.gate = (sel >= 0 ? exp2f((lsel - best) * kLog2e) : 1.f) / sum;
+      rec.gate = (sel >= 0 ? fast_exp2((lsel - best) * kLog2e) : 1.f) / sum;
       out[t] = rec;
       atomicAdd(&s_hist[rec.expert], 1);
       if (bad) atomicExch(err_flag, 1);
     }
+    const long long t_store = clock64();
     asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+    const long long t_bar = clock64();
     for (int e = threadIdx.x; e < E; e += 128) hist_out[(size_t)blockIdx.x * E + e] = s_hist[e];
-    if (kT && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 40))
-      printf("[router cta %d] setup %lld mainloop %lld epilogue %lld\n", blockIdx.x,
-             t_setup - t_start, t_done - t_setup, clock64() - t_done);
+    if (kT && (threadIdx.x == 0 || threadIdx.x == 127) && (blockIdx.x == 0 || blockIdx.x == 40))
+      printf("[router cta %d t%d] setup %lld mainloop %lld softmax %lld store %lld bar %lld hist %lld\n",
+             blockIdx.x, threadIdx.x, t_setup - t_start, t_done - t_setup, t_loop - t_done,
+             t_store - t_loop, t_bar - t_store, clock64() - t_bar);
   }
   tc_fence_before();
   __syncthreads();
@@ -401,7 +448,10 @@ size_t router_tc_smem_bytes(int EP, bool mn) {
 cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
                              const void* w_r, void* wt_r, int n, int h, int E, int EP,
                              const int32_t* forced, RouteRec* out, int32_t* hist_out,
-                             int32_t* err_flag, cudaStream_t s) {
+                             int32_t* err_flag, const void* pf, long long pf_bytes, int pf_ctas,
+                             cudaStream_t s) {
+  const auto* pfb = static_cast<const uint8_t*>(pf);
+  if (pf == nullptr || pf_bytes < 16384) pf_ctas = 0;
   if (n <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -419,17 +469,17 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
     cudaFuncSetAttribute(router_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          RTC_SMEM_BUDGET + 2048);
     router_tc_kernel<true, true><<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP, true), s>>>(
-        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
+        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, 0LL);
   } else if (mn_major) {
-    return launch_pdl(router_tc_kernel<true>, dim3(ceil_div(n, 128)), dim3(192),
+    return launch_pdl(router_tc_kernel<true>, dim3(ceil_div(n, 128) + pf_ctas), dim3(192),
                       router_tc_smem_bytes(EP, true), s, tmX, tmW, n, h, E, EP, forced, out,
-                      hist_out, err_flag);
+                      hist_out, err_flag, pfb, pf_bytes);
   } else {
     dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
     router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,
                                        static_cast<__nv_bfloat16*>(wt_r));
-    router_tc_kernel<false><<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP, false), s>>>(
-        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
+    router_tc_kernel<false><<<ceil_div(n, 128) + pf_ctas, 192, router_tc_smem_bytes(EP, false), s>>>(
+        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, pf_bytes);
   }
   return cudaGetLastError();
 }

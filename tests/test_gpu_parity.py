@@ -220,6 +220,61 @@ def test_virtual_shards_sum_to_unsharded(G):
     assert O.max_abs_rel(acc.cpu().numpy(), y_ref) <= BF16_TOL
 
 
+# --------------------------------------------------------------------- full size, every config
+def _full_size_sampled(N, h, d_ff, E, seed, routing, **kw):
+    """A whole layer at BASELINE size through the C ABI; routing tables exact on
+    every token, outputs vs the oracle on a seeded sample covering every active
+    expert (first/last 2 tokens of each segment + 256 random tokens)."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    dev = "cuda"
+    x = W.make_tokens(seed, N, h, device=dev)
+    w_r = W.make_router_weight(seed, h, E, device=dev)
+    w_i, w_o = W.make_expert_weights(seed, E, h, d_ff, device=dev)
+    forced = W.draw_experts(seed, N, E, routing, device=dev, **kw)
+    L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16)
+    L.load_expert_shards(0, w_i, w_o)
+    y = L.forward(0, x, w_r, forced_expert=forced)
+    r = {k: v.cpu().numpy() for k, v in L.routing(N).items()}
+    L.check()
+    fc = forced.cpu().numpy().astype(np.int64)
+    np.testing.assert_array_equal(r["expert"], fc)
+    counts, offsets, perm = O.group_per_expert(fc, E)
+    np.testing.assert_array_equal(r["counts"], counts)
+    np.testing.assert_array_equal(r["offsets"], offsets)
+    np.testing.assert_array_equal(r["perm"], perm)
+    rng = np.random.default_rng(seed)
+    sample = set(rng.choice(N, 256, replace=False).tolist())
+    for e in range(E):
+        seg = perm[offsets[e]:offsets[e + 1]]
+        sample.update(seg[:2].tolist() + seg[-2:].tolist())
+    sample = np.array(sorted(sample))
+    y_s, rt = O.moe_layer_tokens(x[sample].cpu(), w_r.cpu(),
+                                 lambda e: (w_i[e].cpu(), w_o[e].cpu()), forced_rows=fc[sample])
+    np.testing.assert_allclose(r["gate"][sample], rt.gate, rtol=1e-5, atol=1e-6)
+    err = O.max_abs_rel(y[sample].float().cpu().numpy(), y_s)
+    assert err <= BF16_TOL, err
+    assert torch.isfinite(y).all() and (y.float().abs().sum(1) > 0).all()
+    L.close()
+    return err
+
+
+@pytest.mark.parametrize("routing,kw", [("zipf", {"s": 1.2}), ("uniform", {})])
+def test_c3_switch_base_128_full_size(routing, kw):
+    # BASELINE.json configs[2]: E=128, h=768, d_ff=3072, batch 32 x seq 512 = 16384 tokens
+    _full_size_sampled(16384, 768, 3072, 128, 3, routing, **kw)
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_c4_switch_base_256_pathological_full_size(k):
+    # BASELINE.json configs[3]: E=256, all tokens to k experts (253-255 empty experts)
+    _full_size_sampled(16384, 768, 3072, 256, 4, "patho", k=k)
+
+
+def test_c5_switch_large_128_full_size():
+    # BASELINE.json configs[4]: h=1024, d_ff=4096, E=128, batch 64 x seq 512 = 32768 tokens
+    _full_size_sampled(32768, 1024, 4096, 128, 5, "uniform")
+
+
 # --------------------------------------------------------------------- full size (bench config)
 @pytest.mark.parametrize("routing", ["uniform", "zipf"])
 def test_c2_full_size_sampled(routing):
