@@ -658,6 +658,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // -------------------------------------------------------------- token producer (both CTAs)
     const uint64_t pol_x = policy_evict_last();
     const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
+    int* s_rows = reinterpret_cast<int*>(
+        (reinterpret_cast<uintptr_t>(s_cs + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2;
     int stage = 0;
     uint32_t phase = 0;
     for (int u = cid; u < total; u += ncl) {
@@ -676,15 +678,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int half = ((w.ntok + 31) & ~31) / 2;
       const int nb = half / B2_BOX;
       const int r0 = w.tok0 + static_cast<int>(rank) * half;
+      const bool gather = !down && fp.up.gather != nullptr;
+      if (gather) {   // this CTA's token ids for the unit (padding rows read row 0; masked later)
+        __syncwarp();
+        for (int i = lane; i < half; i += 32)
+          s_rows[i] = (r0 + i < fp.up.n_rows) ? __ldg(fp.up.gather + r0 + i) : 0;
+        __syncwarp();
+      }
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&emptyB[stage], phase ^ 1);
         const uint32_t fb = leader_full + stage * 8;
         if (elect_one()) {
           if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * nb * B2_BOX * BK * 2);
           else mbar_arrive_cluster(fb);
-          for (int i = 0; i < nb; ++i)
-            tma_load_2d_2sm(tm, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
-                            r0 + i * B2_BOX, pol_x);
+          if (gather) {
+            // .shared::cta form: the leader's barrier is addressed by clearing the peer bit
+            const uint32_t fb_cta = smem_u32(&fullB[stage]) & 0xFEFFFFFFu;
+            for (int i = 0; i < half; i += 4)
+              tma_gather4_2sm(tm, fb_cta, sB + stage * B2_BYTES + i * (BK * 2), kb * BK,
+                              *reinterpret_cast<const int4*>(s_rows + i), pol_x);
+          } else {
+            for (int i = 0; i < nb; ++i)
+              tma_load_2d_2sm(tm, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
+                              r0 + i * B2_BOX, pol_x);
+          }
         }
         __syncwarp();
         if (++stage == BS) { stage = 0; phase ^= 1; }
@@ -802,7 +819,7 @@ int variant() {
 
 size_t smem_bytes_2sm(int E, int as, int bs) {
   return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (3 * E + 2) * 4 +
-         16 + 4 * 1024;
+         16 + 4 * 1024 + 128 * 4;   // + staging + gather row ids
 }
 
 template <bool kDown, int AS, int BS, bool kT = false>

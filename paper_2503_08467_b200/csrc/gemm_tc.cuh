@@ -28,6 +28,10 @@ struct TcParams {
   int ld_out;         // F (up) or h (down)
   const int32_t* perm;     // down: perm[j] = global token id of expert-ordered row j
   const RouteRec* route;   // down: gate per global token
+  // up, fused kernel: if gather != nullptr the token tile is gathered straight
+  // from x_all rows gather[j] (TMA gather4) instead of the expert-ordered copy
+  const int32_t* gather = nullptr;
+  int n_rows = 0;          // rows of the gathered tensor (N)
 };
 
 // tcgen05 router (router.cu): logits/softmax/top-1 per 128-token CTA, plus the
@@ -51,6 +55,8 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
 // The CTA-pair (cta_group::2) kernel is used when n_mt is even.
 // Both projections in one persistent CTA-pair launch (needs F/128 and h/128 even).
 // done: [E] int32 zeroed before the launch (Step 2 does it).
+// tmB_up: X_perm [N][h] box {64, 16} - or, when up.gather != nullptr, x_all [N][h]
+// box {64, 1} for TMA gather4.
 cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
                               const TcParams& up, const TcParams& dn, int32_t* done, int grid,

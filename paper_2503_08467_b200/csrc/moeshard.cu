@@ -455,6 +455,7 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   const int HB = c->use_tc ? 128 : 64;                 // tokens per hist-block
   const int nbr = (n + HB - 1) / HB;                    // hist-blocks per rank
   const int NB = (c->coll ? c->world : 1) * nbr;
+  const int N = (c->coll ? c->world : 1) * n;             // tokens of all ranks
   int32_t* my_hist = c->block_hist + (c->coll ? static_cast<size_t>(c->rank) * nbr * E : 0);
   if (c->use_tc) {
     CUtensorMap tm_x, tm_w;
@@ -489,22 +490,28 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     x_all = c->x_all;
   }
   c->mark(2, s);
-  // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs
+  const bool fused = c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_UNFUSED_GEMM) &&
+                     (F / kTcFeatTile) % 2 == 0 && (h / kTcFeatTile) % 2 == 0;
+  const bool gather = fused && (c->cfg.flags & MOESHARD_FLAG_TMA_GATHER);
+  CUtensorMap tm_xg;   // x_all rows for TMA gather4 (box {64, 1})
+  if (gather && !make_tmap(&tm_xg, x_all, h, N, 1))
+    return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for the gather map");
+  // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs (the row
+  // copy is skipped when the FFN gathers rows itself)
   launch_group_blocks(c->block_hist, NB, E, c->tb, F / kTcFeatTile, h / kTcFeatTile, c->route,
-                      x_all, n, nbr, HB, h * c->elt, c->perm, c->x_perm, s);
+                      x_all, n, nbr, HB, h * c->elt, c->perm, gather ? nullptr : c->x_perm, s);
   c->launches += 1;
   c->mark(3, s);
   // Step 4: expert computation, one grouped product per projection
   void* P = c->coll ? c->partial : hidden_out;
-  const bool fused = c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_UNFUSED_GEMM) &&
-                     (F / kTcFeatTile) % 2 == 0 && (h / kTcFeatTile) % 2 == 0;
   if (fused) {
     TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
-                static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
+                static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr,
+                gather ? c->perm : nullptr, N};
     TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
                 static_cast<__nv_bfloat16*>(P), h, c->perm, c->route};
-    CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, c->tm_xperm16, lw.tm_out, c->tm_H16, up, dn,
-                                  c->tb.done, c->num_sms, s));
+    CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather ? tm_xg : c->tm_xperm16, lw.tm_out, c->tm_H16,
+                                  up, dn, c->tb.done, c->num_sms, s));
     c->mark(4, s);
     c->launches += 1;
   } else if (c->use_tc) {

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     const int32_t* __restrict__ hist, int NB, int E, Tables tb, int n_mt_up_tc, int n_mt_down_tc,
     const RouteRec* __restrict__ route, const uint4* __restrict__ x_all, int n, int nbr, int HB,
     int32_t* __restrict__ perm, int row_vecs, uint4* __restrict__ x_perm) {
+  // x_perm == nullptr: the consumer gathers rows itself (TMA gather4); only perm/tables
   constexpr int kThreads = 1024 / kSplit;
   constexpr int kRowsPerWarp = 4;                 // rows copied per warp
   static_assert(kThreads >= 128, "ranks need 128 threads");
@@ -122,10 +123,11 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   ptx::griddep_launch_dependents();
   // issue this CTA's row loads first: the sources are known, only the
   // destinations depend on the scan below
+  const bool copy_rows = x_perm != nullptr;
   uint4 v[kRowsPerWarp][VPL];
 #pragma unroll
   for (int u = 0; u < kRowsPerWarp; ++u) {
-    const int tt = t0 + row_base + warp * kRowsPerWarp + u;
+    const int tt = copy_rows ? t0 + row_base + warp * kRowsPerWarp + u : t1;
 #pragma unroll
     for (int c = 0; c < VPL; ++c) {
       const int col = lane + 32 * c;
@@ -209,6 +211,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   }
   __syncthreads();
   // 3. row stores (rows loaded at the top)
+  if (!copy_rows) return;
   int jj[kRowsPerWarp];
 #pragma unroll
   for (int u = 0; u < kRowsPerWarp; ++u) jj[u] = s_j[row_base + warp * kRowsPerWarp + u];

@@ -157,6 +157,18 @@ __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* d, uint32_t b
       "l"(reinterpret_cast<uint64_t>(d)), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(hint)
       : "memory");
 }
+// TMA gather4 for a CTA pair: rows r.x..r.w (box {64 cols, 1 row}, 128-B swizzle)
+// land as 4 consecutive 128-B rows at smem_dst; completion on `bar_cluster`.
+__device__ __forceinline__ void tma_gather4_2sm(const CUtensorMap* d, uint32_t bar_cluster,
+                                                void* smem_dst, int col, int4 r, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      ".cta_group::2.L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(d)), "r"(col), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w),
+      "r"(bar_cluster), "l"(hint)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    smem_u32(dst_smem)),

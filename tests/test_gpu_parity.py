@@ -155,6 +155,15 @@ def test_fused_and_unfused_gemm_agree_bitwise():
     assert torch.equal(ys[0], ys[1])
 
 
+def test_tma_gather4_token_path_matches_oracle():
+    # experimental: the FFN gathers token rows by perm (TMA gather4) instead of X_perm
+    from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_TMA_GATHER
+    inp = W.make_layer_inputs(20, 1500, 256, 512, 16, dtype=torch.bfloat16, routing="zipf")
+    L, y, r = _run(inp, dtype=torch.bfloat16, flags=MOESHARD_FLAG_TMA_GATHER,
+                   forced=inp.forced.cuda().contiguous())
+    _check_layer(inp, y, r, tol=BF16_TOL)
+
+
 def test_forced_collectives_path_world1():
     # exercises AllGather / partial buffer / ReduceScatter through NCCL with one rank
     from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_FORCE_COLLECTIVES
