@@ -151,6 +151,10 @@ class MoEShardLayer:
         host_out.copy_(dev_out, non_blocking=True)
         return host_out
 
+    def host_streamer(self, n_local: int) -> "HostStreamer":
+        """Streaming inference from/to pinned host memory (see HostStreamer)."""
+        return HostStreamer(self, n_local)
+
     def check(self):
         C.moeshard_check(self.ctx, self._stream())
 
@@ -164,3 +168,53 @@ class MoEShardLayer:
             self.close()
         except Exception:
             pass
+
+
+class HostStreamer:
+    """Streams batches of tokens between pinned host memory and the layer.
+
+    step(k): the H2D copy of batch k runs on a copy stream, the forward on the
+    caller's stream, the D2H copy of its output on a second copy stream, with
+    two device buffers so the copies of neighbouring batches overlap the
+    forward of this one (PCIe is full duplex). join() makes the caller's stream
+    wait for every copy issued so far. Marshalling only: the forward is the
+    library's."""
+
+    def __init__(self, layer: MoEShardLayer, n_local: int):
+        self.layer = layer
+        dev = f"cuda:{layer.device}"
+        self.h2d = torch.cuda.Stream(device=dev)
+        self.d2h = torch.cuda.Stream(device=dev)
+        self.din = [torch.empty(n_local, layer.h, dtype=layer.dtype, device=dev) for _ in range(2)]
+        self.dout = [torch.empty_like(self.din[0]) for _ in range(2)]
+        self.in_ready = [torch.cuda.Event() for _ in range(2)]
+        self.fwd_done = [torch.cuda.Event() for _ in range(2)]
+        self.out_free = [torch.cuda.Event() for _ in range(2)]
+        self.k = 0
+
+    def step(self, layer_idx: int, host_in: torch.Tensor, router_w: torch.Tensor,
+             host_out: torch.Tensor, forced_expert: Optional[torch.Tensor] = None) -> torch.Tensor:
+        b = self.k % 2
+        comp = torch.cuda.current_stream()
+        if self.k >= 2:
+            self.h2d.wait_event(self.fwd_done[b])      # forward(k-2) finished reading din[b]
+        with torch.cuda.stream(self.h2d):
+            self.din[b].copy_(host_in, non_blocking=True)
+            self.in_ready[b].record(self.h2d)
+        comp.wait_event(self.in_ready[b])
+        if self.k >= 2:
+            comp.wait_event(self.out_free[b])          # D2H(k-2) finished reading dout[b]
+        self.layer.forward(layer_idx, self.din[b], router_w, forced_expert=forced_expert,
+                           out=self.dout[b])
+        self.fwd_done[b].record(comp)
+        self.d2h.wait_event(self.fwd_done[b])
+        with torch.cuda.stream(self.d2h):
+            host_out.copy_(self.dout[b], non_blocking=True)
+            self.out_free[b].record(self.d2h)
+        self.k += 1
+        return host_out
+
+    def join(self):
+        comp = torch.cuda.current_stream()
+        comp.wait_stream(self.h2d)
+        comp.wait_stream(self.d2h)

@@ -185,6 +185,28 @@ def test_empty_batch_and_n_below_max():
     _check_layer(inp, y, r, tol=BF16_TOL)
 
 
+def test_host_streamer_matches_device_forward():
+    # pipelined host->device->host streaming gives exactly the device-resident results
+    from paper_2503_08467_b200 import MoEShardLayer
+    N, h, d_ff, E = 512, 256, 512, 8
+    L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16)
+    inp = W.make_layer_inputs(21, N, h, d_ff, E, dtype=torch.bfloat16)
+    L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
+    w_r = inp.w_r.cuda()
+    xs = [W.make_tokens(30 + k, N, h) for k in range(5)]
+    host_in = [x.pin_memory() for x in xs]
+    host_out = [torch.empty_like(x).pin_memory() for x in xs]
+    st = L.host_streamer(N)
+    for k in range(5):
+        st.step(0, host_in[k], w_r, host_out[k])
+    st.join()
+    torch.cuda.synchronize()
+    for k in range(5):
+        ref = L.forward(0, xs[k].cuda(), w_r)
+        torch.cuda.synchronize()
+        assert torch.equal(host_out[k], ref.cpu())
+
+
 def test_forced_out_of_range_is_reported():
     from paper_2503_08467_b200 import MoEShardError, MoEShardLayer
     inp = W.make_layer_inputs(15, 64, 128, 128, 4, dtype=torch.bfloat16)
