@@ -205,6 +205,74 @@ def _config_json(cfg, args, G):
             "routing": "natural learned-style router (near-uniform); skewed = Zipf(1.2) forced"}
 
 
+# ------------------------------------------------------------------ encoder TTFT
+ENCODERS = {
+    "c3": dict(name="Switch-Base-128 encoder, 12 layers (6 MoE), batch 32 x seq 512 "
+                    "(BASELINE.json configs[2])",
+               d_model=768, d_ff=3072, n_heads=12, n_layers=12, n_experts=128, seq=512, batch=32),
+    "c5": dict(name="Switch-Large-128 encoder, 24 layers (12 MoE), batch 64 x seq 512 "
+                    "(BASELINE.json configs[4])",
+               d_model=1024, d_ff=4096, n_heads=16, n_layers=24, n_experts=128, seq=512, batch=64),
+}
+
+
+def encoder_ttft(name, G, rank, local, barrier, dist, reps=10):
+    """TTFT = one encoder forward over the batch, max over ranks:
+    torch attention / dense FFN replicated data-parallel, MoE FFNs through the
+    library. Also the MoE-layer share (TTFT_MoE) and the Zipf(1.2)-skewed TTFT."""
+    import torch
+    import workload as W
+    from harness.encoder import EncoderConfig, SwitchEncoder
+    from paper_2503_08467_b200 import MoEShardLayer
+    spec = dict(ENCODERS[name])
+    title = spec.pop("name")
+    cfg = EncoderConfig(**spec)
+    dev = f"cuda:{local}"
+    seed = SEED[name]
+    factory = lambda n_moe, n_local: MoEShardLayer(cfg.d_model, cfg.d_ff, cfg.n_experts,
+                                                   n_layers=n_moe, max_tokens_per_rank=n_local,
+                                                   dtype=torch.bfloat16, rank=rank, world=G,
+                                                   device=local)
+    enc = SwitchEncoder(cfg, seed=seed, rank=rank, world=G, device=dev, moe_layer_factory=factory)
+    b = cfg.batch // G
+    x = W.make_tokens(seed, b * cfg.seq, cfg.d_model, device=dev,
+                      token_offset=rank * b * cfg.seq).view(b, cfg.seq, cfg.d_model)
+    n_local = b * cfg.seq
+    N = n_local * G
+    zipf = [W.draw_experts(seed, N, cfg.n_experts, "zipf", device=dev, s=1.2, layer=j)
+            [rank * n_local:(rank + 1) * n_local].contiguous() for j in range(len(enc.moe_ids))]
+    stream = torch.cuda.current_stream()
+
+    def run(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        barrier()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record(stream)
+        for _ in range(reps):
+            fn()
+        en.record(stream)
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / reps
+        if G > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms
+
+    ttft = run(lambda: enc.forward(x))
+    ttft_skew = run(lambda: enc.forward(x, forced=zipf))
+    y = torch.randn(n_local, cfg.d_model, device=dev, dtype=torch.bfloat16)
+    moe_only = run(lambda: [enc.moe.forward(j, y, enc.layers[i]["w_r"])
+                            for j, i in enumerate(enc.moe_ids)])
+    enc.moe.close()
+    return {"workload": title, "ttft_ms": ttft, "ttft_ms_zipf": ttft_skew,
+            "ttft_moe_ms": moe_only, "moe_layers": len(enc.moe_ids), "reps": reps,
+            "tokens": N, "note": "non-MoE blocks are torch (cuBLAS/SDPA) replicated on every rank; "
+                                 "MoE FFNs are libmoeshard; T5 relative bias omitted"}
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -215,6 +283,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--encoder", default="c3", choices=["c3", "c5", "none"],
+                    help="also time the MoE-encoder TTFT of this stack (BASELINE.json configs[2]/[4])")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
@@ -419,6 +489,8 @@ def main():
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if args.encoder != "none":
+        line["encoder_ttft"] = encoder_ttft(args.encoder, G, rank, local, barrier, dist)
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, seed, device=dev)

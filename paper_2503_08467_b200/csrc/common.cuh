@@ -91,9 +91,11 @@ void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int 
 
 // Step 2 from the routers' per-block histograms, one launch: one CTA per
 // hist-block of HB <= 128 tokens (offsets, stable scatter, row gather).
-void launch_group_blocks(const int32_t* hist, int NB, int E, Tables tb, int n_mt_up_tc,
-                         int n_mt_down_tc, const RouteRec* route, const void* x_all, int n, int nbr,
-                         int HB, int row_bytes, int32_t* perm, void* x_perm, cudaStream_t s);
+// base [NB][E] and tot [E] are workspace outputs of the block scan.
+void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int32_t* tot,
+                         Tables tb, int n_mt_up_tc, int n_mt_down_tc, const RouteRec* route,
+                         const void* x_all, int n, int nbr, int HB, int row_bytes, int32_t* perm,
+                         void* x_perm, cudaStream_t s);
 
 void launch_transpose(int dtype, const void* src, void* dst, int batch, int rows, int cols,
                       cudaStream_t s);

@@ -140,7 +140,7 @@ Layout make_layout(const moeshard_config& c, int world) {
   L.route = take(Nmax * sizeof(RouteRec));
   L.block_hist = take(nb * E * 4);
   L.block_base = take(nb * E * 4);
-  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E);
+  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + E);
   L.ints = take(L.n_ints * 4);
   L.perm = take(Nmax * 4);
   L.x_all = coll ? take(Nmax * h * elt) : 0;
@@ -168,7 +168,7 @@ struct moeshard_ctx {
   Layout L{};
   char* ws = nullptr;
   RouteRec* route = nullptr;
-  int32_t *block_hist = nullptr, *block_base = nullptr, *perm = nullptr;
+  int32_t *block_hist = nullptr, *block_base = nullptr, *block_tot = nullptr, *perm = nullptr;
   Tables tb{};
   void *x_all = nullptr, *x_perm = nullptr, *H = nullptr, *partial = nullptr;
   CUtensorMap tm_xperm{}, tm_H{}, tm_xperm16{}, tm_H16{}, tm_wt_r{};
@@ -350,6 +350,7 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->tb.simt_chunk_pref = c->tb.tc_chunk_size + E;
   c->tb.stats = c->tb.simt_chunk_pref + (E + 1);
   c->tb.done = c->tb.stats + 8;
+  c->block_tot = c->tb.done + E;
   c->perm = reinterpret_cast<int32_t*>(c->ws + L.perm);
   c->x_all = c->coll ? c->ws + L.x_all : nullptr;
   c->x_perm = c->ws + L.x_perm;
@@ -498,9 +499,10 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for the gather map");
   // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs (the row
   // copy is skipped when the FFN gathers rows itself)
-  launch_group_blocks(c->block_hist, NB, E, c->tb, F / kTcFeatTile, h / kTcFeatTile, c->route,
-                      x_all, n, nbr, HB, h * c->elt, c->perm, gather ? nullptr : c->x_perm, s);
-  c->launches += 1;
+  launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb, F / kTcFeatTile,
+                      h / kTcFeatTile, c->route, x_all, n, nbr, HB, h * c->elt, c->perm,
+                      gather ? nullptr : c->x_perm, s);
+  c->launches += 2;
   c->mark(3, s);
   // Step 4: expert computation, one grouped product per projection
   void* P = c->coll ? c->partial : hidden_out;

@@ -86,12 +86,34 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
 // [r*n + i*HB, min(r*n + (i+1)*HB, (r+1)*n)) with r = b / nbr, i = b % nbr.
 // ===========================================================================
 
+// One CTA per expert: exclusive prefix of hist[.][e] over the NB blocks ->
+// base[b][e] (tokens of expert e in blocks before b) and tot[e]. O(NB*E)
+// in total, so the grouping CTAs read only 2*E values each.
+__global__ void __launch_bounds__(128) group_block_scan(const int32_t* __restrict__ hist, int NB,
+                                                        int E, int32_t* __restrict__ base,
+                                                        int32_t* __restrict__ tot) {
+  ptx::griddep_wait();                 // hist comes from the router (or the AllGather)
+  ptx::griddep_launch_dependents();
+  __shared__ int32_t s_warp[33];
+  const int e = blockIdx.x;
+  const int q = ceil_div(NB, 128);
+  const int b0 = threadIdx.x * q, b1 = min(NB, b0 + q);
+  int sum = 0;
+  for (int b = b0; b < b1; ++b) sum += __ldg(hist + (size_t)b * E + e);
+  int total;
+  int run = block_excl_scan<128>(sum, s_warp, total);
+  for (int b = b0; b < b1; ++b) {
+    base[(size_t)b * E + e] = run;
+    run += __ldg(hist + (size_t)b * E + e);
+  }
+  if (threadIdx.x == 0) tot[e] = total;
+}
+
 // One CTA per hist-block (HB <= 128 tokens; 1024 threads), the whole of
 // Step 2 in one launch:
-//  1. every CTA reduces the [NB][E] histogram array itself: totals per
-//     expert and the count of expert e in earlier blocks (NB*E is small:
-//     16 KB for the bench workload), then offsets = exclusive scan of totals;
-//     CTA 0 also publishes counts / offsets / tile tables / work counters;
+//  1. totals and earlier-block counts come from group_block_scan; offsets =
+//     exclusive scan of the totals; CTA 0 also publishes counts / offsets /
+//     tile tables / work counters;
 //  2. warps 0-3 give each token its stable rank inside the block
 //     (match_any) -> j = offsets[e] + earlier[e] + rank, perm[j] = t;
 //  3. all 32 warps copy the block's rows to X_perm[j] (16-B vectors, 4 rows
@@ -100,9 +122,10 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
 // 128/kSplit of its rows (spreads the row traffic over more SMs).
 template <int VPL, int kSplit>
 __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
-    const int32_t* __restrict__ hist, int NB, int E, Tables tb, int n_mt_up_tc, int n_mt_down_tc,
-    const RouteRec* __restrict__ route, const uint4* __restrict__ x_all, int n, int nbr, int HB,
-    int32_t* __restrict__ perm, int row_vecs, uint4* __restrict__ x_perm) {
+    const int32_t* __restrict__ bbase, const int32_t* __restrict__ btot, int E, Tables tb,
+    int n_mt_up_tc, int n_mt_down_tc, const RouteRec* __restrict__ route,
+    const uint4* __restrict__ x_all, int n, int nbr, int HB, int32_t* __restrict__ perm,
+    int row_vecs, uint4* __restrict__ x_perm) {
   // x_perm == nullptr: the consumer gathers rows itself (TMA gather4); only perm/tables
   constexpr int kThreads = 1024 / kSplit;
   constexpr int kRowsPerWarp = 4;                 // rows copied per warp
@@ -140,21 +163,10 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     e = (t < t1) ? __ldg(&route[t].expert) : -1;
   }
   for (int k = threadIdx.x; k < E; k += kThreads) {
-    s_tot[k] = 0;
-    s_pre[k] = 0;
+    s_tot[k] = __ldg(btot + k);                          // tokens of expert k overall
+    s_pre[k] = __ldg(bbase + (size_t)b * E + k);         // ... in blocks before this one
   }
   for (int k = threadIdx.x; k < 4 * E; k += kThreads) whist[k / E][k % E] = 0;
-  __syncthreads();
-  // 1. totals and earlier-block counts (consecutive threads -> consecutive experts)
-  const int total = NB * E;
-  for (int idx = threadIdx.x; idx < total; idx += kThreads) {
-    const int bb = idx / E, e = idx - bb * E;
-    const int v = __ldg(hist + idx);
-    if (v) {
-      atomicAdd(&s_tot[e], v);
-      if (bb < b) atomicAdd(&s_pre[e], v);
-    }
-  }
   __syncthreads();
   {
     const int e = threadIdx.x;
@@ -226,17 +238,19 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
 
 }  // namespace
 
-void launch_group_blocks(const int32_t* hist, int NB, int E, Tables tb, int n_mt_up_tc,
-                         int n_mt_down_tc, const RouteRec* route, const void* x_all, int n, int nbr,
-                         int HB, int row_bytes, int32_t* perm, void* x_perm, cudaStream_t s) {
+void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int32_t* tot,
+                         Tables tb, int n_mt_up_tc, int n_mt_down_tc, const RouteRec* route,
+                         const void* x_all, int n, int nbr, int HB, int row_bytes, int32_t* perm,
+                         void* x_perm, cudaStream_t s) {
   if (NB <= 0) return;
+  launch_pdl(group_block_scan, dim3(E), dim3(128), 0, s, hist, NB, E, base, tot);
   const int row_vecs = row_bytes / 16;
   const int vpl = ceil_div(row_vecs, 32);
   auto* xs = static_cast<const uint4*>(x_all);
   auto* xd = static_cast<uint4*>(x_perm);
   // each hist-block's rows are copied by kSplit = 4 CTAs of 256 threads
 #define SG(V)                                                                                    \
-  launch_pdl(group_scatter_gather<V, 4>, dim3(NB * 4), dim3(256), 0, s, hist, NB, E, tb,          \
+  launch_pdl(group_scatter_gather<V, 4>, dim3(NB * 4), dim3(256), 0, s, base, tot, E, tb,        \
              n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm, row_vecs, xd)
   switch (vpl) {
     case 1: SG(1); break;
