@@ -71,6 +71,7 @@ typedef enum {
 #define MOESHARD_FLAG_SIMT_GEMM 0x2u         /* bf16 mode: CUDA-core grouped GEMM (ablation / debug) */
 #define MOESHARD_FLAG_UNFUSED_GEMM 0x4u      /* bf16 mode: up and down products as two launches (ablation) */
 #define MOESHARD_FLAG_TMA_GATHER 0x8u        /* bf16 fused mode: gather token rows with TMA gather4 instead of X_perm (experimental, slower) */
+#define MOESHARD_FLAG_H_TRANSPOSED 0x10u     /* bf16 fused mode: keep H transposed, MN-major down operand (experimental, slower) */
 
 typedef struct {
   int32_t d_model;             /* h; multiple of 128 */

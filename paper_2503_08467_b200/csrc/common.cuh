@@ -16,6 +16,8 @@ constexpr int kTcTokTile = 256;       // max tokens per tcgen05 tile (UMMA N <= 
 constexpr int kTcFeatTile = 128;      // weight rows per tcgen05 tile (UMMA M)
 constexpr int kSimtTokTile = 64;      // tokens per SIMT tile
 constexpr int kSimtFeatTile = 64;     // output features per SIMT tile
+constexpr int kSegAlign = 32;         // expert segments in the internal expert-ordered layout
+                                      // start on multiples of 32 rows (padding rows unused)
 
 // Routing record of one token, gathered across ranks in one NCCL AllGather
 // (Step 2 metadata folded into the token exchange): expert id + gate bits.
@@ -33,6 +35,8 @@ struct Tables {
   int32_t* simt_chunk_pref;  // [E+1]
   int32_t* stats;          // [8]: 0 tiles_up, 1 tiles_down, 2 rows_up, 3 error flag
   int32_t* done;           // [E] up-projection tiles completed per expert (fused GEMM), zeroed by Step 2
+  int32_t* pos;            // [E+1] internal segment starts (exclusive scan of round_up(count, 32))
+  int32_t* perm_pad;       // [N + 32E] internal row -> global token id (padding rows: stale)
 };
 
 __device__ __forceinline__ float to_f32(float v) { return v; }
@@ -89,8 +93,9 @@ void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int 
                    const int32_t* forced, RouteRec* out, int32_t* hist_out, int32_t* err_flag,
                    cudaStream_t s);
 
-// Step 2 from the routers' per-block histograms, one launch: one CTA per
-// hist-block of HB <= 128 tokens (offsets, stable scatter, row gather).
+// Step 2 from the routers' per-block histograms: per-expert block scan, then one CTA
+// group per hist-block of HB <= 128 tokens (offsets, stable scatter to the compact
+// public perm and to the padded internal layout, row gather into X_perm).
 // base [NB][E] and tot [E] are workspace outputs of the block scan.
 void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int32_t* tot,
                          Tables tb, int n_mt_up_tc, int n_mt_down_tc, const RouteRec* route,

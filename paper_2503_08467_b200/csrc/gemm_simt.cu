@@ -8,9 +8,10 @@
 //   up:   H[j, f]          = relu( sum_k Xp[j, k] * WiT[e][f][k] )        (Step 4, 1st product)
 //   down: out[perm[j], c]  = gate[perm[j]] * sum_f H[j, f] * WoT[e][c][f] (2nd product, gate,
 //                                                                         un-permute scatter)
-// j runs over expert e's segment [offsets[e], offsets[e+1]) of the
-// expert-contiguous token order. Tiles: 64 tokens x 64 outputs x 32 K,
-// 256 threads each owning a 4x4 fp32 accumulator block; persistent
+// j runs over expert e's segment [pos[e], pos[e] + counts[e]) of the
+// expert-contiguous (32-row padded) internal token order; perm = perm_pad.
+// Tiles: 64 tokens x 64 outputs x 32 K, 256 threads each owning a 4x4 fp32
+// accumulator block; persistent
 // grid-stride loop over (expert, token-chunk, output-tile) units.
 #include "common.cuh"
 
@@ -49,10 +50,12 @@ __global__ void __launch_bounds__(256) simt_grouped_gemm(const T* __restrict__ A
   __shared__ __align__(16) float As[BK][BM + 4];
   __shared__ __align__(16) float Bs[BK][BN + 4];
   __shared__ int32_t s_pref[kMaxExperts + 1];
-  __shared__ int32_t s_off[kMaxExperts + 1];
+  __shared__ int32_t s_off[kMaxExperts + 1];   // internal (padded) segment starts
+  __shared__ int32_t s_cnt[kMaxExperts];
   for (int e = threadIdx.x; e <= E; e += blockDim.x) {
     s_pref[e] = tb.simt_chunk_pref[e];
-    s_off[e] = tb.offsets[e];
+    s_off[e] = tb.pos[e];
+    if (e < E) s_cnt[e] = tb.counts[e];
   }
   __syncthreads();
   const int n_nt = NOUT / BN;
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(256) simt_grouped_gemm(const T* __restrict__ A
     const int c = q - s_pref[e];
     const int nt = u - q * n_nt;
     const int row0 = s_off[e] + c * BM;
-    const int rows = min(BM, s_off[e + 1] - row0);
+    const int rows = min(BM, s_cnt[e] - c * BM);
     const int n0 = nt * BN;
     const T* Wte = Wt + (size_t)e * NOUT * K;
 

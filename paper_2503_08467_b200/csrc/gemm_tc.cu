@@ -50,8 +50,10 @@ struct Unit {
   int e, mt, tok0, ntok;
 };
 
+// pref: cumulative chunks [E+1]; pos: internal segment starts; end: pos + count; csz: chunk size
 __device__ __forceinline__ Unit decode(int u, int n_mt, int E, const int32_t* pref,
-                                       const int32_t* off, const int32_t* csz) {
+                                       const int32_t* pos, const int32_t* end,
+                                       const int32_t* csz) {
   const int q = u / n_mt;
   int lo = 0, hi = E;
   while (hi - lo > 1) {
@@ -65,8 +67,8 @@ __device__ __forceinline__ Unit decode(int u, int n_mt, int E, const int32_t* pr
   w.mt = local / nch;
   const int c = local - w.mt * nch;
   const int cs = csz[lo];
-  w.tok0 = off[lo] + c * cs;
-  w.ntok = min(cs, off[lo + 1] - w.tok0);
+  w.tok0 = pos[lo] + c * cs;
+  w.ntok = min(cs, end[lo] - w.tok0);
   return w;
 }
 
@@ -79,6 +81,34 @@ template <bool kDown>
 __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok, int nmma,
                                            int fbase, uint32_t taddr, int lane, uint64_t pol_keep,
                                            __nv_bfloat16* stage) {
+  if (!kDown && p.ht) {
+    // H^T row f = fbase + lane: this thread owns it; 32 tokens per TMEM load -> 4 x 16 B
+    __nv_bfloat16* row = p.out + (size_t)(fbase + lane) * p.ld_ht + tok0;
+    for (int c0 = 0; c0 < nmma; c0 += 32) {
+      uint32_t r[32];
+      if (c0 + 16 < nmma) {
+        tmem_ld32(taddr + c0, r);
+      } else {
+        uint32_t (&r16)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[0]);
+        tmem_ld16(taddr + c0, r16);
+      }
+      tmem_ld_wait();
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const __nv_bfloat162 v = __floats2bfloat162_rn(fmaxf(__uint_as_float(r[2 * j]), 0.f),
+                                                       fmaxf(__uint_as_float(r[2 * j + 1]), 0.f));
+        pk[j] = *reinterpret_cast<const uint32_t*>(&v);
+      }
+      const int nv = min(32, nmma - c0);   // columns written (padding columns are harmless:
+#pragma unroll                              // they lie inside this expert's chunk or the tail)
+      for (int q = 0; q < 4; ++q)
+        if (q * 8 < nv && c0 + q * 8 < ntok)
+          st_v4_hint(row + c0 + q * 8, make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]),
+                     pol_keep);
+    }
+    return;
+  }
   uint16_t* st16 = reinterpret_cast<uint16_t*>(stage);
   for (int c0 = 0; c0 < nmma; c0 += 16) {
     uint32_t r[16];
@@ -149,14 +179,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int32_t* s_pref = reinterpret_cast<int32_t*>(tmem_slot + 4);
-  int32_t* s_off = s_pref + (p.E + 1);
+  int32_t* s_off = s_pref + (p.E + 1);   // internal segment starts (pos)
   int32_t* s_cs = s_off + (p.E + 1);
+  int32_t* s_end = s_cs + p.E;           // pos + count
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i <= p.E; i += kThreads) {
     s_pref[i] = p.tb.tc_chunk_pref[i];
-    s_off[i] = p.tb.offsets[i];
-    if (i < p.E) s_cs[i] = p.tb.tc_chunk_size[i];
+    s_off[i] = p.tb.pos[i];
+    if (i < p.E) {
+      s_cs[i] = p.tb.tc_chunk_size[i];
+      s_end[i] = p.tb.pos[i] + p.tb.counts[i];
+    }
   }
   if (warp == 3 && lane == 0) tma_prefetch_desc(&tmB);
   if (warp == 1 && lane == 0) {
@@ -192,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       long long t_blk = 0, t_all = clock64();
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_cs);
+        const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
         const __nv_bfloat16* tiles =
             p.a_tiles + (static_cast<size_t>(w.e) * n_mt + w.mt) * nkb * (BM * BK);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -220,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       long long t_blk = 0, t_all = clock64();
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_cs);
+        const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
         const int nb = (w.ntok + B_BOX - 1) / B_BOX;
         for (int kb = 0; kb < nkb; ++kb) {
           TWAIT(t_blk, mbar_wait(&emptyB[stage], phase ^ 1));
@@ -250,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       long long t_a = 0, t_b = 0, t_t = 0, t_all = clock64();
       int units = 0;
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_cs);
+        const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
         const int nmma = (w.ntok + 15) & ~15;
         const uint32_t idesc = idesc_bf16_f32(BM, nmma);
         ++units;
@@ -295,13 +329,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // -------------------------------------------------------------- epilogue
     const int wq = warp & 3;
     __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(
-        (reinterpret_cast<uintptr_t>(s_cs + p.E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
+        (reinterpret_cast<uintptr_t>(s_end + p.E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
     const uint64_t pol_keep = policy_evict_last();  // H is re-read by the down product
     int as = 0;
     uint32_t aphase = 0;
     long long t_w = 0, t_all = clock64();
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
-      const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_cs);
+      const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
       TWAIT(t_w, mbar_wait(&tfull[as], aphase));
       tc_fence_after();
       const int f = w.mt * BM + wq * 32 + lane;
@@ -365,16 +399,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int32_t* s_pref = reinterpret_cast<int32_t*>(tmem_slot + 4);
-  int32_t* s_off = s_pref + (p.E + 1);
+  int32_t* s_off = s_pref + (p.E + 1);   // internal segment starts (pos)
   int32_t* s_cs = s_off + (p.E + 1);
+  int32_t* s_end = s_cs + p.E;           // pos + count
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   for (int i = threadIdx.x; i <= p.E; i += kThreads) {
     s_pref[i] = p.tb.tc_chunk_pref[i];
-    s_off[i] = p.tb.offsets[i];
-    if (i < p.E) s_cs[i] = p.tb.tc_chunk_size[i];
+    s_off[i] = p.tb.pos[i];
+    if (i < p.E) {
+      s_cs[i] = p.tb.tc_chunk_size[i];
+      s_end[i] = p.tb.pos[i] + p.tb.counts[i];
+    }
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -416,7 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       long long t_blk = 0, t_all = clock64();
       for (int u = cid; u < total; u += ncl) {
-        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_cs);
+        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
         const int mt = 2 * w.mt + static_cast<int>(rank);
         const int row0 = ((w.e * n_mt + mt) * nkb) * BM;
         for (int kb = 0; kb < nkb; ++kb) {
@@ -442,7 +480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = cid; u < total; u += ncl) {
-        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_cs);
+        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
         const int half = ((w.ntok + 31) & ~31) / 2;     // rows per CTA
         const int nb = half / B2_BOX;
         const int r0 = w.tok0 + static_cast<int>(rank) * half;
@@ -471,7 +509,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       long long t_a = 0, t_b = 0, t_t = 0, t_all = clock64();
       int units = 0;
       for (int u = cid; u < total; u += ncl) {
-        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_cs);
+        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
         const int nmma = (w.ntok + 31) & ~31;
         const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
         ++units;
@@ -508,14 +546,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // -------------------------------------------------------------- epilogue (both CTAs)
     const int wq = warp & 3;
     __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(
-        (reinterpret_cast<uintptr_t>(s_cs + p.E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
+        (reinterpret_cast<uintptr_t>(s_end + p.E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
     const uint64_t pol_keep = policy_evict_last();
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
     int as = 0;
     uint32_t aphase = 0;
     long long t_w = 0, t_all = clock64();
     for (int u = cid; u < total; u += ncl) {
-      const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_cs);
+      const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
       TWAIT(t_w, mbar_wait(&tfull[as], aphase));
       tc_fence_after();
       const int mt = 2 * w.mt + static_cast<int>(rank);
@@ -558,7 +596,8 @@ struct FusedParams {
   int32_t* done;  // [E], zeroed by Step 2 before every forward
 };
 
-template <int AS, int BS>
+// KA: 64-wide k-atoms per ring stage (1 or 2); a stage holds KA weight tiles and KA token tiles.
+template <int AS, int BS, int KA, bool kT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_moe_ffn_2sm(const __grid_constant__ CUtensorMap tmA_up, const __grid_constant__ CUtensorMap tmB_up,
                    const __grid_constant__ CUtensorMap tmA_dn, const __grid_constant__ CUtensorMap tmB_dn,
@@ -568,8 +607,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int E = fp.up.E;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + AS * A_BYTES;
-  uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + BS * B2_BYTES);
+  constexpr int SA_BYTES = KA * A_BYTES, SB_BYTES = KA * B2_BYTES;   // per stage
+  uint8_t* sB = smem + AS * SA_BYTES;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + BS * SB_BYTES);
   uint64_t* emptyA = fullA + AS;
   uint64_t* fullB = emptyA + AS;
   uint64_t* emptyB = fullB + BS;
@@ -577,8 +617,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int32_t* s_pref = reinterpret_cast<int32_t*>(tmem_slot + 4);
-  int32_t* s_off = s_pref + (E + 1);
+  int32_t* s_off = s_pref + (E + 1);     // internal segment starts (pos)
   int32_t* s_cs = s_off + (E + 1);
+  int32_t* s_end = s_cs + E;             // pos + count
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -612,8 +653,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   griddep_wait();
   for (int i = threadIdx.x; i <= E; i += kThreads) {
     s_pref[i] = fp.up.tb.tc_chunk_pref[i];
-    s_off[i] = fp.up.tb.offsets[i];
-    if (i < E) s_cs[i] = fp.up.tb.tc_chunk_size[i];
+    s_off[i] = fp.up.tb.pos[i];
+    if (i < E) {
+      s_cs[i] = fp.up.tb.tc_chunk_size[i];
+      s_end[i] = fp.up.tb.pos[i] + fp.up.tb.counts[i];
+    }
   }
   tc_fence_before();
   cluster_sync_all();
@@ -625,7 +669,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int chunks = s_pref[E];
   const int total_up = chunks * n_mp_up;
   const int total = total_up + chunks * n_mp_dn;
-  const int nkb_up = fp.up.K / BK, nkb_dn = fp.dn.K / BK;
+  const int nkb_up = fp.up.K / (BK * KA), nkb_dn = fp.dn.K / (BK * KA);   // stages per unit
   const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
 
   if (warp == 0) {
@@ -636,19 +680,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     for (int u = cid; u < total; u += ncl) {
       const bool down = u >= total_up;
-      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_cs);
+      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
       const int n_mt = down ? fp.dn.n_mt : fp.up.n_mt;
       const int nkb = down ? nkb_dn : nkb_up;
       const CUtensorMap* tm = down ? &tmA_dn : &tmA_up;
       const int mt = 2 * w.mt + static_cast<int>(rank);
-      const int row0 = ((w.e * n_mt + mt) * nkb) * BM;
+      const int row0 = ((w.e * n_mt + mt) * nkb * KA) * BM;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&emptyA[stage], phase ^ 1);
         const uint32_t fb = leader_full + stage * 8;
         if (elect_one()) {
-          if (leader) mbar_arrive_expect_tx(&fullA[stage], 2 * A_BYTES);
+          if (leader) mbar_arrive_expect_tx(&fullA[stage], 2 * SA_BYTES);
           else mbar_arrive_cluster(fb);
-          tma_load_2d_2sm(tm, fb, sA + stage * A_BYTES, 0, row0 + kb * BM, pol_w);
+#pragma unroll
+          for (int a = 0; a < KA; ++a)
+            tma_load_2d_2sm(tm, fb, sA + stage * SA_BYTES + a * A_BYTES, 0, row0 + (kb * KA + a) * BM,
+                            pol_w);
         }
         __syncwarp();
         if (++stage == AS) { stage = 0; phase ^= 1; }
@@ -659,12 +706,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint64_t pol_x = policy_evict_last();
     const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
     int* s_rows = reinterpret_cast<int*>(
-        (reinterpret_cast<uintptr_t>(s_cs + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2;
+        (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2;
     int stage = 0;
     uint32_t phase = 0;
     for (int u = cid; u < total; u += ncl) {
       const bool down = u >= total_up;
-      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_cs);
+      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
       const int nkb = down ? nkb_dn : nkb_up;
       const CUtensorMap* tm = down ? &tmB_dn : &tmB_up;
       if (down) {   // H rows of expert e complete? (acquire), then order the TMA after it
@@ -679,28 +726,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int nb = half / B2_BOX;
       const int r0 = w.tok0 + static_cast<int>(rank) * half;
       const bool gather = !down && fp.up.gather != nullptr;
+      const bool mn = down && fp.dn.ht;   // H^T: MN-major token tile, 64-token x 64-feature boxes
+      const int nbx = (half + 63) / 64;
+      const uint32_t stage_bytes = KA * (mn ? nbx * 8192 : nb * B2_BOX * BK * 2);
       if (gather) {   // this CTA's token ids for the unit (padding rows read row 0; masked later)
         __syncwarp();
         for (int i = lane; i < half; i += 32)
-          s_rows[i] = (r0 + i < fp.up.n_rows) ? __ldg(fp.up.gather + r0 + i) : 0;
+          s_rows[i] = (r0 + i < w.tok0 + w.ntok) ? __ldg(fp.up.gather + r0 + i) : 0;
         __syncwarp();
       }
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&emptyB[stage], phase ^ 1);
         const uint32_t fb = leader_full + stage * 8;
         if (elect_one()) {
-          if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * nb * B2_BOX * BK * 2);
+          if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * stage_bytes);
           else mbar_arrive_cluster(fb);
           if (gather) {
             // .shared::cta form: the leader's barrier is addressed by clearing the peer bit
             const uint32_t fb_cta = smem_u32(&fullB[stage]) & 0xFEFFFFFFu;
-            for (int i = 0; i < half; i += 4)
-              tma_gather4_2sm(tm, fb_cta, sB + stage * B2_BYTES + i * (BK * 2), kb * BK,
-                              *reinterpret_cast<const int4*>(s_rows + i), pol_x);
+            for (int a = 0; a < KA; ++a)
+              for (int i = 0; i < half; i += 4)
+                tma_gather4_2sm(tm, fb_cta, sB + stage * SB_BYTES + a * B2_BYTES + i * (BK * 2),
+                                (kb * KA + a) * BK, *reinterpret_cast<const int4*>(s_rows + i), pol_x);
+          } else if (mn) {
+            for (int a = 0; a < KA; ++a)
+              for (int j = 0; j < nbx; ++j)
+                tma_load_2d_2sm(tm, fb, sB + stage * SB_BYTES + a * B2_BYTES + j * 8192, r0 + 64 * j,
+                                (kb * KA + a) * BK, pol_x);
           } else {
-            for (int i = 0; i < nb; ++i)
-              tma_load_2d_2sm(tm, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
-                              r0 + i * B2_BOX, pol_x);
+            for (int a = 0; a < KA; ++a)
+              for (int i = 0; i < nb; ++i)
+                tma_load_2d_2sm(tm, fb, sB + stage * SB_BYTES + a * B2_BYTES + i * (B2_BOX * BK * 2),
+                                (kb * KA + a) * BK, r0 + i * B2_BOX, pol_x);
           }
         }
         __syncwarp();
@@ -714,25 +771,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t pa = 0, pb = 0;
       int as = 0;
       uint32_t aphase = 0;
+      long long t_a = 0, t_b = 0, t_t = 0, t_all = clock64(), t_first_down = 0;
+      int n_up = 0, n_dn = 0, kb_total = 0;
       for (int u = cid; u < total; u += ncl) {
         const bool down = u >= total_up;
-        const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_cs);
+        if (kT) { if (down) { if (!n_dn) t_first_down = clock64() - t_all; ++n_dn; } else ++n_up; }
+        const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
         const int nkb = down ? nkb_dn : nkb_up;
         const int nmma = (w.ntok + 31) & ~31;
-        const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
-        mbar_wait(&tempty[as], aphase ^ 1);
+        const bool mn = down && fp.dn.ht;
+        const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma, mn);
+        const uint32_t bstep = mn ? 128 : 2;   // K=16 step: 16 rows x 128 B (MN) or 32 B (K)
+        if (kT) { TWAIT(t_t, mbar_wait(&tempty[as], aphase ^ 1)); } else mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + as * BN_MAX;
+        if (kT) kb_total += nkb;
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&fullB[sb], pb);
-          mbar_wait(&fullA[sa], pa);
+          if (kT) { TWAIT(t_b, mbar_wait(&fullB[sb], pb)); TWAIT(t_a, mbar_wait(&fullA[sa], pa)); }
+          else { mbar_wait(&fullB[sb], pb); mbar_wait(&fullA[sa], pa); }
           tc_fence_after();
-          const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
-          const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B2_BYTES));
           if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              mma_bf16_ss_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            for (int a = 0; a < KA; ++a) {
+              const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * SA_BYTES + a * A_BYTES));
+              const uint32_t baddr = smem_u32(sB + sb * SB_BYTES + a * B2_BYTES);
+              const uint64_t bd = mn ? smem_desc_mn_sw128(baddr, 8192) : smem_desc_k_sw128(baddr);
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                mma_bf16_ss_2sm(d, ad + 2 * k, bd + bstep * k, idesc, (kb | a | k) != 0);
+            }
             mma_commit_2sm(&emptyA[sa], 0x3);
             mma_commit_2sm(&emptyB[sb], 0x3);
           }
@@ -745,19 +812,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         as ^= 1;
         if (as == 0) aphase ^= 1;
       }
+      if (kT && lane == 0)
+        printf("[ffn c%02d] up %d dn %d kb %d total %lld first_down %lld waitA %lld waitB %lld waitT %lld\n",
+               cid, n_up, n_dn, kb_total, clock64() - t_all, t_first_down, t_a, t_b, t_t);
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
     const int wq = warp & 3;
     __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(
-        (reinterpret_cast<uintptr_t>(s_cs + E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
+        (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
     const uint64_t pol_keep = policy_evict_last();
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
     int as = 0;
     uint32_t aphase = 0;
     for (int u = cid; u < total; u += ncl) {
       const bool down = u >= total_up;
-      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_cs);
+      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const int mt = 2 * w.mt + static_cast<int>(rank);
@@ -788,7 +858,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 size_t smem_bytes(int E, int as, int bs) {
-  return 1024 + as * A_BYTES + bs * B_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (3 * E + 2) * 4 +
+  return 1024 + as * A_BYTES + bs * B_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (4 * E + 2) * 4 +
          16 + 4 * 1024;
 }
 
@@ -818,7 +888,7 @@ int variant() {
 }
 
 size_t smem_bytes_2sm(int E, int as, int bs) {
-  return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (3 * E + 2) * 4 +
+  return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (4 * E + 2) * 4 +
          16 + 4 * 1024 + 128 * 4;   // + staging + gather row ids
 }
 
@@ -863,22 +933,35 @@ cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUten
 
 }  // namespace
 
-cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
-                              const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
-                              const TcParams& up, const TcParams& dn, int32_t* done, int grid,
-                              cudaStream_t s) {
-  constexpr int AS = 6, BS = 6;
+namespace {
+template <int AS, int BS, int KA, bool kT = false>
+cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
+                         const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn, const TcParams& up,
+                         const TcParams& dn, int32_t* done, int grid, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS>,
+    cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS, KA, kT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_bytes_2sm(kMaxExperts, AS, BS)));
+                                         static_cast<int>(smem_bytes_2sm(kMaxExperts, AS * KA, BS * KA)));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   FusedParams fp{up, dn, done};
-  return launch_pdl(tc_moe_ffn_2sm<AS, BS>, dim3(grid & ~1), dim3(kThreads),
-                    smem_bytes_2sm(up.E, AS, BS), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
+  return launch_pdl(tc_moe_ffn_2sm<AS, BS, KA, kT>, dim3(grid & ~1), dim3(kThreads),
+                    smem_bytes_2sm(up.E, AS * KA, BS * KA), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
+}
+}  // namespace
+
+cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
+                              const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
+                              const TcParams& up, const TcParams& dn, int32_t* done, int grid,
+                              cudaStream_t s) {
+  // MOESHARD_TC_VARIANT 20: two k-atoms per ring stage (3 + 3 stages of 32 KB)
+  if (variant() == 21)
+    return launch_fused<6, 6, 1, true>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, grid, s);
+  if (variant() == 20 && up.K % 128 == 0 && dn.K % 128 == 0)
+    return launch_fused<3, 3, 2>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, grid, s);
+  return launch_fused<6, 6, 1>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, grid, s);
 }
 
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,

@@ -32,6 +32,11 @@ struct TcParams {
   // from x_all rows gather[j] (TMA gather4) instead of the expert-ordered copy
   const int32_t* gather = nullptr;
   int n_rows = 0;          // rows of the gathered tensor (N)
+  // fused kernel: H stored transposed, H^T [F][ld_ht] (tokens contiguous). The up
+  // epilogue then writes each feature row directly; the down product reads it as
+  // an MN-major B operand.
+  bool ht = false;
+  int ld_ht = 0;           // token stride of H^T (N_max)
 };
 
 // tcgen05 router (router.cu): logits/softmax/top-1 per 128-token CTA, plus the

@@ -118,8 +118,9 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 // Workspace carve-up, shared by moeshard_workspace_size and moeshard_init.
 struct Layout {
-  size_t wt_r, route, block_hist, block_base, ints, perm, x_all, x_perm, H, partial, total;
+  size_t wt_r, route, block_hist, block_base, ints, perm, perm_pad, x_all, x_perm, H, partial, total;
   int n_ints;
+  size_t npad;   // rows of the internal expert-ordered layout: N_max + 32 per expert, rounded to 64
 };
 
 Layout make_layout(const moeshard_config& c, int world) {
@@ -140,12 +141,14 @@ Layout make_layout(const moeshard_config& c, int world) {
   L.route = take(Nmax * sizeof(RouteRec));
   L.block_hist = take(nb * E * 4);
   L.block_base = take(nb * E * 4);
-  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + E);
+  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + E + (E + 1));
+  L.npad = (Nmax + kSegAlign * E + 63) / 64 * 64;
   L.ints = take(L.n_ints * 4);
   L.perm = take(Nmax * 4);
+  L.perm_pad = take(L.npad * 4);
   L.x_all = coll ? take(Nmax * h * elt) : 0;
-  L.x_perm = take(Nmax * h * elt);
-  L.H = take(Nmax * F * elt);
+  L.x_perm = take(L.npad * h * elt);
+  L.H = take(L.npad * F * elt);
   L.partial = coll ? take(Nmax * h * elt) : 0;
   L.total = off;
   return L;
@@ -171,7 +174,7 @@ struct moeshard_ctx {
   int32_t *block_hist = nullptr, *block_base = nullptr, *block_tot = nullptr, *perm = nullptr;
   Tables tb{};
   void *x_all = nullptr, *x_perm = nullptr, *H = nullptr, *partial = nullptr;
-  CUtensorMap tm_xperm{}, tm_H{}, tm_xperm16{}, tm_H16{}, tm_wt_r{};
+  CUtensorMap tm_xperm{}, tm_H{}, tm_xperm16{}, tm_H16{}, tm_Ht{}, tm_wt_r{};
   void* wt_r = nullptr;
   int EP = 16;
   std::vector<LayerW> layers;
@@ -351,6 +354,8 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->tb.stats = c->tb.simt_chunk_pref + (E + 1);
   c->tb.done = c->tb.stats + 8;
   c->block_tot = c->tb.done + E;
+  c->tb.pos = c->block_tot + E;
+  c->tb.perm_pad = reinterpret_cast<int32_t*>(c->ws + L.perm_pad);
   c->perm = reinterpret_cast<int32_t*>(c->ws + L.perm);
   c->x_all = c->coll ? c->ws + L.x_all : nullptr;
   c->x_perm = c->ws + L.x_perm;
@@ -364,10 +369,12 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   }
   const int Nmax = world * cfg->max_tokens_per_rank;
   if (c->use_tc && Nmax > 0) {
-    if (!make_tmap(&c->tm_xperm, c->x_perm, c->h, Nmax, 32) ||
-        !make_tmap(&c->tm_H, c->H, c->F, Nmax, 32) ||
-        !make_tmap(&c->tm_xperm16, c->x_perm, c->h, Nmax, 16) ||
-        !make_tmap(&c->tm_H16, c->H, c->F, Nmax, 16) ||
+    const uint64_t np = L.npad;
+    if (!make_tmap(&c->tm_xperm, c->x_perm, c->h, np, 32) ||
+        !make_tmap(&c->tm_H, c->H, c->F, np, 32) ||
+        !make_tmap(&c->tm_xperm16, c->x_perm, c->h, np, 16) ||
+        !make_tmap(&c->tm_H16, c->H, c->F, np, 16) ||
+        !make_tmap(&c->tm_Ht, c->H, np, c->F, 64) ||   // H^T [F][npad], 64 tokens x 64 features
         !make_tmap(&c->tm_wt_r, c->wt_r, c->h, c->EP, c->EP)) {
       delete c;
       return fail(nullptr, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
@@ -507,13 +514,17 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   // Step 4: expert computation, one grouped product per projection
   void* P = c->coll ? c->partial : hidden_out;
   if (fused) {
+    // MOESHARD_FLAG_H_TRANSPOSED (experimental): H stored as H^T [F][npad]; the up epilogue
+    // writes feature rows directly and the down product reads an MN-major token tile
+    const bool ht = (c->cfg.flags & MOESHARD_FLAG_H_TRANSPOSED) != 0;
+    const int np = static_cast<int>(c->L.npad);
     TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
                 static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr,
-                gather ? c->perm : nullptr, N};
+                gather ? c->tb.perm_pad : nullptr, N, ht, np};
     TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
-                static_cast<__nv_bfloat16*>(P), h, c->perm, c->route};
-    CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather ? tm_xg : c->tm_xperm16, lw.tm_out, c->tm_H16,
-                                  up, dn, c->tb.done, c->num_sms, s));
+                static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route, nullptr, 0, ht, np};
+    CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather ? tm_xg : c->tm_xperm16, lw.tm_out,
+                                  ht ? c->tm_Ht : c->tm_H16, up, dn, c->tb.done, c->num_sms, s));
     c->mark(4, s);
     c->launches += 1;
   } else if (c->use_tc) {
@@ -522,13 +533,13 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     CUDA_TRY(c, launch_tc_gemm(false, lw.tm_in, c->tm_xperm, c->tm_xperm16, up, c->num_sms, s));
     c->mark(4, s);
     TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
-                static_cast<__nv_bfloat16*>(P), h, c->perm, c->route};
+                static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
     CUDA_TRY(c, launch_tc_gemm(true, lw.tm_out, c->tm_H, c->tm_H16, dn, c->num_sms, s));
     c->launches += 2;
   } else {
     launch_simt_up(c->cfg.dtype, c->x_perm, lw.wt_in, h, F, E, c->tb, c->H, c->num_sms, s);
     c->mark(4, s);
-    launch_simt_down(c->cfg.dtype, c->H, lw.wt_out, F, h, E, c->tb, c->perm, c->route, P,
+    launch_simt_down(c->cfg.dtype, c->H, lw.wt_out, F, h, E, c->tb, c->tb.perm_pad, c->route, P,
                      c->num_sms, s);
     c->launches += 2;
   }

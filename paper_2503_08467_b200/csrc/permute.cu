@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   static_assert(kThreads >= 128, "ranks need 128 threads");
   __shared__ int32_t s_tot[kMaxExperts];
   __shared__ int32_t s_pre[kMaxExperts];
-  __shared__ int32_t s_base[kMaxExperts];
+  __shared__ int32_t s_base[kMaxExperts];   // compact (public perm) position of this block's first e
+  __shared__ int32_t s_bpad[kMaxExperts];   // padded internal position
   __shared__ int32_t whist[4][kMaxExperts];
   __shared__ int32_t s_j[128];
   __shared__ int32_t s_warp[33];
@@ -177,9 +178,13 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
       rows = nc > 0 ? (cnt / cs) * cs + round_up(cnt % cs, 32) : 0;
       sc = ceil_div(cnt, kSimtTokTile);
     }
-    int tot_cnt;
+    int tot_cnt, tot_pad;
     const int off = block_excl_scan<kThreads>(cnt, s_warp, tot_cnt);
-    if (e < E) s_base[e] = off + s_pre[e];
+    const int pos = block_excl_scan<kThreads>(round_up(cnt, kSegAlign), s_warp, tot_pad);
+    if (e < E) {
+      s_base[e] = off + s_pre[e];
+      s_bpad[e] = pos + s_pre[e];
+    }
     if (blockIdx.x == 0) {  // publish the tables the grouped GEMMs read
       int tot_tc, tot_sc, tot_rows;
       const int tcp = block_excl_scan<kThreads>(nc, s_warp, tot_tc);
@@ -187,6 +192,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
       block_excl_scan<kThreads>(rows, s_warp, tot_rows);
       if (e < E) {
         tb.done[e] = 0;
+        tb.pos[e] = pos;
         tb.counts[e] = cnt;
         tb.tc_chunk_size[e] = cs;
         tb.offsets[e] = off;
@@ -194,6 +200,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
         tb.simt_chunk_pref[e] = smp;
       }
       if (threadIdx.x == 0) {
+        tb.pos[E] = tot_pad;
         tb.offsets[E] = tot_cnt;
         tb.tc_chunk_pref[E] = tot_tc;
         tb.simt_chunk_pref[E] = tot_sc;
@@ -214,9 +221,13 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     if (e >= 0) {
       int before = 0;
       for (int w = 0; w < warp; ++w) before += whist[w][e];
-      const int j = s_base[e] + before + rank_w;
-      if (part == 0) perm[j] = t;
-      s_j[threadIdx.x] = j;
+      const int j = s_base[e] + before + rank_w;         // public, compact
+      const int jp = s_bpad[e] + before + rank_w;        // internal, padded segments
+      if (part == 0) {
+        perm[j] = t;
+        tb.perm_pad[jp] = t;
+      }
+      s_j[threadIdx.x] = jp;
     } else {
       s_j[threadIdx.x] = -1;
     }

@@ -22,6 +22,7 @@ MOESHARD_FLAG_FORCE_COLLECTIVES = 0x1
 MOESHARD_FLAG_SIMT_GEMM = 0x2
 MOESHARD_FLAG_UNFUSED_GEMM = 0x4
 MOESHARD_FLAG_TMA_GATHER = 0x8
+MOESHARD_FLAG_H_TRANSPOSED = 0x10
 
 STATUS = {
     0: "MOESHARD_OK", -1: "MOESHARD_ERR_INVALID_ARG", -2: "MOESHARD_ERR_SHAPE",

@@ -164,6 +164,15 @@ def test_tma_gather4_token_path_matches_oracle():
     _check_layer(inp, y, r, tol=BF16_TOL)
 
 
+def test_transposed_h_path_matches_oracle():
+    # experimental: H kept as H^T, the down product reads an MN-major token tile
+    from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_H_TRANSPOSED
+    inp = W.make_layer_inputs(22, 1700, 256, 512, 16, dtype=torch.bfloat16, routing="zipf")
+    L, y, r = _run(inp, dtype=torch.bfloat16, flags=MOESHARD_FLAG_H_TRANSPOSED,
+                   forced=inp.forced.cuda().contiguous())
+    _check_layer(inp, y, r, tol=BF16_TOL)
+
+
 def test_forced_collectives_path_world1():
     # exercises AllGather / partial buffer / ReduceScatter through NCCL with one rank
     from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_FORCE_COLLECTIVES
