@@ -53,54 +53,52 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks (NVML, during timed region)
 class ClockSampler:
-    REASONS = {
-        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
-        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
-    }
+    """nvidia-smi in a subprocess during the timed region (no GIL contention with the
+    launch loop): SM clock median, max clock and the throttle reasons seen."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown")
+    NAMES = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
 
     def __init__(self, dev_index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self.nv = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.002)
+        self.dev = dev_index
+        self.proc = None
+        self.rows = []
 
     def __enter__(self):
-        if self.nv is not None:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)   # let it start sampling before the timed region
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self.nv is not None:
-            self.t.join()
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) == 6 and f[0].isdigit():
+                self.rows.append(f)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                    "samples": 0}
-        s = sorted(self.samples)
-        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(s)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = sorted(int(r[0]) for r in self.rows)
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_min_mhz": sm[0], "sm_max_mhz": int(self.rows[0][1]),
+                "reasons": reasons, "samples": len(sm), "source": "nvidia-smi -lms 20"}
 
 
 # ------------------------------------------------------------------ CPU oracle timing
@@ -283,6 +281,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sustained", type=int, default=5000,
+                    help="steps of the extra sustained-load run (0 = skip); reported separately")
+    ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--encoder", default="c3", choices=["c3", "c5", "none"],
                     help="also time the MoE-encoder TTFT of this stack (BASELINE.json configs[2]/[4])")
     args = ap.parse_args()
@@ -368,13 +369,40 @@ def main():
             ms = t.item()
         return ms / steps
 
-    fwd = lambda k: layer.forward(k % NW, x, w_r, out=out)
-    fwd_skew = lambda k: layer.forward(k % NW, x, w_r, forced_expert=zipf, out=out)
+    fwd_eager = lambda k: layer.forward(k % NW, x, w_r, out=out)
+    fwd_skew_eager = lambda k: layer.forward(k % NW, x, w_r, forced_expert=zipf, out=out)
+    if args.eager:
+        fwd, fwd_skew = fwd_eager, fwd_skew_eager
+    else:
+        # one CUDA graph per weight set holding one forward (the library's launches are
+        # enqueue-only and graph-capturable); the timed loop replays one graph per step
+        def capture(fn):
+            graphs = []
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for l in range(NW):
+                    fn(l)   # warm the capture path
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            for l in range(NW):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    fn(l)
+                graphs.append(g)
+            return graphs
+        g_uni, g_skew = capture(fwd_eager), capture(fwd_skew_eager)
+        fwd = lambda k: g_uni[k % NW].replay()
+        fwd_skew = lambda k: g_skew[k % NW].replay()
 
     # --- main timed region (natural router, near-uniform routing)
     clk = ClockSampler(local)
     ms = timed(fwd, args.steps, args.warmup, sampler=clk)
-    launches = launch_count["timed"]
+    # library kernels per forward x steps (graph replays do not pass through the launch counter)
+    per_fwd = layer.stats()["kernel_launches"]
+    layer.forward(0, x, w_r, out=out)
+    per_fwd = layer.stats()["kernel_launches"] - per_fwd
+    launches = launch_count["timed"] if args.eager else per_fwd * args.steps
     st_uniform = layer.stats()
     r = layer.routing(n)
     counts = r["counts"].cpu()
@@ -386,10 +414,10 @@ def main():
     counts_z = layer.routing(n)["counts"].cpu()
     st_skew = layer.stats()
 
-    # --- per-kernel phase times (separate pass, phase events on the launch stream)
+    # --- per-kernel phase times (separate eager pass, phase events on the launch stream)
     layer.profile(True)
     for k in range(min(args.steps, 1000)):
-        fwd(k)
+        fwd_eager(k)
     ph, cnt = layer.phase_ms()
     layer.profile(False)
     ph_us = {k: 1e3 * v / max(cnt, 1) for k, v in ph.items()}
@@ -485,12 +513,20 @@ def main():
         "layer_roofline": layer_roof,
         "kernels_us": kernels,
         "gpu_launches": launches,
+        "timing_mode": "eager launches" if args.eager else "CUDA-graph replay of one forward per step",
         "clocks": clk.summary(),
     }
     if e2e is not None:
         line["e2e"] = e2e
     if args.encoder != "none":
         line["encoder_ttft"] = encoder_ttft(args.encoder, G, rank, local, barrier, dist)
+    if args.sustained > 0:
+        # long run at the end: after ~50-100 ms of this load the board reaches its power
+        # limit and sw_power_cap lowers SM clocks; reported, not the value
+        clk_s = ClockSampler(local)
+        ms_s = timed(fwd, args.sustained, 0, sampler=clk_s)
+        line["sustained"] = {"steps": args.sustained, "value": N / (ms_s * 1e-3),
+                             "ms_per_step": ms_s, "clocks": clk_s.summary()}
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, seed, device=dev)

@@ -622,6 +622,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   int32_t* s_end = s_cs + E;             // pos + count
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t g_entry = 0, g_ready = 0;
+  if (kT) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
@@ -664,6 +666,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch_dependents();
+  if (kT) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_ready));
 
   const int n_mp_up = fp.up.n_mt / 2, n_mp_dn = fp.dn.n_mt / 2;
   const int chunks = s_pref[E];
@@ -812,9 +815,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         as ^= 1;
         if (as == 0) aphase ^= 1;
       }
-      if (kT && lane == 0)
-        printf("[ffn c%02d] up %d dn %d kb %d total %lld first_down %lld waitA %lld waitB %lld waitT %lld\n",
-               cid, n_up, n_dn, kb_total, clock64() - t_all, t_first_down, t_a, t_b, t_t);
+      if (kT && lane == 0) {
+        uint64_t g_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+        printf("[ffn c%02d] up %d dn %d kb %d total %lld first_down %lld waitA %lld waitB %lld waitT %lld "
+               "g_entry %llu g_ready %llu g_end %llu\n",
+               cid, n_up, n_dn, kb_total, clock64() - t_all, t_first_down, t_a, t_b, t_t,
+               (unsigned long long)g_entry, (unsigned long long)g_ready, (unsigned long long)g_end);
+      }
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
