@@ -409,6 +409,22 @@ def main():
     e_active_u = int((counts > 0).sum())
     max_tok_u = int(counts.max())
 
+    # --- per-step distribution (event pair around every step, separate pass) and the
+    # eager-launch time of the same loop (median / p10 / p90, eager and graph)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        ev[k][0].record(stream)
+        fwd(k)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    per_step = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
+    pct = lambda q: round(per_step[min(len(per_step) - 1, int(q * len(per_step)))], 2)
+    dist_us = {"p10": pct(0.10), "p50": pct(0.50), "p90": pct(0.90), "max": round(per_step[-1], 2),
+               "note": "per-step event pairs, separate pass (includes ~1-2 us event overhead)"}
+    ms_eager = timed(fwd_eager, args.steps, args.warmup) if not args.eager else ms
+
     # --- skewed routing (Zipf 1.2, paper's replaced-router hook)
     ms_skew = timed(fwd_skew, args.steps, args.warmup)
     counts_z = layer.routing(n)["counts"].cpu()
@@ -514,6 +530,7 @@ def main():
         "kernels_us": kernels,
         "gpu_launches": launches,
         "timing_mode": "eager launches" if args.eager else "CUDA-graph replay of one forward per step",
+        "step_us": dict(dist_us, mean=round(ms * 1e3, 2), eager_mean=round(ms_eager * 1e3, 2)),
         "clocks": clk.summary(),
     }
     if e2e is not None:

@@ -110,18 +110,41 @@ __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok
     return;
   }
   uint16_t* st16 = reinterpret_cast<uint16_t*>(stage);
-  for (int c0 = 0; c0 < nmma; c0 += 16) {
-    uint32_t r[16];
-    tmem_ld16(taddr + c0, r);
-    tmem_ld_wait();
+  // down: the destination rows perm[j] and gates of the unit's tokens are fetched
+  // up front (lane holds tokens lane + 32 i), so the loop below has no dependent
+  // global loads - one perm latency and one gate latency per tile instead of one
+  // pair per 16 tokens (exposed when K is short, e.g. d_ff/G = 384)
+  int rows_r[BN_MAX / 32];
+  float g_r[BN_MAX / 32];
+  if (kDown) {
+#pragma unroll
+    for (int i = 0; i < BN_MAX / 32; ++i) {
+      const int tk = lane + 32 * i;
+      rows_r[i] = tk < ntok ? __ldg(p.perm + tok0 + tk) : 0;
+    }
+#pragma unroll
+    for (int i = 0; i < BN_MAX / 32; ++i) {
+      const int tk = lane + 32 * i;
+      g_r[i] = tk < ntok ? __ldg(&p.route[rows_r[i]].gate) : 0.f;
+    }
+  }
+  // TMEM reads are double-buffered: the load of columns c0+16.. is in flight while
+  // columns c0.. are converted and stored
+  uint32_t rbuf[2][16];
+  tmem_ld16(taddr, rbuf[0]);
+  tmem_ld_wait(rbuf[0]);
+#pragma unroll
+  for (int c0 = 0; c0 < BN_MAX; c0 += 16) {
+    if (c0 >= nmma) break;
+    uint32_t (&r)[16] = rbuf[(c0 / 16) & 1];
+    uint32_t (&rn)[16] = rbuf[((c0 / 16) + 1) & 1];
+    if (c0 + 16 < nmma) tmem_ld16(taddr + c0 + 16, rn);
     int row = 0;
     if (kDown) {
-      float g = 0.f;
-      const int tk = c0 + (lane & 15);
-      if (tk < ntok) {
-        row = p.perm[tok0 + tk];
-        g = p.route[row].gate;
-      }
+      // token c0 + (lane & 15) lives in lane (c0 & 16) + (lane & 15), register c0 / 32
+      const int src = (c0 & 16) + (lane & 15);
+      row = __shfl_sync(0xffffffffu, rows_r[c0 / 32], src);
+      const float g = __shfl_sync(0xffffffffu, g_r[c0 / 32], src);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float gj = __shfl_sync(0xffffffffu, g, j);
@@ -150,6 +173,7 @@ __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok
       }
     }
     __syncwarp();
+    if (c0 + 16 < nmma) tmem_ld_wait(rn);
   }
 }
 

@@ -13,7 +13,9 @@ import os
 from typing import Optional
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libmoeshard.so")
+# MOESHARD_LIB_PATH: another in-tree build of the same library (A/B experiments,
+# scripts/ab_lib.sh); the default is the package's own libmoeshard.so
+LIB_PATH = os.environ.get("MOESHARD_LIB_PATH") or os.path.join(PKG, "libmoeshard.so")
 
 MOESHARD_OK = 0
 MOESHARD_BF16 = 0

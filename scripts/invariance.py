@@ -1,0 +1,80 @@
+"""Per-rank load-balance invariance on ONE GPU (SURVEY.md §8(d) C4 checks 2-4).
+
+Rank g of a G-GPU MoEShard layer computes, after the AllGather, the Switch MoE
+layer of ALL N tokens against its d_ff/G column shard. That
+compute is a world=1 layer with d_ff/G and N tokens, so each virtual rank g is
+timed here on its own weight shard: per-rank compute time max/min, tile counts
+(exactly equal by construction) and skewed/uniform time ratios. Collectives are
+not included (one GPU). Writes one JSON document to stdout.
+"""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import workload as W
+from paper_2503_08467_b200 import MoEShardLayer, shard_columns
+
+CASES = {   # name: (E, h, d_ff, N, G, seed, routings)
+    "c4_g8": (256, 768, 3072, 16384, 8, 4, ["uniform", ("patho", {"k": 1}), ("patho", {"k": 3}), "skew",
+                                             ("zipf", {"s": 1.2})]),
+    "c2_g8": (64, 768, 3072, 8192, 8, 2, ["uniform", ("zipf", {"s": 1.2})]),
+    "c2_g4": (64, 768, 3072, 8192, 4, 2, ["uniform", ("zipf", {"s": 1.2})]),
+    "c2_g2": (64, 768, 3072, 8192, 2, 2, ["uniform", ("zipf", {"s": 1.2})]),
+}
+
+
+def time_fwd(L, x, w_r, forced, out, iters=50, warm=5):
+    for _ in range(warm):
+        L.forward(0, x, w_r, forced_expert=forced, out=out)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        L.forward(0, x, w_r, forced_expert=forced, out=out)
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters * 1e3   # us
+
+
+def main():
+    names = sys.argv[1:] or list(CASES)
+    res = {}
+    for name in names:
+        E, h, d_ff, N, G, seed, routings = CASES[name]
+        F = d_ff // G
+        x = W.make_tokens(seed, N, h, device="cuda")
+        w_r = W.make_router_weight(seed, h, E, device="cuda")
+        out = torch.empty_like(x)
+        layers = []
+        for g in range(G):
+            c0, c1 = shard_columns(d_ff, G, g)
+            L = MoEShardLayer(h, F, E, max_tokens_per_rank=N, dtype=torch.bfloat16)
+            wi, wo = W.make_expert_weights(seed, E, h, d_ff, cols=(c0, c1), device="cuda")
+            L.load_expert_shards(0, wi, wo)
+            del wi, wo
+            layers.append(L)
+        case = {"E": E, "h": h, "d_ff": d_ff, "N": N, "G": G, "d_ff_per_rank": F, "routings": {}}
+        for r in routings:
+            rname, kw = (r, {}) if isinstance(r, str) else r
+            forced = W.draw_experts(seed, N, E, rname, device="cuda", **kw)
+            label = rname + "".join(f"_{k}{v}" for k, v in kw.items())
+            t, tiles = [], []
+            for L in layers:
+                t.append(time_fwd(L, x, w_r, forced, out))
+                st = L.stats()
+                tiles.append((st["tiles_up"], st["tiles_down"]))
+            case["routings"][label] = {
+                "rank_us": [round(v, 2) for v in t], "max_over_min": round(max(t) / min(t), 4),
+                "tiles_equal_on_all_ranks": len(set(tiles)) == 1, "tiles": list(tiles[0]),
+                "experts_active": int((torch.bincount(forced.long(), minlength=E) > 0).sum())}
+        u = max(case["routings"]["uniform"]["rank_us"])
+        for k, v in case["routings"].items():
+            v["max_rank_time_over_uniform"] = round(max(v["rank_us"]) / u, 4)
+        for L in layers:
+            L.close()
+        res[name] = case
+        print(json.dumps({name: case}), file=sys.stderr, flush=True)
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -6,22 +6,30 @@ import torch
 from torch.profiler import profile, ProfilerActivity
 import workload as W
 from paper_2503_08467_b200 import MoEShardLayer
-E, h, d_ff, N, NW = 64, 768, 3072, 8192, 3
+import argparse
+ap = argparse.ArgumentParser()
+ap.add_argument("--E", type=int, default=64); ap.add_argument("--h", type=int, default=768)
+ap.add_argument("--dff", type=int, default=3072); ap.add_argument("--N", type=int, default=8192)
+ap.add_argument("--routing", default="natural"); ap.add_argument("--k", type=int, default=1)
+a = ap.parse_args()
+E, h, d_ff, N, NW = a.E, a.h, a.dff, a.N, 3
 L = MoEShardLayer(h, d_ff, E, n_layers=NW, max_tokens_per_rank=N)
 for l in range(NW):
     wi, wo = W.make_expert_weights(2, E, h, d_ff, device="cuda", layer=l); L.load_expert_shards(l, wi, wo); del wi, wo
 x = W.make_tokens(2, N, h, device="cuda"); w_r = W.make_router_weight(2, h, E, device="cuda")
 out = torch.empty_like(x)
-for k in range(30): L.forward(k % NW, x, w_r, out=out)
+forced = None if a.routing == "natural" else W.draw_experts(2, N, E, a.routing, device="cuda",
+                                                            **({"k": a.k} if a.routing == "patho" else {}))
+for k in range(30): L.forward(k % NW, x, w_r, forced_expert=forced, out=out)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as p:
-    for k in range(12): L.forward(k % NW, x, w_r, out=out)
+    for k in range(12): L.forward(k % NW, x, w_r, forced_expert=forced, out=out)
     torch.cuda.synchronize()
 p.export_chrome_trace("/tmp/trace.json")
 ev = [e for e in json.load(open("/tmp/trace.json"))["traceEvents"] if e.get("cat") == "kernel"]
 ev.sort(key=lambda e: e["ts"])
 t0 = ev[0]["ts"]
-for e in ev[:24]:
+for e in ev[:12]:
     print(f'{e["ts"]-t0:9.2f} {e["ts"]+e["dur"]-t0:9.2f} {e["dur"]:8.2f}  {e["name"][:60]}')
 # per-kernel mean durations and step period
 from collections import defaultdict
