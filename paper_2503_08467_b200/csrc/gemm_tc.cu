@@ -692,7 +692,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   griddep_launch_dependents();
   if (kT) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_ready));
 
-  const int n_mp_up = fp.up.n_mt / 2, n_mp_dn = fp.dn.n_mt / 2;
+  // pair-units cover m-tiles (2q, 2q+1); with an odd count the last pair has
+  // both CTAs on the same m-tile (the follower's copy is computed, not stored)
+  const int n_mp_up = (fp.up.n_mt + 1) / 2, n_mp_dn = (fp.dn.n_mt + 1) / 2;
   const int chunks = s_pref[E];
   const int total_up = chunks * n_mp_up;
   const int total = total_up + chunks * n_mp_dn;
@@ -711,7 +713,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int n_mt = down ? fp.dn.n_mt : fp.up.n_mt;
       const int nkb = down ? nkb_dn : nkb_up;
       const CUtensorMap* tm = down ? &tmA_dn : &tmA_up;
-      const int mt = 2 * w.mt + static_cast<int>(rank);
+      const int mt = min(2 * w.mt + static_cast<int>(rank), n_mt - 1);
       const int row0 = ((w.e * n_mt + mt) * nkb * KA) * BM;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&emptyA[stage], phase ^ 1);
@@ -864,12 +866,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int mt = 2 * w.mt + static_cast<int>(rank);
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * BN_MAX;
-      if (down)
-        store_tile<true>(fp.dn, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
-                         pol_keep, stage);
-      else
-        store_tile<false>(fp.up, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
-                          pol_keep, stage);
+      if (mt < (down ? fp.dn.n_mt : fp.up.n_mt)) {   // else: duplicate of the leader's tile
+        if (down)
+          store_tile<true>(fp.dn, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
+                           pol_keep, stage);
+        else
+          store_tile<false>(fp.up, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
+                            pol_keep, stage);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + as * 8);

@@ -499,7 +499,7 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   }
   c->mark(2, s);
   const bool fused = c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_UNFUSED_GEMM) &&
-                     (F / kTcFeatTile) % 2 == 0 && (h / kTcFeatTile) % 2 == 0;
+                     F % kTcFeatTile == 0 && h % kTcFeatTile == 0;   // odd tile counts: see FFN kernel
   const bool gather = fused && (c->cfg.flags & MOESHARD_FLAG_TMA_GATHER);
   CUtensorMap tm_xg;   // x_all rows for TMA gather4 (box {64, 1})
   if (gather && !make_tmap(&tm_xg, x_all, h, N, 1))

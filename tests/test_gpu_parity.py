@@ -139,15 +139,19 @@ def test_unfused_two_launch_gemm_ablation_matches_oracle():
     _check_layer(inp, y, r, tol=BF16_TOL)
 
 
-def test_fused_and_unfused_gemm_agree_bitwise():
+@pytest.mark.parametrize("N,h,d_ff,E", [
+    (3000, 512, 1024, 64),   # even tile counts: both schedules use CTA pairs
+    (1500, 384, 640, 16),    # odd (3 and 5 tiles): fused duplicates the last pair's tile,
+])                           # the unfused path runs 1-CTA M=128 tiles
+def test_fused_and_unfused_gemm_agree_bitwise(N, h, d_ff, E):
     # same arithmetic in both schedules: outputs must be identical bit for bit
     from paper_2503_08467_b200 import MoEShardLayer
     from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_UNFUSED_GEMM
-    inp = W.make_layer_inputs(19, 3000, 512, 1024, 64, dtype=torch.bfloat16, routing="zipf")
+    inp = W.make_layer_inputs(19, N, h, d_ff, E, dtype=torch.bfloat16, routing="zipf")
     f = inp.forced.cuda().contiguous()
     ys = []
     for flags in (0, MOESHARD_FLAG_UNFUSED_GEMM):
-        L = MoEShardLayer(512, 1024, 64, max_tokens_per_rank=3000, dtype=torch.bfloat16, flags=flags)
+        L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16, flags=flags)
         L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
         ys.append(L.forward(0, inp.x.cuda(), inp.w_r.cuda(), forced_expert=f))
         torch.cuda.synchronize()
