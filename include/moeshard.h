@@ -72,6 +72,8 @@ typedef enum {
 #define MOESHARD_FLAG_UNFUSED_GEMM 0x4u      /* bf16 mode: up and down products as two launches (ablation) */
 #define MOESHARD_FLAG_TMA_GATHER 0x8u        /* bf16 fused mode: gather token rows with TMA gather4 instead of X_perm (experimental, slower) */
 #define MOESHARD_FLAG_H_TRANSPOSED 0x10u     /* bf16 fused mode: keep H transposed, MN-major down operand (experimental, slower) */
+#define MOESHARD_FLAG_FUSED_ROUTE_GROUP 0x20u /* world = 1: run Step 2 inside the router launch (grid barriers; experimental, slower) */
+#define MOESHARD_FLAG_CPASYNC_GATHER 0x40u    /* bf16 fused mode: the FFN gathers token rows with cp.async (no X_perm copy) */
 
 typedef struct {
   int32_t d_model;             /* h; multiple of 128 */

@@ -738,11 +738,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2;
     int stage = 0;
     uint32_t phase = 0;
+    // cp.async gather (fp.up.gather_cp): a stage is published to the MMA (arrive on
+    // the leader's full barrier) kGD stages after its copies were issued, once they
+    // have landed and been fenced for the tensor core; npend stages are in flight
+    const int kGD = fp.up.gather_depth;   // 1 .. BS - 1
+    int npend = 0;
+    auto publish_oldest = [&]() {
+      fence_proxy_async_shared();
+      __syncwarp();
+      const int st = (stage - npend + BS) % BS;
+      if (elect_one()) {
+        if (leader) mbar_arrive(&fullB[st]);
+        else mbar_arrive_cluster(leader_full + st * 8);
+      }
+      __syncwarp();
+      --npend;
+    };
+    auto drain = [&]() {
+      cp_async_wait<0>();
+      while (npend > 0) publish_oldest();
+    };
     for (int u = cid; u < total; u += ncl) {
       const bool down = u >= total_up;
       const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
       const int nkb = down ? nkb_dn : nkb_up;
       const CUtensorMap* tm = down ? &tmB_dn : &tmB_up;
+      if (down && npend > 0) drain();
       if (down) {   // H rows of expert e complete? (acquire), then order the TMA after it
         const int target = 2 * (s_pref[w.e + 1] - s_pref[w.e]) * n_mp_up;
         if (elect_one()) {
@@ -758,11 +779,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool mn = down && fp.dn.ht;   // H^T: MN-major token tile, 64-token x 64-feature boxes
       const int nbx = (half + 63) / 64;
       const uint32_t stage_bytes = KA * (mn ? nbx * 8192 : nb * B2_BOX * BK * 2);
-      if (gather) {   // this CTA's token ids for the unit (padding rows read row 0; masked later)
-        __syncwarp();
+      const bool gcp = gather && fp.up.gather_cp;
+      if (gather) {   // this CTA's token ids for the unit (padding rows: row 0 for gather4,
+        __syncwarp(); // -1 = zero fill for cp.async; masked in the epilogue either way)
         for (int i = lane; i < half; i += 32)
-          s_rows[i] = (r0 + i < w.tok0 + w.ntok) ? __ldg(fp.up.gather + r0 + i) : 0;
+          s_rows[i] = (r0 + i < w.tok0 + w.ntok) ? __ldg(fp.up.gather + r0 + i) : (gcp ? -1 : 0);
         __syncwarp();
+      }
+      if (gcp) {
+        // rows of x_all gathered by 16-B cp.async into the 128-B-swizzled K-major image:
+        // row i, 16-B chunk c -> i * 128 + ((c ^ (i & 7)) * 16); 4 rows per warp instruction
+        const int c = lane & 7;
+        const __nv_bfloat16* src0 = fp.up.gsrc + c * 8;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&emptyB[stage], phase ^ 1);
+          const uint32_t dst0 = smem_u32(sB + stage * SB_BYTES);
+          for (int i = lane >> 3; i < half; i += 4) {
+            const int row = s_rows[i];
+            cp_async_16(dst0 + i * 128 + ((c ^ (i & 7)) << 4),
+                        src0 + static_cast<size_t>(row < 0 ? 0 : row) * fp.up.K + kb * BK,
+                        row < 0 ? 0u : 16u, pol_x);
+          }
+          cp_async_commit();
+          ++npend;
+          if (++stage == BS) { stage = 0; phase ^= 1; }
+          if (npend > kGD) {
+            switch (kGD) {   // cp.async.wait_group takes an immediate
+              case 1: cp_async_wait<1>(); break;
+              case 2: cp_async_wait<2>(); break;
+              case 3: cp_async_wait<3>(); break;
+              case 4: cp_async_wait<4>(); break;
+              default: cp_async_wait<5>(); break;
+            }
+            publish_oldest();
+          }
+        }
+        continue;
       }
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&emptyB[stage], phase ^ 1);
@@ -793,6 +845,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (++stage == BS) { stage = 0; phase ^= 1; }
       }
     }
+    if (npend > 0) drain();
   } else if (warp == 1) {
     if (leader) {
       // ------------------------------------------------------------ MMA issuer (leader only)
@@ -995,7 +1048,7 @@ cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_
   // MOESHARD_TC_VARIANT 20: two k-atoms per ring stage (3 + 3 stages of 32 KB)
   if (variant() == 21)
     return launch_fused<6, 6, 1, true>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, grid, s);
-  if (variant() == 20 && up.K % 128 == 0 && dn.K % 128 == 0)
+  if (variant() == 20 && up.K % 128 == 0 && dn.K % 128 == 0 && !up.gather_cp)
     return launch_fused<3, 3, 2>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, grid, s);
   return launch_fused<6, 6, 1>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, grid, s);
 }

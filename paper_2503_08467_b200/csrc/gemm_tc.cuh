@@ -37,6 +37,23 @@ struct TcParams {
   // an MN-major B operand.
   bool ht = false;
   int ld_ht = 0;           // token stride of H^T (N_max)
+  // cp.async gather instead of TMA gather4: rows gsrc[gather[j]] ([n_rows][K] bf16)
+  bool gather_cp = false;
+  const __nv_bfloat16* gsrc = nullptr;
+  int gather_depth = 4;    // stages in flight before one is published (<= ring depth - 1)
+};
+
+// Step 2 outputs for the fused route+group launch (world = 1): see launch_route_group_tc.
+struct RouteGroupArgs {
+  Tables tb;
+  int32_t* base;        // [NB][E] workspace: tokens of e in earlier hist-blocks
+  int32_t* tot;         // [E] workspace
+  int32_t* perm;        // [N] public compact permutation
+  const uint4* x;       // hidden [n][h] (row_vecs 16-B vectors per row)
+  uint4* x_perm;        // internal expert-ordered rows (nullptr: no row copy)
+  int row_vecs;         // h * 2 / 16, <= 128
+  int n_mt_up, n_mt_dn; // 128-row tiles of the two products (tile statistics)
+  int32_t* bar;         // 2 ints (grid barrier), zero-initialised once
 };
 
 // tcgen05 router (router.cu): logits/softmax/top-1 per 128-token CTA, plus the
@@ -52,6 +69,15 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
                              const int32_t* forced, RouteRec* out, int32_t* hist_out,
                              int32_t* err_flag, const void* pf, long long pf_bytes, int pf_ctas,
                              cudaStream_t s);
+
+// Router + the whole of Step 2 in one launch (world = 1, ceil(n/128) <= SMs,
+// router_w MN-major (E % 8 == 0), h <= 1024): routes 128 tokens per CTA like
+// launch_router_tc, then (grid barriers) per-expert block scans, segment
+// tables, stable permutation and the X_perm row copy.
+cudaError_t launch_route_group_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, int n, int h,
+                                  int E, int EP, const int32_t* forced, RouteRec* out,
+                                  int32_t* hist_out, int32_t* err_flag, const RouteGroupArgs& ga,
+                                  cudaStream_t s);
 
 // grid = number of persistent CTAs (normally the SM count).
 //   tmA:  packed weight tiles as a [rows][64] bf16 tensor, box {64, 128}, no swizzle

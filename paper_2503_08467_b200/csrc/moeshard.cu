@@ -182,6 +182,7 @@ struct moeshard_ctx {
   int last_n = 0;
   int64_t launches = 0;  // cumulative kernel launches of this context
   long long pf_bytes = 0;  // experimental L2 weight prefetch during routing (MOESHARD_L2_PREFETCH_MB)
+  int gather_depth = 4;    // cp.async gather: stages in flight (MOESHARD_GATHER_DEPTH, 1..5)
   // phase profiling (measurement only)
   bool prof = false;
   static constexpr int kRing = 1024, kEv = 7;
@@ -337,6 +338,14 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->coll = world > 1 || (c->cfg.flags & MOESHARD_FLAG_FORCE_COLLECTIVES);
   c->use_tc = cfg->dtype == MOESHARD_BF16 && !(c->cfg.flags & MOESHARD_FLAG_SIMT_GEMM);
   if (const char* pf = getenv("MOESHARD_L2_PREFETCH_MB")) c->pf_bytes = atoll(pf) << 20;
+  if (const char* gd = getenv("MOESHARD_GATHER_DEPTH")) c->gather_depth = std::max(1, std::min(5, atoi(gd)));
+  if (const char* pl = getenv("MOESHARD_L2_PERSIST_MB")) {   // experiment: L2 set-aside for evict_last lines
+    size_t want = static_cast<size_t>(atoll(pl)) << 20, got = 0;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+    fprintf(stderr, "[moeshard] persisting L2 limit %zu MB (max %d MB)\n", got >> 20,
+            prop.persistingL2CacheMaxSize >> 20);
+  }
   c->L = L;
   c->ws = static_cast<char*>(workspace);
   c->route = reinterpret_cast<RouteRec*>(c->ws + L.route);
@@ -465,7 +474,27 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   const int NB = (c->coll ? c->world : 1) * nbr;
   const int N = (c->coll ? c->world : 1) * n;             // tokens of all ranks
   int32_t* my_hist = c->block_hist + (c->coll ? static_cast<size_t>(c->rank) * nbr * E : 0);
-  if (c->use_tc) {
+  const bool fused = c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_UNFUSED_GEMM) &&
+                     F % kTcFeatTile == 0 && h % kTcFeatTile == 0;   // odd tile counts: see FFN kernel
+  // token rows gathered by the FFN itself (no X_perm copy): TMA gather4 or cp.async
+  const bool gather_cp = fused && (c->cfg.flags & MOESHARD_FLAG_CPASYNC_GATHER);
+  const bool gather = fused && ((c->cfg.flags & MOESHARD_FLAG_TMA_GATHER) || gather_cp);
+  // world = 1: the router launch also runs Step 2 (grid barriers need every CTA resident)
+  const bool route_group = c->use_tc && !c->coll && (E % 8) == 0 && nbr <= c->num_sms &&
+                           h <= 1024 && c->pf_bytes == 0 &&
+                           (c->cfg.flags & MOESHARD_FLAG_FUSED_ROUTE_GROUP);
+  if (route_group) {
+    CUtensorMap tm_x, tm_w;
+    if (!make_tmap(&tm_x, hidden, h, n, 128) || !make_tmap(&tm_w, router_w, E, h, 64))
+      return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden/router_w");
+    RouteGroupArgs ga{c->tb, c->block_base, c->block_tot, c->perm,
+                      static_cast<const uint4*>(hidden),
+                      gather ? nullptr : static_cast<uint4*>(c->x_perm), h * c->elt / 16,
+                      F / kTcFeatTile, h / kTcFeatTile, c->tb.stats + 4};
+    CUDA_TRY(c, launch_route_group_tc(tm_x, tm_w, n, h, E, c->EP, forced, my_route, my_hist,
+                                      err_flag, ga, s));
+    c->launches += 1;
+  } else if (c->use_tc) {
     CUtensorMap tm_x, tm_w;
     const bool mn = (E % 8) == 0;
     if (!make_tmap(&tm_x, hidden, h, n, 128) ||
@@ -498,18 +527,17 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     x_all = c->x_all;
   }
   c->mark(2, s);
-  const bool fused = c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_UNFUSED_GEMM) &&
-                     F % kTcFeatTile == 0 && h % kTcFeatTile == 0;   // odd tile counts: see FFN kernel
-  const bool gather = fused && (c->cfg.flags & MOESHARD_FLAG_TMA_GATHER);
   CUtensorMap tm_xg;   // x_all rows for TMA gather4 (box {64, 1})
-  if (gather && !make_tmap(&tm_xg, x_all, h, N, 1))
+  if (gather && !gather_cp && !make_tmap(&tm_xg, x_all, h, N, 1))
     return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for the gather map");
   // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs (the row
   // copy is skipped when the FFN gathers rows itself)
-  launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb, F / kTcFeatTile,
-                      h / kTcFeatTile, c->route, x_all, n, nbr, HB, h * c->elt, c->perm,
-                      gather ? nullptr : c->x_perm, s);
-  c->launches += 2;
+  if (!route_group) {
+    launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb, F / kTcFeatTile,
+                        h / kTcFeatTile, c->route, x_all, n, nbr, HB, h * c->elt, c->perm,
+                        gather ? nullptr : c->x_perm, s);
+    c->launches += 2;
+  }
   c->mark(3, s);
   // Step 4: expert computation, one grouped product per projection
   void* P = c->coll ? c->partial : hidden_out;
@@ -520,10 +548,11 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     const int np = static_cast<int>(c->L.npad);
     TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
                 static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr,
-                gather ? c->tb.perm_pad : nullptr, N, ht, np};
+                gather ? c->tb.perm_pad : nullptr, N, ht, np, gather_cp,
+                static_cast<const __nv_bfloat16*>(x_all), c->gather_depth};
     TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
                 static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route, nullptr, 0, ht, np};
-    CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather ? tm_xg : c->tm_xperm16, lw.tm_out,
+    CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather && !gather_cp ? tm_xg : c->tm_xperm16, lw.tm_out,
                                   ht ? c->tm_Ht : c->tm_H16, up, dn, c->tb.done, c->num_sms, s));
     c->mark(4, s);
     c->launches += 1;

@@ -12,17 +12,12 @@
 // Also: a batched transpose used once at load time to repack expert shards
 // K-major (loadShard).
 #include "common.cuh"
+#include "group.cuh"
 #include "ptx.cuh"
 
 namespace moeshard {
 namespace {
 
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-  unsigned m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
 
 template <typename T>
 __global__ void transpose_kernel(const T* __restrict__ src, T* __restrict__ dst, int rows,
@@ -42,39 +37,6 @@ __global__ void transpose_kernel(const T* __restrict__ src, T* __restrict__ dst,
     if (r < rows && c < cols) d[(size_t)c * rows + r] = tile[threadIdx.x][i];
   }
 }
-
-
-// Exclusive scan over the CTA (kThreads <= 1024, one value per thread); total in `total`.
-template <int kThreads>
-__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
-  constexpr int kWarps = kThreads / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int o = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += o;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const int w = lane < kWarps ? s_warp[lane] : 0;
-    int wi = w;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int o = __shfl_up_sync(0xffffffffu, wi, off);
-      if (lane >= off) wi += o;
-    }
-    if (lane < kWarps) s_warp[lane] = wi - w;
-    if (lane == 31) s_warp[32] = wi;
-  }
-  __syncthreads();
-  const int res = s_warp[warp] + incl - v;
-  total = s_warp[32];
-  __syncthreads();
-  return res;
-}
-
 
 
 // ===========================================================================
@@ -169,47 +131,8 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   }
   for (int k = threadIdx.x; k < 4 * E; k += kThreads) whist[k / E][k % E] = 0;
   __syncthreads();
-  {
-    const int e = threadIdx.x;
-    int cnt = 0, nc = 0, cs = 0, rows = 0, sc = 0;
-    if (e < E) {
-      cnt = s_tot[e];
-      tc_chunking(cnt, &nc, &cs);
-      rows = nc > 0 ? (cnt / cs) * cs + round_up(cnt % cs, 32) : 0;
-      sc = ceil_div(cnt, kSimtTokTile);
-    }
-    int tot_cnt, tot_pad;
-    const int off = block_excl_scan<kThreads>(cnt, s_warp, tot_cnt);
-    const int pos = block_excl_scan<kThreads>(round_up(cnt, kSegAlign), s_warp, tot_pad);
-    if (e < E) {
-      s_base[e] = off + s_pre[e];
-      s_bpad[e] = pos + s_pre[e];
-    }
-    if (blockIdx.x == 0) {  // publish the tables the grouped GEMMs read
-      int tot_tc, tot_sc, tot_rows;
-      const int tcp = block_excl_scan<kThreads>(nc, s_warp, tot_tc);
-      const int smp = block_excl_scan<kThreads>(sc, s_warp, tot_sc);
-      block_excl_scan<kThreads>(rows, s_warp, tot_rows);
-      if (e < E) {
-        tb.done[e] = 0;
-        tb.pos[e] = pos;
-        tb.counts[e] = cnt;
-        tb.tc_chunk_size[e] = cs;
-        tb.offsets[e] = off;
-        tb.tc_chunk_pref[e] = tcp;
-        tb.simt_chunk_pref[e] = smp;
-      }
-      if (threadIdx.x == 0) {
-        tb.pos[E] = tot_pad;
-        tb.offsets[E] = tot_cnt;
-        tb.tc_chunk_pref[E] = tot_tc;
-        tb.simt_chunk_pref[E] = tot_sc;
-        tb.stats[0] = tot_tc * n_mt_up_tc;
-        tb.stats[1] = tot_tc * n_mt_down_tc;
-        tb.stats[2] = tot_rows * n_mt_up_tc;
-      }
-    }
-  }
+  segment_tables<kThreads>(E, s_tot, s_pre, s_base, s_bpad, s_warp, blockIdx.x == 0, tb,
+                           n_mt_up_tc, n_mt_down_tc);
   // 2. stable ranks inside the block
   if (warp < 4) {
     const unsigned peers = __match_any_sync(0xffffffffu, e);

@@ -147,6 +147,23 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// 16-B cp.async (L2 only) with zero fill when src_bytes = 0, a commit group, and
+// waits; shared-memory writes made this way reach the tensor core (async proxy)
+// only after fence_proxy_async_shared().
+__device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes,
+                                            uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst),
+               "l"(src), "r"(src_bytes), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 // TMA 2-D load for a CTA pair: data lands in the executing CTA's smem, completion
 // is signalled on the mbarrier at `bar_cluster` (normally in the leader CTA).
 __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* d, uint32_t bar_cluster,

@@ -199,6 +199,8 @@ void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int 
 #include <cstdio>
 #include <cstdlib>
 
+#include "gemm_tc.cuh"
+#include "group.cuh"
 #include "ptx.cuh"
 
 namespace moeshard {
@@ -230,15 +232,125 @@ __global__ void router_transpose(const __nv_bfloat16* __restrict__ w_r, int h, i
   }
 }
 
+// Step 2 (groupPerExpert + the Sec. 3.3 per-expert concatenation,
+// PAPER.md:191-195, 339-341) inside the router launch, world = 1. CTA b owns
+// hist-block b = tokens [128 b, 128 b + 128). Three phases split by grid
+// barriers (all CTAs resident):
+//   1. (routing, above) hist[b][e] and each token's expert in s_tok_e;
+//   2. CTA c scans hist[.][e] over the blocks for experts e = c, c + NB, ... ->
+//      base[b][e] (tokens of e in earlier blocks) and tot[e];
+//   3. every CTA: segment offsets from tot (CTA 0 publishes the tables), the
+//      stable rank of each token inside its block (match_any), perm / perm_pad,
+//      and the copy of its 128 rows x[t] -> X_perm[j] (x is still in L2).
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <bool kT>
+__device__ __forceinline__ void route_group(const RouteGroupArgs& ga, const int32_t* hist,
+                                            const int32_t* s_tok_e, int n, int E, uint64_t t_entry,
+                                            uint64_t t_routed) {
+  uint64_t ts[6];
+  __shared__ int32_t s_tot[kMaxExperts], s_pre[kMaxExperts], s_base[kMaxExperts],
+      s_bpad[kMaxExperts];
+  __shared__ int32_t whist[4][kMaxExperts];
+  __shared__ int32_t s_j[128];
+  __shared__ int32_t s_warp[33];
+  const int NB = gridDim.x, b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (kT) ts[0] = gtimer();
+  grid_barrier(ga.bar, NB);               // every block's histogram is in memory
+  ptx::griddep_launch_dependents();       // all CTAs of this grid are resident now
+  if (kT) ts[1] = gtimer();
+  for (int e = b; e < E; e += NB) {       // CTA-uniform loop
+    const int v = threadIdx.x < NB ? __ldcg(hist + static_cast<size_t>(threadIdx.x) * E + e) : 0;
+    int total;
+    const int ex = block_excl_scan<256>(v, s_warp, total);
+    if (threadIdx.x < NB) ga.base[static_cast<size_t>(threadIdx.x) * E + e] = ex;
+    if (threadIdx.x == 0) ga.tot[e] = total;
+  }
+  if (kT) ts[2] = gtimer();
+  grid_barrier(ga.bar, NB);               // base / tot complete
+  if (kT) ts[3] = gtimer();
+  for (int k = threadIdx.x; k < E; k += 256) {
+    s_tot[k] = __ldcg(ga.tot + k);
+    s_pre[k] = __ldcg(ga.base + static_cast<size_t>(b) * E + k);
+  }
+  for (int k = threadIdx.x; k < 4 * E; k += 256) whist[k / E][k % E] = 0;
+  __syncthreads();
+  segment_tables<256>(E, s_tot, s_pre, s_base, s_bpad, s_warp, b == 0, ga.tb, ga.n_mt_up,
+                      ga.n_mt_dn);
+  const int t = b * 128 + threadIdx.x;
+  int e = -1, rank_w = 0;
+  if (warp < 4) {
+    e = s_tok_e[threadIdx.x];
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    rank_w = __popc(peers & lanemask_lt());
+    if (e >= 0 && rank_w == 0) whist[warp][e] = __popc(peers);
+  }
+  __syncthreads();
+  if (warp < 4) {
+    int jp = -1;
+    if (e >= 0) {
+      int before = 0;
+      for (int w = 0; w < warp; ++w) before += whist[w][e];
+      ga.perm[s_base[e] + before + rank_w] = t;            // public, compact
+      jp = s_bpad[e] + before + rank_w;                    // internal, padded segments
+      ga.tb.perm_pad[jp] = t;
+    }
+    s_j[threadIdx.x] = jp;
+  }
+  __syncthreads();
+  if (kT) ts[4] = gtimer();
+  if (ga.x_perm == nullptr) return;
+  // rows: 8 warps x 16 rows, 4 rows in flight per warp (row_vecs <= 128)
+  const int rv = ga.row_vecs;
+  for (int r0 = warp * 16; r0 < warp * 16 + 16; r0 += 4) {
+    uint4 v[4][4];
+    int jj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      jj[u] = s_j[r0 + u];
+      const uint4* src = ga.x + static_cast<size_t>(b * 128 + r0 + u) * rv;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (jj[u] >= 0 && lane + 32 * c < rv) v[u][c] = __ldcg(src + lane + 32 * c);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint4* dst = ga.x_perm + static_cast<size_t>(jj[u]) * rv;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (jj[u] >= 0 && lane + 32 * c < rv) dst[lane + 32 * c] = v[u][c];
+    }
+  }
+  if (kT) {
+    __syncthreads();
+    ts[5] = gtimer();
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+      printf("[route_group cta %d] ns from entry: routed %llu arrive1 %llu pass1 %llu scanned %llu "
+             "pass2 %llu ranked %llu copied %llu\n", blockIdx.x,
+             (unsigned long long)(t_routed - t_entry), (unsigned long long)(ts[0] - t_entry),
+             (unsigned long long)(ts[1] - t_entry), (unsigned long long)(ts[2] - t_entry),
+             (unsigned long long)(ts[3] - t_entry), (unsigned long long)(ts[4] - t_entry),
+             (unsigned long long)(ts[5] - t_entry));
+  }
+}
+
 // kMN: B = router_w [h][E] read directly (MN-major, 64-expert x 64-k TMA boxes);
 // otherwise B = the transposed copy [EP][h] (K-major).
-template <bool kMN, bool kT = false>
-__global__ void __launch_bounds__(192, 1)
+// kGroup (world = 1 only, grid <= SMs so every CTA is resident): after routing,
+// the same launch runs the whole of Step 2 (see route_group below) - the block
+// histograms never leave the kernel boundary and the row copy re-reads x from L2.
+template <bool kMN, bool kT = false, bool kGroup = false>
+__global__ void __launch_bounds__(256, 1)
     router_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      int n, int h, int E, int EP, const int32_t* __restrict__ forced,
                      RouteRec* __restrict__ out, int32_t* __restrict__ hist_out,
                      int32_t* __restrict__ err_flag, const uint8_t* __restrict__ pf,
-                     long long pf_bytes) {
+                     long long pf_bytes, RouteGroupArgs ga) {
   // CTAs beyond the token tiles run on otherwise idle SMs and pull the first
   // weight tiles the FFN kernel will stream into L2 while routing and grouping
   // are latency-bound (the weights do not depend on the routing result).
@@ -258,6 +370,7 @@ __global__ void __launch_bounds__(192, 1)
   const int n_atoms = (EP + 63) / 64;
   const int b_bytes = kMN ? n_atoms * 8192 : EP * 128;
   __shared__ int32_t s_hist[kMaxExperts];
+  __shared__ int32_t s_tok_e[128];   // kGroup: expert of each of the CTA's tokens (-1: none)
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
   const int RTC_STAGES = min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (RTC_A_BYTES + b_bytes));
   uint8_t* sA = smem;
@@ -280,6 +393,7 @@ __global__ void __launch_bounds__(192, 1)
     fence_mbar_init();
   }
   const long long t_start = clock64();
+  const uint64_t g_entry = kT ? gtimer() : 0;
   if (warp == 0) tmem_alloc(tmem_slot, ncols);
   tc_fence_before();
   __syncthreads();
@@ -288,14 +402,16 @@ __global__ void __launch_bounds__(192, 1)
   // PDL: x may come from the previous kernel, and the previous forward's FFN
   // still reads the route records this kernel overwrites
   griddep_wait();
-  griddep_launch_dependents();
+  // kGroup: only after the first grid barrier (every CTA of this grid resident),
+  // else the dependent FFN's CTAs could take the SMs a not-yet-running CTA needs
+  if (!kGroup) griddep_launch_dependents();
   const long long t_setup = clock64();
   const int tok0 = blockIdx.x * 128;
   const int nkb = h / 64;
 
   if (warp == 4) {
     {  // TMA producer (warp-uniform loop, one elected lane issues)
-      const uint64_t pol_x = policy_evict_first();
+      const uint64_t pol_x = kGroup ? policy_evict_last() : policy_evict_first();  // kGroup re-reads x
       const uint64_t pol_w = policy_evict_last();
       int s = 0;
       uint32_t ph = 0;
@@ -339,7 +455,7 @@ __global__ void __launch_bounds__(192, 1)
       if (elect_one()) mma_commit(done);
       __syncwarp();
     }
-  } else {
+  } else if (warp < 4) {
     // epilogue: warps 0-3, thread = token (TMEM lane 32*warp + lane)
     const int t = tok0 + warp * 32 + lane;
     int sel = -1;
@@ -422,11 +538,12 @@ __global__ void __launch_bounds__(192, 1)
       atomicAdd(&s_hist[rec.expert], 1);
       if (bad) atomicExch(err_flag, 1);
     }
+    if (kGroup) s_tok_e[threadIdx.x] = t < n ? (sel >= 0 ? sel : best_e) : -1;
     const long long t_store = clock64();
     asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
     const long long t_bar = clock64();
     for (int e = threadIdx.x; e < E; e += 128) hist_out[(size_t)blockIdx.x * E + e] = s_hist[e];
-    if (kT && (threadIdx.x == 0 || threadIdx.x == 127) && (blockIdx.x == 0 || blockIdx.x == 40))
+    if (kT && !kGroup && (threadIdx.x == 0 || threadIdx.x == 127) && (blockIdx.x == 0 || blockIdx.x == 40))
       printf("[router cta %d t%d] setup %lld mainloop %lld softmax %lld store %lld bar %lld hist %lld\n",
              blockIdx.x, threadIdx.x, t_setup - t_start, t_done - t_setup, t_loop - t_done,
              t_store - t_loop, t_bar - t_store, clock64() - t_bar);
@@ -435,6 +552,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 0) tmem_dealloc(tmem, ncols);
+  if constexpr (kGroup) route_group<kT>(ga, hist_out, s_tok_e, n, E, g_entry, kT ? gtimer() : 0);
 }
 
 }  // namespace
@@ -464,24 +582,51 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  const RouteGroupArgs none{};
   static const bool timing = getenv("MOESHARD_ROUTER_TIMING") != nullptr;
   if (mn_major && timing) {
     cudaFuncSetAttribute(router_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          RTC_SMEM_BUDGET + 2048);
     router_tc_kernel<true, true><<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP, true), s>>>(
-        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, 0LL);
+        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, 0LL, none);
   } else if (mn_major) {
     return launch_pdl(router_tc_kernel<true>, dim3(ceil_div(n, 128) + pf_ctas), dim3(192),
                       router_tc_smem_bytes(EP, true), s, tmX, tmW, n, h, E, EP, forced, out,
-                      hist_out, err_flag, pfb, pf_bytes);
+                      hist_out, err_flag, pfb, pf_bytes, none);
   } else {
     dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
     router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,
                                        static_cast<__nv_bfloat16*>(wt_r));
     router_tc_kernel<false><<<ceil_div(n, 128) + pf_ctas, 192, router_tc_smem_bytes(EP, false), s>>>(
-        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, pf_bytes);
+        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, pf_bytes, none);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_route_group_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, int n, int h,
+                                  int E, int EP, const int32_t* forced, RouteRec* out,
+                                  int32_t* hist_out, int32_t* err_flag, const RouteGroupArgs& ga,
+                                  cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(router_tc_kernel<true, false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         RTC_SMEM_BUDGET + 2048);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  static const bool timing = getenv("MOESHARD_ROUTER_TIMING") != nullptr;
+  if (timing) {
+    cudaFuncSetAttribute(router_tc_kernel<true, true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, RTC_SMEM_BUDGET + 2048);
+    return launch_pdl(router_tc_kernel<true, true, true>, dim3(ceil_div(n, 128)), dim3(256),
+                      router_tc_smem_bytes(EP, true), s, tmX, tmW, n, h, E, EP, forced, out,
+                      hist_out, err_flag, static_cast<const uint8_t*>(nullptr), 0LL, ga);
+  }
+  return launch_pdl(router_tc_kernel<true, false, true>, dim3(ceil_div(n, 128)), dim3(256),
+                    router_tc_smem_bytes(EP, true), s, tmX, tmW, n, h, E, EP, forced, out,
+                    hist_out, err_flag, static_cast<const uint8_t*>(nullptr), 0LL, ga);
 }
 
 }  // namespace moeshard

@@ -25,6 +25,8 @@ MOESHARD_FLAG_SIMT_GEMM = 0x2
 MOESHARD_FLAG_UNFUSED_GEMM = 0x4
 MOESHARD_FLAG_TMA_GATHER = 0x8
 MOESHARD_FLAG_H_TRANSPOSED = 0x10
+MOESHARD_FLAG_FUSED_ROUTE_GROUP = 0x20
+MOESHARD_FLAG_CPASYNC_GATHER = 0x40
 
 STATUS = {
     0: "MOESHARD_OK", -1: "MOESHARD_ERR_INVALID_ARG", -2: "MOESHARD_ERR_SHAPE",

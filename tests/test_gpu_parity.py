@@ -357,3 +357,105 @@ def test_c2_full_size_sampled(routing):
     assert err <= BF16_TOL, err
     # every output row was written (droplessness): no NaN/garbage, no zero rows
     assert torch.isfinite(y).all() and (y.float().abs().sum(1) > 0).all()
+
+
+# --------------------------------------------------------------------- fused route + group (world = 1)
+@pytest.mark.parametrize("N,h,d_ff,E,routing", [
+    (3000, 512, 1024, 64, "zipf"),       # 24 router CTAs, multi-chunk segments
+    (18944, 256, 256, 16, "uniform"),    # 148 hist-blocks = one CTA on every SM (largest fused grid)
+    (18945, 256, 256, 16, "uniform"),    # 149 blocks: falls back to the separate grouping launches
+    (700, 1024, 512, 256, "patho"),      # E = 256 (two expert scans per CTA), h = 1024
+])
+def test_route_group_fused_matches_separate_and_oracle(N, h, d_ff, E, routing):
+    """Step 2 inside the router launch (grid barriers) == the separate launches,
+    bit for bit, and == the oracle; repeated forwards reuse the barrier."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_FUSED_ROUTE_GROUP
+    inp = W.make_layer_inputs(23, N, h, d_ff, E, dtype=torch.bfloat16, routing=routing, k=2)
+    f = inp.forced.cuda().contiguous()
+    outs, routes = [], []
+    for flags in (MOESHARD_FLAG_FUSED_ROUTE_GROUP, 0):
+        L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16, flags=flags)
+        L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
+        for _ in range(3):
+            y = L.forward(0, inp.x.cuda(), inp.w_r.cuda(), forced_expert=f)
+        L.check()
+        torch.cuda.synchronize()
+        outs.append(y.clone())
+        routes.append({k: v.cpu().numpy() for k, v in L.routing(N).items()})
+        L.close()
+    assert torch.equal(outs[0], outs[1])
+    for k in routes[0]:
+        np.testing.assert_array_equal(routes[0][k], routes[1][k])
+    _check_layer(inp, outs[0], routes[0], tol=BF16_TOL)
+
+
+@pytest.mark.parametrize("flag", ["FUSED_ROUTE_GROUP", "CPASYNC_GATHER", None])
+def test_forward_under_cuda_graph_replay(flag):
+    """A captured forward replays correctly with new token values and new routing
+    (the grid barrier of the fused route+group launch carries no launch arguments)."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200 import moeshard as C
+    flags = getattr(C, f"MOESHARD_FLAG_{flag}") if flag else 0
+    N, h, d_ff, E = 2000, 256, 512, 32
+    a = W.make_layer_inputs(24, N, h, d_ff, E, dtype=torch.bfloat16, routing="zipf")
+    b = W.make_layer_inputs(25, N, h, d_ff, E, dtype=torch.bfloat16, routing="uniform")
+    L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16, flags=flags)
+    L.load_expert_shards(0, a.w_i.cuda(), a.w_o.cuda())
+    x = a.x.cuda().clone()
+    w_r = a.w_r.cuda()
+    f = a.forced.cuda().contiguous().clone()
+    out = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        L.forward(0, x, w_r, forced_expert=f, out=out)   # warm-up outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        L.forward(0, x, w_r, forced_expert=f, out=out)
+    for inp in (b, a, b):
+        x.copy_(inp.x.cuda())
+        f.copy_(inp.forced.cuda())
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        r = {k: v.cpu().numpy() for k, v in L.routing(N).items()}
+        y_ref, rt, counts, offsets, perm = O.moe_layer(inp.x, a.w_r, a.w_i, a.w_o,
+                                                       forced=inp.forced.cpu().numpy(),
+                                                       return_routing=True)
+        np.testing.assert_array_equal(r["counts"], counts)
+        np.testing.assert_array_equal(r["perm"], perm)
+        assert O.max_abs_rel(out.float().cpu().numpy(), y_ref) <= BF16_TOL
+    L.close()
+
+
+# --------------------------------------------------------------------- cp.async token gather
+@pytest.mark.parametrize("N,h,d_ff,E,routing", [
+    (3000, 512, 1024, 64, "zipf"),       # multi-chunk segments, ragged halves
+    (1000, 256, 512, 8, "uniform"),
+    (777, 384, 640, 16, "patho"),        # odd tile counts (duplicated last pair), empty experts
+    (8192, 768, 3072, 64, "zipf"),       # C2 shape
+])
+def test_cpasync_gather_matches_xperm_path_bitwise_and_oracle(N, h, d_ff, E, routing):
+    """The FFN gathering token rows itself (cp.async, zero-filled padding rows) gives
+    the same bits as reading the X_perm copy, and matches the oracle."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_CPASYNC_GATHER
+    inp = W.make_layer_inputs(26, N, h, d_ff, E, dtype=torch.bfloat16, routing=routing, k=1)
+    f = inp.forced.cuda().contiguous()
+    ys, routes = [], []
+    for flags in (MOESHARD_FLAG_CPASYNC_GATHER, 0):
+        L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16, flags=flags)
+        L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
+        for _ in range(2):
+            y = L.forward(0, inp.x.cuda(), inp.w_r.cuda(), forced_expert=f)
+        L.check()
+        torch.cuda.synchronize()
+        ys.append(y.clone())
+        routes.append({k: v.cpu().numpy() for k, v in L.routing(N).items()})
+        L.close()
+    assert torch.equal(ys[0], ys[1])
+    if N <= 3000:
+        _check_layer(inp, ys[0], routes[0], tol=BF16_TOL)
