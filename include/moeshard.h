@@ -73,7 +73,9 @@ typedef enum {
 #define MOESHARD_FLAG_TMA_GATHER 0x8u        /* bf16 fused mode: gather token rows with TMA gather4 instead of X_perm (experimental, slower) */
 #define MOESHARD_FLAG_H_TRANSPOSED 0x10u     /* bf16 fused mode: keep H transposed, MN-major down operand (experimental, slower) */
 #define MOESHARD_FLAG_FUSED_ROUTE_GROUP 0x20u /* world = 1: run Step 2 inside the router launch (grid barriers; experimental, slower) */
-#define MOESHARD_FLAG_CPASYNC_GATHER 0x40u    /* bf16 fused mode: the FFN gathers token rows with cp.async (no X_perm copy) */
+#define MOESHARD_FLAG_CPASYNC_GATHER 0x40u    /* bf16 fused mode: the FFN gathers token rows with cp.async (no X_perm copy; experimental, slower) */
+#define MOESHARD_FLAG_NO_L2_PERSIST 0x80u     /* bf16 mode: leave the device's persisting-L2 limit alone (see moeshard_init) */
+#define MOESHARD_FLAG_ROW_COPY_IN_FFN 0x100u  /* bf16 fused mode: copy token rows into expert order inside the FFN launch (per-expert hand-off; experimental, slower) */
 
 typedef struct {
   int32_t d_model;             /* h; multiple of 128 */
@@ -108,7 +110,12 @@ int moeshard_weight_storage_size(const moeshard_config* cfg, int world, size_t* 
  *      aligned, must stay alive until moeshard_destroy.
  * Errors: DIVISIBILITY (d_ff % world), CONFIG (shape limits, device not
  * sm_100), BOUNDS (rank not in [0, world)), NCCL, CUDA. Collective when a
- * communicator is created. */
+ * communicator is created.
+ * Side effect (bf16 mode, unless MOESHARD_FLAG_NO_L2_PERSIST): raises the
+ * device's persisting-L2 limit (cudaLimitPersistingL2CacheSize) to 64 MB (or
+ * the device maximum) so the kernels' evict_last lines - H between the two
+ * products, the token rows re-read by every feature tile - stay in L2 while
+ * the expert weights stream through it; never lowers an existing limit. */
 int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int world,
                   const uint8_t uid[128], void* workspace, size_t ws_bytes, int device);
 

@@ -618,6 +618,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 struct FusedParams {
   TcParams up, dn;
   int32_t* done;  // [E], zeroed by Step 2 before every forward
+  // in-kernel row copy (Sec. 3.3 per-expert concatenation): X_perm[j] = x_all[perm_pad[j]]
+  // by the epilogue warps before their first tile; cp_src == nullptr: X_perm is ready
+  const uint4* cp_src = nullptr;
+  uint4* cp_dst = nullptr;
+  int cp_row_vecs = 0;
 };
 
 // KA: 64-wide k-atoms per ring stage (1 or 2); a stage holds KA weight tiles and KA token tiles.
@@ -691,6 +696,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch_dependents();
   if (kT) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_ready));
+  if (warp >= 4 && fp.cp_src != nullptr) {
+    // Step 2 row copy, 8 expert-ordered rows per warp iteration (segments start on
+    // multiples of 32 rows, so a group never straddles experts), earliest rows
+    // first - the first units' experts are released first. A group is published
+    // with a release add on copied[e]; the token producer acquires it.
+    const int nw = gridDim.x * 4, gw = blockIdx.x * 4 + (warp - 4);
+    const int rv = fp.cp_row_vecs;
+    const int rows_end = s_off[E];
+    for (int q = gw; q * 8 < rows_end; q += nw) {
+      const int j0 = q * 8;
+      int lo = 0, hi = E;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_off[mid] <= j0) lo = mid; else hi = mid;
+      }
+      const int jend = s_end[lo];
+      if (j0 >= jend) continue;   // segment padding only
+      int tok[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) tok[r] = j0 + r < jend ? __ldg(fp.up.tb.perm_pad + j0 + r) : -1;
+      for (int c0 = 0; c0 < rv; c0 += 128) {
+        uint4 v[8][4];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int col = c0 + lane + 32 * c;
+            if (tok[r] >= 0 && col < rv) v[r][c] = __ldg(fp.cp_src + static_cast<size_t>(tok[r]) * rv + col);
+          }
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int col = c0 + lane + 32 * c;
+            if (tok[r] >= 0 && col < rv) fp.cp_dst[static_cast<size_t>(j0 + r) * rv + col] = v[r][c];
+          }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        red_release_gpu_add(fp.up.tb.copied + lo, 1);
+      }
+    }
+  }
 
   // pair-units cover m-tiles (2q, 2q+1); with an odd count the last pair has
   // both CTAs on the same m-tile (the follower's copy is computed, not stored)
@@ -764,6 +813,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int nkb = down ? nkb_dn : nkb_up;
       const CUtensorMap* tm = down ? &tmB_dn : &tmB_up;
       if (down && npend > 0) drain();
+      if (!down && fp.cp_src != nullptr) {   // this expert's rows copied into X_perm? (acquire)
+        const int target = (s_end[w.e] - s_off[w.e] + 7) / 8;
+        if (elect_one()) {
+          while (ld_acquire_gpu(fp.up.tb.copied + w.e) < target) __nanosleep(64);
+          fence_proxy_async_global();
+        }
+        __syncwarp();
+      }
       if (down) {   // H rows of expert e complete? (acquire), then order the TMA after it
         const int target = 2 * (s_pref[w.e + 1] - s_pref[w.e]) * n_mp_up;
         if (elect_one()) {
@@ -1026,7 +1083,8 @@ namespace {
 template <int AS, int BS, int KA, bool kT = false>
 cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                          const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn, const TcParams& up,
-                         const TcParams& dn, int32_t* done, int grid, cudaStream_t s) {
+                         const TcParams& dn, int32_t* done, const void* cp_src, void* cp_dst,
+                         int cp_row_vecs, int grid, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS, KA, kT>,
@@ -1035,7 +1093,8 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  FusedParams fp{up, dn, done};
+  FusedParams fp{up, dn, done, static_cast<const uint4*>(cp_src), static_cast<uint4*>(cp_dst),
+                 cp_row_vecs};
   return launch_pdl(tc_moe_ffn_2sm<AS, BS, KA, kT>, dim3(grid & ~1), dim3(kThreads),
                     smem_bytes_2sm(up.E, AS * KA, BS * KA), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
 }
@@ -1043,14 +1102,18 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
 
 cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
-                              const TcParams& up, const TcParams& dn, int32_t* done, int grid,
+                              const TcParams& up, const TcParams& dn, int32_t* done,
+                              const void* cp_src, void* cp_dst, int cp_row_vecs, int grid,
                               cudaStream_t s) {
   // MOESHARD_TC_VARIANT 20: two k-atoms per ring stage (3 + 3 stages of 32 KB)
   if (variant() == 21)
-    return launch_fused<6, 6, 1, true>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, grid, s);
+    return launch_fused<6, 6, 1, true>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src,
+                                       cp_dst, cp_row_vecs, grid, s);
   if (variant() == 20 && up.K % 128 == 0 && dn.K % 128 == 0 && !up.gather_cp)
-    return launch_fused<3, 3, 2>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, grid, s);
-  return launch_fused<6, 6, 1>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, grid, s);
+    return launch_fused<3, 3, 2>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src, cp_dst,
+                                 cp_row_vecs, grid, s);
+  return launch_fused<6, 6, 1>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src, cp_dst,
+                               cp_row_vecs, grid, s);
 }
 
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,

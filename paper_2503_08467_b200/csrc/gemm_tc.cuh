@@ -88,9 +88,13 @@ cudaError_t launch_route_group_tc(const CUtensorMap& tmX, const CUtensorMap& tmW
 // done: [E] int32 zeroed before the launch (Step 2 does it).
 // tmB_up: X_perm [N][h] box {64, 16} - or, when up.gather != nullptr, x_all [N][h]
 // box {64, 1} for TMA gather4.
+// cp_src != nullptr: the kernel itself copies X_perm[j] = cp_src[perm_pad[j]] (rows of
+// cp_row_vecs 16-B vectors) into cp_dst before the up-projection reads it (Step 2
+// then skips its row copy); per-expert release/acquire on tb.copied.
 cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
-                              const TcParams& up, const TcParams& dn, int32_t* done, int grid,
+                              const TcParams& up, const TcParams& dn, int32_t* done,
+                              const void* cp_src, void* cp_dst, int cp_row_vecs, int grid,
                               cudaStream_t s);
 
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,

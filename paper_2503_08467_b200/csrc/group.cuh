@@ -79,6 +79,7 @@ __device__ __forceinline__ void segment_tables(int E, const int* s_tot, const in
     block_excl_scan<kThreads>(rows, s_warp, tot_rows);
     if (e < E) {
       tb.done[e] = 0;
+      tb.copied[e] = 0;
       tb.pos[e] = pos;
       tb.counts[e] = cnt;
       tb.tc_chunk_size[e] = cs;

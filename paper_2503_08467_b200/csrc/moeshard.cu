@@ -114,6 +114,8 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
   return r == CUDA_SUCCESS;
 }
 
+constexpr int kL2PersistDefaultMB = 64;   // measured best of 0/32/48/64/79 MB on c2
+
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 // Workspace carve-up, shared by moeshard_workspace_size and moeshard_init.
@@ -141,7 +143,7 @@ Layout make_layout(const moeshard_config& c, int world) {
   L.route = take(Nmax * sizeof(RouteRec));
   L.block_hist = take(nb * E * 4);
   L.block_base = take(nb * E * 4);
-  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + E + (E + 1));
+  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + E + (E + 1) + E);
   L.npad = (Nmax + kSegAlign * E + 63) / 64 * 64;
   L.ints = take(L.n_ints * 4);
   L.perm = take(Nmax * 4);
@@ -339,12 +341,16 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->use_tc = cfg->dtype == MOESHARD_BF16 && !(c->cfg.flags & MOESHARD_FLAG_SIMT_GEMM);
   if (const char* pf = getenv("MOESHARD_L2_PREFETCH_MB")) c->pf_bytes = atoll(pf) << 20;
   if (const char* gd = getenv("MOESHARD_GATHER_DEPTH")) c->gather_depth = std::max(1, std::min(5, atoi(gd)));
-  if (const char* pl = getenv("MOESHARD_L2_PERSIST_MB")) {   // experiment: L2 set-aside for evict_last lines
-    size_t want = static_cast<size_t>(atoll(pl)) << 20, got = 0;
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
-    fprintf(stderr, "[moeshard] persisting L2 limit %zu MB (max %d MB)\n", got >> 20,
-            prop.persistingL2CacheMaxSize >> 20);
+  // L2 set-aside for the kernels' evict_last lines (H between the two products, the
+  // expert-ordered token rows re-read by every feature tile): without it the
+  // 128-B-line hints lose to the weight stream. Raised, never lowered; device-wide.
+  if (c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_NO_L2_PERSIST)) {
+    size_t want = static_cast<size_t>(kL2PersistDefaultMB) << 20, cur = 0;
+    if (const char* pl = getenv("MOESHARD_L2_PERSIST_MB")) want = static_cast<size_t>(atoll(pl)) << 20;
+    want = std::min(want, static_cast<size_t>(prop.persistingL2CacheMaxSize));
+    if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur < want)
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    cudaGetLastError();   // a refused set-aside is not an error (e.g. MIG, MPS)
   }
   c->L = L;
   c->ws = static_cast<char*>(workspace);
@@ -364,6 +370,7 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->tb.done = c->tb.stats + 8;
   c->block_tot = c->tb.done + E;
   c->tb.pos = c->block_tot + E;
+  c->tb.copied = c->tb.pos + (E + 1);
   c->tb.perm_pad = reinterpret_cast<int32_t*>(c->ws + L.perm_pad);
   c->perm = reinterpret_cast<int32_t*>(c->ws + L.perm);
   c->x_all = c->coll ? c->ws + L.x_all : nullptr;
@@ -479,6 +486,9 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   // token rows gathered by the FFN itself (no X_perm copy): TMA gather4 or cp.async
   const bool gather_cp = fused && (c->cfg.flags & MOESHARD_FLAG_CPASYNC_GATHER);
   const bool gather = fused && ((c->cfg.flags & MOESHARD_FLAG_TMA_GATHER) || gather_cp);
+  // opt-in: the Sec. 3.3 row copy inside the FFN launch (per-expert hand-off); measured
+  // slower than copying in the grouping launch (the copy's HBM bytes stay on the path)
+  const bool copy_in_ffn = fused && !gather && (c->cfg.flags & MOESHARD_FLAG_ROW_COPY_IN_FFN);
   // world = 1: the router launch also runs Step 2 (grid barriers need every CTA resident)
   const bool route_group = c->use_tc && !c->coll && (E % 8) == 0 && nbr <= c->num_sms &&
                            h <= 1024 && c->pf_bytes == 0 &&
@@ -489,7 +499,8 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
       return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden/router_w");
     RouteGroupArgs ga{c->tb, c->block_base, c->block_tot, c->perm,
                       static_cast<const uint4*>(hidden),
-                      gather ? nullptr : static_cast<uint4*>(c->x_perm), h * c->elt / 16,
+                      gather || copy_in_ffn ? nullptr : static_cast<uint4*>(c->x_perm),
+                      h * c->elt / 16,
                       F / kTcFeatTile, h / kTcFeatTile, c->tb.stats + 4};
     CUDA_TRY(c, launch_route_group_tc(tm_x, tm_w, n, h, E, c->EP, forced, my_route, my_hist,
                                       err_flag, ga, s));
@@ -535,7 +546,7 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   if (!route_group) {
     launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb, F / kTcFeatTile,
                         h / kTcFeatTile, c->route, x_all, n, nbr, HB, h * c->elt, c->perm,
-                        gather ? nullptr : c->x_perm, s);
+                        gather || copy_in_ffn ? nullptr : c->x_perm, s);
     c->launches += 2;
   }
   c->mark(3, s);
@@ -553,7 +564,9 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
                 static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route, nullptr, 0, ht, np};
     CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather && !gather_cp ? tm_xg : c->tm_xperm16, lw.tm_out,
-                                  ht ? c->tm_Ht : c->tm_H16, up, dn, c->tb.done, c->num_sms, s));
+                                  ht ? c->tm_Ht : c->tm_H16, up, dn, c->tb.done,
+                                  copy_in_ffn ? x_all : nullptr, c->x_perm, h * c->elt / 16,
+                                  c->num_sms, s));
     c->mark(4, s);
     c->launches += 1;
   } else if (c->use_tc) {

@@ -27,6 +27,8 @@ MOESHARD_FLAG_TMA_GATHER = 0x8
 MOESHARD_FLAG_H_TRANSPOSED = 0x10
 MOESHARD_FLAG_FUSED_ROUTE_GROUP = 0x20
 MOESHARD_FLAG_CPASYNC_GATHER = 0x40
+MOESHARD_FLAG_NO_L2_PERSIST = 0x80
+MOESHARD_FLAG_ROW_COPY_IN_FFN = 0x100
 
 STATUS = {
     0: "MOESHARD_OK", -1: "MOESHARD_ERR_INVALID_ARG", -2: "MOESHARD_ERR_SHAPE",

@@ -39,12 +39,34 @@ for routing in ("uniform", "zipf"):
     e.record()
     torch.cuda.synchronize()
     us = s.elapsed_time(e) / steps * 1e3
+    # CUDA-graph replay of NW forwards (one per weight set), as bench.py times it
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        for k in range(NW):
+            fwd(k)
+    torch.cuda.current_stream().wait_stream(st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for k in range(NW):
+            fwd(k)
+    reps = max(1, steps // NW)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(reps):
+        g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    us_graph = s.elapsed_time(e) / (reps * NW) * 1e3
     L.profile(True)
     for k in range(min(steps, 500)):
         fwd(k)
     ph, cnt = L.phase_ms()
     L.profile(False)
-    res[routing] = {"step_us": round(us, 2),
+    res[routing] = {"step_us": round(us_graph, 2), "step_us_eager": round(us, 2),
                     "phases_us": {k: round(1e3 * v / max(cnt, 1), 2) for k, v in ph.items()},
                     "stats": L.stats()}
 print(json.dumps(res))

@@ -390,7 +390,7 @@ def test_route_group_fused_matches_separate_and_oracle(N, h, d_ff, E, routing):
     _check_layer(inp, outs[0], routes[0], tol=BF16_TOL)
 
 
-@pytest.mark.parametrize("flag", ["FUSED_ROUTE_GROUP", "CPASYNC_GATHER", None])
+@pytest.mark.parametrize("flag", ["FUSED_ROUTE_GROUP", "CPASYNC_GATHER", "ROW_COPY_IN_FFN", None])
 def test_forward_under_cuda_graph_replay(flag):
     """A captured forward replays correctly with new token values and new routing
     (the grid barrier of the fused route+group launch carries no launch arguments)."""
@@ -431,22 +431,24 @@ def test_forward_under_cuda_graph_replay(flag):
     L.close()
 
 
-# --------------------------------------------------------------------- cp.async token gather
+# --------------------------------------------------------------------- alternative token paths
+@pytest.mark.parametrize("flag", ["ROW_COPY_IN_FFN", "CPASYNC_GATHER", "TMA_GATHER", "FUSED_ROUTE_GROUP"])
 @pytest.mark.parametrize("N,h,d_ff,E,routing", [
     (3000, 512, 1024, 64, "zipf"),       # multi-chunk segments, ragged halves
-    (1000, 256, 512, 8, "uniform"),
     (777, 384, 640, 16, "patho"),        # odd tile counts (duplicated last pair), empty experts
     (8192, 768, 3072, 64, "zipf"),       # C2 shape
 ])
-def test_cpasync_gather_matches_xperm_path_bitwise_and_oracle(N, h, d_ff, E, routing):
-    """The FFN gathering token rows itself (cp.async, zero-filled padding rows) gives
-    the same bits as reading the X_perm copy, and matches the oracle."""
+def test_token_paths_bitwise_equal_and_match_oracle(flag, N, h, d_ff, E, routing):
+    """How the expert-ordered token rows reach the up-projection (copied by the grouping
+    launch - the default -, copied inside the FFN launch, gathered by cp.async or TMA
+    gather4, grouped inside the router launch) changes no arithmetic: outputs and
+    routing tables are identical bit for bit, and match the oracle."""
     from paper_2503_08467_b200 import MoEShardLayer
-    from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_CPASYNC_GATHER
+    from paper_2503_08467_b200 import moeshard as C
     inp = W.make_layer_inputs(26, N, h, d_ff, E, dtype=torch.bfloat16, routing=routing, k=1)
     f = inp.forced.cuda().contiguous()
     ys, routes = [], []
-    for flags in (MOESHARD_FLAG_CPASYNC_GATHER, 0):
+    for flags in (getattr(C, f"MOESHARD_FLAG_{flag}"), 0):
         L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16, flags=flags)
         L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
         for _ in range(2):
@@ -457,5 +459,7 @@ def test_cpasync_gather_matches_xperm_path_bitwise_and_oracle(N, h, d_ff, E, rou
         routes.append({k: v.cpu().numpy() for k, v in L.routing(N).items()})
         L.close()
     assert torch.equal(ys[0], ys[1])
+    for k in routes[0]:
+        np.testing.assert_array_equal(routes[0][k], routes[1][k])
     if N <= 3000:
         _check_layer(inp, ys[0], routes[0], tol=BF16_TOL)
