@@ -200,7 +200,10 @@ def _config_json(cfg, args, G):
     return {"workload": cfg["name"], "d_model": cfg["h"], "d_ff": cfg["d_ff"], "experts": cfg["E"],
             "tokens_global": cfg["N"], "tokens_per_rank": cfg["N"] // G, "top_k": 1,
             "parallelism": f"moeshard expert-sharding x{G} (each rank: 1/{G} of every expert)",
-            "routing": "natural learned-style router (near-uniform); skewed = Zipf(1.2) forced"}
+            "routing": "natural learned-style router (near-uniform); skewed = Zipf(1.2) forced",
+            "transport": ("none (one GPU)" if G == 1 else
+                          "peer-memory stores (MOESHARD_FLAG_P2P)" if getattr(args, "transport", "nccl") == "p2p"
+                          else "NCCL AllGather + ReduceScatter")}
 
 
 # ------------------------------------------------------------------ encoder TTFT
@@ -279,6 +282,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="G > 1 token / partial exchange: NCCL collectives, or device-initiated "
+                         "stores into peer memory (MOESHARD_FLAG_P2P)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sustained", type=int, default=5000,
@@ -320,8 +326,10 @@ def main():
     # weight sets: rotate so a step's weights were evicted from L2 by the previous steps
     per_set = 2 * E * h * F * 2
     NW = max(1, math.ceil(3 * L2_BYTES / per_set))
+    from paper_2503_08467_b200 import moeshard as C
     layer = MoEShardLayer(h, d_ff, E, n_layers=NW, max_tokens_per_rank=n, dtype=torch.bfloat16,
-                          rank=rank, world=G, device=local)
+                          rank=rank, world=G, device=local,
+                          flags=C.MOESHARD_FLAG_P2P if args.transport == "p2p" else 0)
     for l in range(NW):
         wi, wo = W.make_expert_weights(seed, E, h, d_ff, cols=(c0, c1), device=dev, layer=l)
         layer.load_expert_shards(l, wi, wo)

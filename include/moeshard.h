@@ -76,6 +76,15 @@ typedef enum {
 #define MOESHARD_FLAG_CPASYNC_GATHER 0x40u    /* bf16 fused mode: the FFN gathers token rows with cp.async (no X_perm copy; experimental, slower) */
 #define MOESHARD_FLAG_NO_L2_PERSIST 0x80u     /* bf16 mode: leave the device's persisting-L2 limit alone (see moeshard_init) */
 #define MOESHARD_FLAG_ROW_COPY_IN_FFN 0x100u  /* bf16 fused mode: copy token rows into expert order inside the FFN launch (per-expert hand-off; experimental, slower) */
+#define MOESHARD_FLAG_P2P 0x200u              /* bf16: Steps 3 and 5 by device-initiated stores into peer GPU memory instead of NCCL (see moeshard_p2p_*) */
+
+/* moeshard_forward_stages masks: ROUTE = Step 1 + the token exchange (Step 3 push),
+ * COMPUTE = Steps 2 and 4 (+ the Step 5 send in P2P mode), REDUCE = the Step 5 aggregate. */
+#define MOESHARD_STAGE_ROUTE 0x1
+#define MOESHARD_STAGE_COMPUTE 0x2
+#define MOESHARD_STAGE_REDUCE 0x4
+#define MOESHARD_STAGE_ALL 0x7
+#define MOESHARD_P2P_HANDLE_BYTES 64
 
 typedef struct {
   int32_t d_model;             /* h; multiple of 128 */
@@ -156,6 +165,39 @@ int moeshard_forward(moeshard_ctx* ctx, int layer, const void* hidden, int n_loc
  *   offsets    [dev] int32 [E+1]            exclusive scan of counts
  *   perm       [dev] int32 [world*n_local]  global token ids grouped by expert,
  *                                           ascending inside each expert */
+/* moeshard_forward split into stages (a mask of MOESHARD_STAGE_*), run in order
+ * ROUTE -> COMPUTE -> REDUCE with the same layer / n_local; moeshard_forward ==
+ * all three. Lets a caller interleave other work between the exchange steps, or
+ * drive several ranks that share one GPU in lock-step (each stage's waits are then
+ * already satisfied). Errors: as moeshard_forward; PROTOCOL if n_local differs
+ * from the ROUTE stage's or P2P is configured but not connected. */
+int moeshard_forward_stages(moeshard_ctx* ctx, int layer, const void* hidden, int n_local,
+                            const void* router_w, void* hidden_out, const int32_t* forced_expert,
+                            int stages, void* stream);
+
+/* Peer-memory exchange (MOESHARD_FLAG_P2P). Each rank's context owns one
+ * exchange region - the only device memory the library allocates (cudaMalloc in
+ * moeshard_init, freed by moeshard_destroy): flags, the rank-major x_all / route
+ * records / block histograms every rank pushes into (Step 3), and G receive
+ * slots the down-projection epilogues of all ranks store their partial output
+ * rows into (Step 5). Setup, once, after moeshard_init on every rank:
+ *   1. moeshard_p2p_export: this region's CUDA IPC handle (64 bytes [host] out);
+ *   2. exchange the handles between the ranks (e.g. torch.distributed all_gather);
+ *   3. moeshard_p2p_open: map a peer's handle in this process ([host] out:
+ *      device pointer; closed at destroy). Ranks that share a process use
+ *      moeshard_p2p_region's pointers directly instead;
+ *   4. moeshard_p2p_connect(regions[world]): [host] array of every rank's region
+ *      as seen from this process; regions[rank] must be this context's own.
+ * moeshard_forward then needs no NCCL: every cross-rank wait inside it is a
+ * bounded spin on a flag in the local region; a peer that never arrives makes
+ * moeshard_check return PROTOCOL instead of hanging. Errors: CONFIG (context
+ * without MOESHARD_FLAG_P2P), INVALID_ARG, PROTOCOL, CUDA. */
+int moeshard_p2p_region(moeshard_ctx* ctx, void** dev_ptr, size_t* bytes);
+int moeshard_p2p_export(moeshard_ctx* ctx, uint8_t handle[MOESHARD_P2P_HANDLE_BYTES]);
+int moeshard_p2p_open(moeshard_ctx* ctx, const uint8_t handle[MOESHARD_P2P_HANDLE_BYTES],
+                      void** dev_ptr);
+int moeshard_p2p_connect(moeshard_ctx* ctx, void* const* regions);
+
 int moeshard_get_routing(moeshard_ctx* ctx, int32_t* expert_all, float* gate_all, int32_t* counts,
                          int32_t* offsets, int32_t* perm, void* stream);
 

@@ -166,8 +166,16 @@ __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok
       const uint4 v = reinterpret_cast<const uint4*>(stage)[q];
       if (kDown) {
         const int rj = __shfl_sync(0xffffffffu, row, j);
-        if (c0 + j < ntok)
-          *reinterpret_cast<uint4*>(p.out + (size_t)rj * p.ld_out + fbase + part * 8) = v;
+        if (c0 + j < ntok) {
+          __nv_bfloat16* dst;
+          if (p.p2p_n > 0) {   // the owner's receive slot for this rank, over NVLink
+            const int o = rj / p.p2p_n;
+            dst = p.p2p_out[o] + (size_t)(rj - o * p.p2p_n) * p.ld_out;
+          } else {
+            dst = p.out + (size_t)rj * p.ld_out;
+          }
+          *reinterpret_cast<uint4*>(dst + fbase + part * 8) = v;
+        }
       } else if (c0 + j < ntok) {
         st_v4_hint(p.out + (size_t)(tok0 + c0 + j) * p.ld_out + fbase + part * 8, v, pol_keep);
       }
@@ -995,6 +1003,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       as ^= 1;
       if (as == 0) aphase ^= 1;
     }
+    if (fp.dn.p2p_n > 0) __threadfence_system();   // remote partial rows before the signal kernel
   }
 
   tc_fence_before();

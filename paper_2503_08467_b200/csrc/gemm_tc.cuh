@@ -41,6 +41,10 @@ struct TcParams {
   bool gather_cp = false;
   const __nv_bfloat16* gsrc = nullptr;
   int gather_depth = 4;    // stages in flight before one is published (<= ring depth - 1)
+  // down, peer-memory exchange (MOESHARD_FLAG_P2P): p2p_n > 0 sends the partial row of
+  // global token t to its owner o = t / p2p_n, row t - o * p2p_n of p2p_out[o]
+  int p2p_n = 0;
+  __nv_bfloat16* p2p_out[kMaxWorld] = {};
 };
 
 // Step 2 outputs for the fused route+group launch (world = 1): see launch_route_group_tc.

@@ -34,6 +34,7 @@
 #include "../../include/moeshard.h"
 #include "common.cuh"
 #include "gemm_tc.cuh"
+#include "p2p.cuh"
 
 using namespace moeshard;
 
@@ -126,7 +127,8 @@ struct Layout {
 };
 
 Layout make_layout(const moeshard_config& c, int world) {
-  const bool coll = world > 1 || (c.flags & MOESHARD_FLAG_FORCE_COLLECTIVES);
+  const bool p2p = (c.flags & MOESHARD_FLAG_P2P) != 0;   // x_all / partials live in the region
+  const bool coll = !p2p && (world > 1 || (c.flags & MOESHARD_FLAG_FORCE_COLLECTIVES));
   const size_t elt = c.dtype == MOESHARD_BF16 ? 2 : 4;
   const size_t Nmax = static_cast<size_t>(world) * c.max_tokens_per_rank;
   // hist-blocks: >= 64 tokens each (128 for the tcgen05 router), per rank
@@ -181,6 +183,13 @@ struct moeshard_ctx {
   int EP = 16;
   std::vector<LayerW> layers;
   ncclComm_t comm = nullptr;
+  // peer-memory exchange (MOESHARD_FLAG_P2P): this rank's region (library-owned) and
+  // every rank's region as mapped here; opened IPC mappings are closed at destroy
+  bool p2p = false, connected = false;
+  char* region = nullptr;
+  P2PLayout PL{};
+  P2PArgs pa{};
+  std::vector<void*> ipc_opened;
   int last_n = 0;
   int64_t launches = 0;  // cumulative kernel launches of this context
   long long pf_bytes = 0;  // experimental L2 weight prefetch during routing (MOESHARD_L2_PREFETCH_MB)
@@ -240,6 +249,12 @@ int validate(const moeshard_config* c, int world) {
     return fail(nullptr, MOESHARD_ERR_CONFIG, "d_ff/world=%d must be a multiple of 128",
                 c->d_ff / world);
   if (c->n_layers < 1) return fail(nullptr, MOESHARD_ERR_CONFIG, "n_layers=%d < 1", c->n_layers);
+  if ((c->flags & MOESHARD_FLAG_P2P) &&
+      (c->dtype != MOESHARD_BF16 || world > kMaxWorld ||
+       (c->flags & (MOESHARD_FLAG_SIMT_GEMM | MOESHARD_FLAG_UNFUSED_GEMM | MOESHARD_FLAG_FORCE_COLLECTIVES))))
+    return fail(nullptr, MOESHARD_ERR_CONFIG,
+                "MOESHARD_FLAG_P2P needs bf16, the fused tcgen05 FFN, no FORCE_COLLECTIVES and "
+                "world <= %d (world=%d)", kMaxWorld, world);
   if (c->max_tokens_per_rank < 0 ||
       static_cast<long long>(c->max_tokens_per_rank) * world > (1LL << 30))
     return fail(nullptr, MOESHARD_ERR_CONFIG, "max_tokens_per_rank=%d out of range",
@@ -337,7 +352,9 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->F = cfg->d_ff / world;
   c->E = cfg->n_experts;
   c->elt = cfg->dtype == MOESHARD_BF16 ? 2 : 4;
-  c->coll = world > 1 || (c->cfg.flags & MOESHARD_FLAG_FORCE_COLLECTIVES);
+  c->p2p = (c->cfg.flags & MOESHARD_FLAG_P2P) != 0;
+  // coll: tokens of all ranks are exchanged (rank-major x_all / route / hist buffers)
+  c->coll = world > 1 || (c->cfg.flags & MOESHARD_FLAG_FORCE_COLLECTIVES) || c->p2p;
   c->use_tc = cfg->dtype == MOESHARD_BF16 && !(c->cfg.flags & MOESHARD_FLAG_SIMT_GEMM);
   if (const char* pf = getenv("MOESHARD_L2_PREFETCH_MB")) c->pf_bytes = atoll(pf) << 20;
   if (const char* gd = getenv("MOESHARD_GATHER_DEPTH")) c->gather_depth = std::max(1, std::min(5, atoi(gd)));
@@ -373,10 +390,10 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->tb.copied = c->tb.pos + (E + 1);
   c->tb.perm_pad = reinterpret_cast<int32_t*>(c->ws + L.perm_pad);
   c->perm = reinterpret_cast<int32_t*>(c->ws + L.perm);
-  c->x_all = c->coll ? c->ws + L.x_all : nullptr;
+  c->x_all = c->coll && !c->p2p ? c->ws + L.x_all : nullptr;
   c->x_perm = c->ws + L.x_perm;
   c->H = c->ws + L.H;
-  c->partial = c->coll ? c->ws + L.partial : nullptr;
+  c->partial = c->coll && !c->p2p ? c->ws + L.partial : nullptr;
   c->layers.resize(cfg->n_layers);
   cudaError_t e = cudaMemset(ints, 0, L.n_ints * 4);
   if (e != cudaSuccess) {
@@ -396,7 +413,33 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
       return fail(nullptr, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
     }
   }
-  if (c->coll) {
+  if (c->p2p) {
+    // the exchange region: the one device allocation the library owns (CUDA IPC needs
+    // the base of a cudaMalloc); x_all / route records / block histograms live in it
+    const int nbr_max = (cfg->max_tokens_per_rank + 63) / 64;
+    c->PL = p2p_layout(world, std::max(1, cfg->max_tokens_per_rank), c->h, E, std::max(1, nbr_max));
+    void* reg = nullptr;
+    cudaError_t er = cudaMalloc(&reg, c->PL.total);
+    if (er == cudaSuccess) er = cudaMemset(reg, 0, c->PL.total);
+    if (er != cudaSuccess) {
+      if (reg) cudaFree(reg);
+      delete c;
+      return fail(nullptr, MOESHARD_ERR_CUDA, "exchange region (%zu B): %s", c->PL.total,
+                  cudaGetErrorString(er));
+    }
+    c->region = static_cast<char*>(reg);
+    c->x_all = c->region + c->PL.off_x;
+    c->route = reinterpret_cast<RouteRec*>(c->region + c->PL.off_route);
+    c->block_hist = reinterpret_cast<int32_t*>(c->region + c->PL.off_hist);
+    c->pa.self = c->region;
+    c->pa.rank = rank;
+    c->pa.world = world;
+    c->pa.n_max = std::max(1, cfg->max_tokens_per_rank);
+    c->pa.off_x = c->PL.off_x;
+    c->pa.off_route = c->PL.off_route;
+    c->pa.off_hist = c->PL.off_hist;
+    c->pa.off_recv = c->PL.off_recv;
+  } else if (c->coll) {
     if (!uid) {
       delete c;
       return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "uid is NULL but a communicator is needed");
@@ -455,7 +498,19 @@ int moeshard_load_expert_shards(moeshard_ctx* c, int layer, const void* w_in_sha
 
 int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, const void* router_w,
                      void* hidden_out, const int32_t* forced, void* stream) {
+  return moeshard_forward_stages(c, layer, hidden, n, router_w, hidden_out, forced,
+                                 MOESHARD_STAGE_ALL, stream);
+}
+
+int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int n,
+                            const void* router_w, void* hidden_out, const int32_t* forced,
+                            int stages, void* stream) {
   if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "ctx is NULL");
+  if (stages <= 0 || (stages & ~MOESHARD_STAGE_ALL))
+    return fail(c, MOESHARD_ERR_INVALID_ARG, "stages=%d is not a non-empty MOESHARD_STAGE_* mask",
+                stages);
+  if (c->p2p && !c->connected)
+    return fail(c, MOESHARD_ERR_PROTOCOL, "MOESHARD_FLAG_P2P: moeshard_p2p_connect was not called");
   if (layer < 0 || layer >= c->cfg.n_layers)
     return fail(c, MOESHARD_ERR_BOUNDS, "layer=%d not in [0, %d)", layer, c->cfg.n_layers);
   if (!c->layers[layer].loaded)
@@ -468,8 +523,13 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const LayerW& lw = c->layers[layer];
   const int h = c->h, F = c->F, E = c->E;
+  if (!(stages & MOESHARD_STAGE_ROUTE) && n != c->last_n)
+    return fail(c, MOESHARD_ERR_PROTOCOL, "n_local=%d differs from the ROUTE stage's %d", n,
+                c->last_n);
   c->last_n = n;
   if (n == 0) return MOESHARD_OK;
+  const bool st_route = stages & MOESHARD_STAGE_ROUTE, st_compute = stages & MOESHARD_STAGE_COMPUTE,
+             st_reduce = stages & MOESHARD_STAGE_REDUCE;
   const ncclDataType_t ndt = c->cfg.dtype == MOESHARD_BF16 ? ncclBfloat16 : ncclFloat32;
   int32_t* err_flag = c->tb.stats + 3;
 
@@ -493,7 +553,9 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   const bool route_group = c->use_tc && !c->coll && (E % 8) == 0 && nbr <= c->num_sms &&
                            h <= 1024 && c->pf_bytes == 0 &&
                            (c->cfg.flags & MOESHARD_FLAG_FUSED_ROUTE_GROUP);
-  if (route_group) {
+  if (!st_route) {
+    // (routing and the token exchange ran in an earlier call)
+  } else if (route_group) {
     CUtensorMap tm_x, tm_w;
     if (!make_tmap(&tm_x, hidden, h, n, 128) || !make_tmap(&tm_w, router_w, E, h, 64))
       return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden/router_w");
@@ -526,8 +588,12 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
   }
   c->mark(1, s);
   // Steps 2+3: metadata + token scatter (replicate all tokens on all GPUs)
-  const void* x_all = hidden;
-  if (c->coll) {
+  const void* x_all = c->coll ? c->x_all : hidden;
+  if (st_route && c->p2p) {
+    // Step 3 over peer memory: push this rank's tokens / records / histograms to every rank
+    CUDA_TRY(c, launch_p2p_push(c->pa, hidden, n, h * c->elt / 16, nbr, E, c->num_sms, s));
+    c->launches += 1;
+  } else if (st_route && c->coll) {
     NCCL_TRY(c, nccl().GroupStart());
     NCCL_TRY(c, nccl().AllGather(hidden, c->x_all, static_cast<size_t>(n) * h, ndt, c->comm, s));
     NCCL_TRY(c, nccl().AllGather(my_route, c->route, static_cast<size_t>(n) * 2, ncclInt32,
@@ -535,64 +601,130 @@ int moeshard_forward(moeshard_ctx* c, int layer, const void* hidden, int n, cons
     NCCL_TRY(c, nccl().AllGather(my_hist, c->block_hist, static_cast<size_t>(nbr) * E, ncclInt32,
                                  c->comm, s));
     NCCL_TRY(c, nccl().GroupEnd());
-    x_all = c->x_all;
   }
   c->mark(2, s);
-  CUtensorMap tm_xg;   // x_all rows for TMA gather4 (box {64, 1})
-  if (gather && !gather_cp && !make_tmap(&tm_xg, x_all, h, N, 1))
-    return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for the gather map");
-  // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs (the row
-  // copy is skipped when the FFN gathers rows itself)
-  if (!route_group) {
-    launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb, F / kTcFeatTile,
-                        h / kTcFeatTile, c->route, x_all, n, nbr, HB, h * c->elt, c->perm,
-                        gather || copy_in_ffn ? nullptr : c->x_perm, s);
-    c->launches += 2;
+  if (st_compute) {
+    if (c->p2p) {   // every rank's Step-3 data has landed here (bounded wait)
+      CUDA_TRY(c, launch_p2p_wait_tokens(c->pa, err_flag, s));
+      c->launches += 1;
+    }
+    CUtensorMap tm_xg;   // x_all rows for TMA gather4 (box {64, 1})
+    if (gather && !gather_cp && !make_tmap(&tm_xg, x_all, h, N, 1))
+      return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for the gather map");
+    // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs (the row
+    // copy is skipped when the FFN gathers rows itself)
+    if (!route_group) {
+      launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb,
+                          F / kTcFeatTile, h / kTcFeatTile, c->route, x_all, n, nbr, HB,
+                          h * c->elt, c->perm, gather || copy_in_ffn ? nullptr : c->x_perm, s);
+      c->launches += 2;
+    }
+    c->mark(3, s);
+    // Step 4: expert computation, one grouped product per projection
+    void* P = c->coll && !c->p2p ? c->partial : hidden_out;
+    if (fused) {
+      // MOESHARD_FLAG_H_TRANSPOSED (experimental): H stored as H^T [F][npad]; the up
+      // epilogue writes feature rows directly and the down product reads an MN-major tile
+      const bool ht = (c->cfg.flags & MOESHARD_FLAG_H_TRANSPOSED) != 0;
+      const int np = static_cast<int>(c->L.npad);
+      TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
+                  static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr,
+                  gather ? c->tb.perm_pad : nullptr, N, ht, np, gather_cp,
+                  static_cast<const __nv_bfloat16*>(x_all), c->gather_depth};
+      TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
+                  static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route, nullptr, 0, ht, np};
+      if (c->p2p) {   // Step 5 send: partial rows go straight to their owner's receive slot
+        dn.p2p_n = n;
+        for (int g = 0; g < c->world; ++g)
+          dn.p2p_out[g] = reinterpret_cast<__nv_bfloat16*>(
+              c->pa.peers[g] + c->PL.off_recv +
+              static_cast<size_t>(c->rank) * c->pa.n_max * h * 2);
+      }
+      CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather && !gather_cp ? tm_xg : c->tm_xperm16,
+                                    lw.tm_out, ht ? c->tm_Ht : c->tm_H16, up, dn, c->tb.done,
+                                    copy_in_ffn ? x_all : nullptr, c->x_perm, h * c->elt / 16,
+                                    c->num_sms, s));
+      c->mark(4, s);
+      c->launches += 1;
+      if (c->p2p) {
+        CUDA_TRY(c, launch_p2p_signal_partials(c->pa, s));
+        c->launches += 1;
+      }
+    } else if (c->use_tc) {
+      TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
+                  static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
+      CUDA_TRY(c, launch_tc_gemm(false, lw.tm_in, c->tm_xperm, c->tm_xperm16, up, c->num_sms, s));
+      c->mark(4, s);
+      TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
+                  static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
+      CUDA_TRY(c, launch_tc_gemm(true, lw.tm_out, c->tm_H, c->tm_H16, dn, c->num_sms, s));
+      c->launches += 2;
+    } else {
+      launch_simt_up(c->cfg.dtype, c->x_perm, lw.wt_in, h, F, E, c->tb, c->H, c->num_sms, s);
+      c->mark(4, s);
+      launch_simt_down(c->cfg.dtype, c->H, lw.wt_out, F, h, E, c->tb, c->tb.perm_pad, c->route, P,
+                       c->num_sms, s);
+      c->launches += 2;
+    }
+    CUDA_TRY(c, cudaGetLastError());
   }
-  c->mark(3, s);
-  // Step 4: expert computation, one grouped product per projection
-  void* P = c->coll ? c->partial : hidden_out;
-  if (fused) {
-    // MOESHARD_FLAG_H_TRANSPOSED (experimental): H stored as H^T [F][npad]; the up epilogue
-    // writes feature rows directly and the down product reads an MN-major token tile
-    const bool ht = (c->cfg.flags & MOESHARD_FLAG_H_TRANSPOSED) != 0;
-    const int np = static_cast<int>(c->L.npad);
-    TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
-                static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr,
-                gather ? c->tb.perm_pad : nullptr, N, ht, np, gather_cp,
-                static_cast<const __nv_bfloat16*>(x_all), c->gather_depth};
-    TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
-                static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route, nullptr, 0, ht, np};
-    CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather && !gather_cp ? tm_xg : c->tm_xperm16, lw.tm_out,
-                                  ht ? c->tm_Ht : c->tm_H16, up, dn, c->tb.done,
-                                  copy_in_ffn ? x_all : nullptr, c->x_perm, h * c->elt / 16,
-                                  c->num_sms, s));
-    c->mark(4, s);
-    c->launches += 1;
-  } else if (c->use_tc) {
-    TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
-                static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
-    CUDA_TRY(c, launch_tc_gemm(false, lw.tm_in, c->tm_xperm, c->tm_xperm16, up, c->num_sms, s));
-    c->mark(4, s);
-    TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
-                static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
-    CUDA_TRY(c, launch_tc_gemm(true, lw.tm_out, c->tm_H, c->tm_H16, dn, c->num_sms, s));
-    c->launches += 2;
-  } else {
-    launch_simt_up(c->cfg.dtype, c->x_perm, lw.wt_in, h, F, E, c->tb, c->H, c->num_sms, s);
-    c->mark(4, s);
-    launch_simt_down(c->cfg.dtype, c->H, lw.wt_out, F, h, E, c->tb, c->tb.perm_pad, c->route, P,
-                     c->num_sms, s);
-    c->launches += 2;
-  }
-  CUDA_TRY(c, cudaGetLastError());
   c->mark(5, s);
   // Step 5: gather partial outputs to their owner and sum (aggregateTokens)
-  if (c->coll)
-    NCCL_TRY(c, nccl().ReduceScatter(P, hidden_out, static_cast<size_t>(n) * h, ndt, ncclSum,
-                                     c->comm, s));
+  if (st_reduce && c->p2p) {
+    CUDA_TRY(c, launch_p2p_reduce(c->pa, n, h * c->elt / 16, hidden_out, err_flag, c->num_sms, s));
+    c->launches += 1;
+  } else if (st_reduce && c->coll) {
+    NCCL_TRY(c, nccl().ReduceScatter(c->partial, hidden_out, static_cast<size_t>(n) * h, ndt,
+                                     ncclSum, c->comm, s));
+  }
   c->mark(6, s);
   if (c->prof) c->prof_count++;
+  return MOESHARD_OK;
+}
+
+int moeshard_p2p_region(moeshard_ctx* c, void** dev_ptr, size_t* bytes) {
+  if (!c || !dev_ptr) return fail(c, MOESHARD_ERR_INVALID_ARG, "NULL ctx or dev_ptr");
+  if (!c->p2p) return fail(c, MOESHARD_ERR_CONFIG, "context was not created with MOESHARD_FLAG_P2P");
+  *dev_ptr = c->region;
+  if (bytes) *bytes = c->PL.total;
+  return MOESHARD_OK;
+}
+
+int moeshard_p2p_export(moeshard_ctx* c, uint8_t handle[MOESHARD_P2P_HANDLE_BYTES]) {
+  if (!c || !handle) return fail(c, MOESHARD_ERR_INVALID_ARG, "NULL ctx or handle");
+  if (!c->p2p) return fail(c, MOESHARD_ERR_CONFIG, "context was not created with MOESHARD_FLAG_P2P");
+  static_assert(sizeof(cudaIpcMemHandle_t) == MOESHARD_P2P_HANDLE_BYTES, "IPC handle size");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaIpcMemHandle_t hd;
+  CUDA_TRY(c, cudaIpcGetMemHandle(&hd, c->region));
+  memcpy(handle, &hd, sizeof(hd));
+  return MOESHARD_OK;
+}
+
+int moeshard_p2p_open(moeshard_ctx* c, const uint8_t handle[MOESHARD_P2P_HANDLE_BYTES],
+                      void** dev_ptr) {
+  if (!c || !handle || !dev_ptr) return fail(c, MOESHARD_ERR_INVALID_ARG, "NULL argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, handle, sizeof(hd));
+  void* p = nullptr;
+  CUDA_TRY(c, cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+  c->ipc_opened.push_back(p);
+  *dev_ptr = p;
+  return MOESHARD_OK;
+}
+
+int moeshard_p2p_connect(moeshard_ctx* c, void* const* regions) {
+  if (!c || !regions) return fail(c, MOESHARD_ERR_INVALID_ARG, "NULL ctx or regions");
+  if (!c->p2p) return fail(c, MOESHARD_ERR_CONFIG, "context was not created with MOESHARD_FLAG_P2P");
+  if (regions[c->rank] != c->region)
+    return fail(c, MOESHARD_ERR_PROTOCOL, "regions[rank=%d] is not this context's own region",
+                c->rank);
+  for (int g = 0; g < c->world; ++g) {
+    if (!regions[g]) return fail(c, MOESHARD_ERR_INVALID_ARG, "regions[%d] is NULL", g);
+    c->pa.peers[g] = static_cast<char*>(regions[g]);
+  }
+  c->connected = true;
   return MOESHARD_OK;
 }
 
@@ -676,6 +808,10 @@ int moeshard_check(moeshard_ctx* c, void* stream) {
   }
   if (flag) {
     cudaMemset(c->tb.stats + 3, 0, 4);
+    if (flag & 4)
+      return fail(c, MOESHARD_ERR_PROTOCOL,
+                  "MOESHARD_FLAG_P2P: a peer's tokens or partial outputs never arrived (wait timed "
+                  "out; did every rank call moeshard_forward?)");
     return fail(c, MOESHARD_ERR_BOUNDS, "forced_expert contained ids outside [0, %d)", c->E);
   }
   return MOESHARD_OK;
@@ -684,6 +820,9 @@ int moeshard_check(moeshard_ctx* c, void* stream) {
 int moeshard_destroy(moeshard_ctx* c) {
   if (!c) return MOESHARD_OK;
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  cudaSetDevice(c->device);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (c->region) cudaFree(c->region);
   for (auto& e : c->ev) cudaEventDestroy(e);
   delete c;
   return MOESHARD_OK;

@@ -1,0 +1,203 @@
+// p2p.cu - the two exchange steps of Alg. 1 done with device-initiated stores
+// into peer GPU memory instead of NCCL (MOESHARD_FLAG_P2P; SURVEY.md §8(f)
+// NEXT(1)): Step 3 "scatter tokens" and Step 5
+// "gather + aggregate".
+//
+// Every rank owns an exchange region (one cudaMalloc, mapped by every peer
+// through CUDA IPC or, for ranks sharing a process, directly):
+//   header: [0] epoch (forwards completed), [1] push CTA counter,
+//           flags_ag[g] at int 32*(1+g), flags_rs[g] at int 32*(1+G+g)
+//   x_all [G*n_max][h] bf16, route [G*n_max] RouteRec, hist [G*nbr_max][E] int32,
+//   recv [G][n_max][h] bf16 (slot g = rank g's partial output for this rank's tokens)
+// Step 3: push_tokens copies this rank's tokens, route records and block
+// histograms into slot r of every region (its own included), then its last CTA
+// publishes flags_ag[r] = epoch + 1 everywhere (release, system scope). The
+// grouping launch acquires all G flags before it reads x_all.
+// Step 5: the fused FFN's down-projection epilogue stores each partial row
+// straight into recv[r] of the row's owner (no partial buffer, no separate
+// collective); rs_signal then publishes flags_rs[r] = epoch + 1 everywhere and
+// reduce_partials sums the G slots in ascending rank order (fp32, so the
+// aggregate is bit-reproducible) into hidden_out and advances the epoch.
+// Waits are bounded: a peer that never arrives sets error bit 4 (reported by
+// moeshard_check) instead of hanging the GPU.
+#include "common.cuh"
+#include "p2p.cuh"
+#include "ptx.cuh"
+
+#include <algorithm>
+
+namespace moeshard {
+namespace {
+
+__device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(int32_t* p, int v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// all G flags >= target, bounded (~2^24 polls of >= 256 ns); on timeout raise error bit 4
+__device__ __forceinline__ void wait_flags(const int32_t* flags, int world, int target,
+                                           int32_t* err) {
+  for (int g = 0; g < world; ++g) {
+    const int32_t* f = flags + 32 * g;
+    uint32_t it = 0;
+    while (ld_acquire_sys(f) < target) {
+      if (++it > (1u << 24)) {
+        atomicOr(err, 4);
+        return;
+      }
+      __nanosleep(256);
+    }
+  }
+}
+
+// Step 3 push: this rank's n rows / records / block histograms into slot `rank`
+// of every peer region. 16-B vectors, grid-stride.
+__global__ void __launch_bounds__(256) push_tokens(P2PArgs a, const uint4* __restrict__ x, int n,
+                                                   int row_vecs, int nbr, int E) {
+  ptx::griddep_wait();   // x / route / hist come from the router
+  const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
+  const size_t nx = static_cast<size_t>(n) * row_vecs;
+  const size_t nrec = static_cast<size_t>(n);              // RouteRec = 8 B -> half vectors
+  const size_t nh = static_cast<size_t>(nbr) * E;          // int32
+  const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const RouteRec* my_route = reinterpret_cast<const RouteRec*>(a.self + a.off_route) + a.rank * nrec;
+  const int32_t* my_hist = reinterpret_cast<const int32_t*>(a.self + a.off_hist) + a.rank * nh;
+  for (int g = 0; g < a.world; ++g) {
+    char* peer = a.peers[g];
+    uint4* dx = reinterpret_cast<uint4*>(peer + a.off_x) + a.rank * nx;
+    for (size_t i = tid; i < nx; i += stride) dx[i] = __ldg(x + i);
+    if (g != a.rank) {   // the router already wrote its own slot of route / hist
+      RouteRec* dr = reinterpret_cast<RouteRec*>(peer + a.off_route) + a.rank * nrec;
+      for (size_t i = tid; i < nrec; i += stride) dr[i] = my_route[i];
+      int32_t* dh = reinterpret_cast<int32_t*>(peer + a.off_hist) + a.rank * nh;
+      for (size_t i = tid; i < nh; i += stride) dh[i] = my_hist[i];
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t* ctr = reinterpret_cast<int32_t*>(a.self) + 1;
+    if (atomicAdd(ctr, 1) == static_cast<int>(gridDim.x) - 1) {   // every CTA's stores fenced
+      *ctr = 0;
+      __threadfence_system();
+      for (int g = 0; g < a.world; ++g)
+        st_release_sys(reinterpret_cast<int32_t*>(a.peers[g]) + 32 * (1 + a.rank), epoch + 1);
+    }
+  }
+}
+
+// Step 5 signal: after the FFN's remote partial-row stores (stream order)
+__global__ void rs_signal(P2PArgs a) {
+  const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
+  __threadfence_system();
+  const int g = threadIdx.x;
+  if (g < a.world)
+    st_release_sys(reinterpret_cast<int32_t*>(a.peers[g]) + 32 * (1 + a.world + a.rank), epoch + 1);
+}
+
+// Step 5 aggregate: out[i] = sum_g recv[g][i] (fp32, ascending g), then epoch += 1
+__global__ void __launch_bounds__(256) reduce_partials(P2PArgs a, int n, int row_vecs,
+                                                       uint4* __restrict__ out, int32_t* err) {
+  const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    wait_flags(reinterpret_cast<const int32_t*>(a.self) + 32 * (1 + a.world), a.world, epoch + 1,
+               err);
+    s_ok = 1;
+  }
+  __syncthreads();
+  const size_t nv = static_cast<size_t>(n) * row_vecs;
+  const size_t slot = static_cast<size_t>(a.n_max) * row_vecs;
+  const uint4* recv = reinterpret_cast<const uint4*>(a.self + a.off_recv);
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int g = 0; g < a.world; ++g) {
+      const uint4 v = __ldcg(recv + g * slot + i);   // written by peers: bypass L1
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(b[k]);
+        acc[2 * k] += f.x;
+        acc[2 * k + 1] += f.y;
+      }
+    }
+    uint4 o;
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ob[k] = __floats2bfloat162_rn(acc[2 * k], acc[2 * k + 1]);
+    out[i] = o;
+  }
+  // the last CTA out advances the epoch (every CTA has read it by now)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t* ctr = reinterpret_cast<int32_t*>(a.self) + 2;
+    __threadfence();
+    if (atomicAdd(ctr, 1) == static_cast<int>(gridDim.x) - 1) {
+      *ctr = 0;
+      *reinterpret_cast<volatile int32_t*>(a.self) = epoch + 1;
+      __threadfence();
+    }
+  }
+  (void)s_ok;
+}
+
+// grouping-side wait for Step 3 (one CTA; launched just before the grouping kernels)
+__global__ void wait_tokens(P2PArgs a, int32_t* err) {
+  const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
+  if (threadIdx.x == 0)
+    wait_flags(reinterpret_cast<const int32_t*>(a.self) + 32, a.world, epoch + 1, err);
+}
+
+}  // namespace
+
+P2PLayout p2p_layout(int world, int n_max, int h, int E, int nbr_max) {
+  auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+  P2PLayout L{};
+  size_t off = al(static_cast<size_t>(32) * 4 * (1 + 2 * world));
+  L.off_x = off;
+  off += al(static_cast<size_t>(world) * n_max * h * 2);
+  L.off_route = off;
+  off += al(static_cast<size_t>(world) * n_max * sizeof(RouteRec));
+  L.off_hist = off;
+  off += al(static_cast<size_t>(world) * nbr_max * E * 4);
+  L.off_recv = off;
+  off += al(static_cast<size_t>(world) * n_max * h * 2);
+  L.total = off;
+  return L;
+}
+
+cudaError_t launch_p2p_push(const P2PArgs& a, const void* x, int n, int row_vecs, int nbr, int E,
+                            int num_sms, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const size_t work = static_cast<size_t>(n) * row_vecs;
+  const int grid = static_cast<int>(std::min<size_t>(2 * num_sms, (work + 255) / 256));
+  return launch_pdl(push_tokens, dim3(std::max(grid, 1)), dim3(256), 0, s, a,
+                    static_cast<const uint4*>(x), n, row_vecs, nbr, E);
+}
+
+cudaError_t launch_p2p_wait_tokens(const P2PArgs& a, int32_t* err, cudaStream_t s) {
+  wait_tokens<<<1, 32, 0, s>>>(a, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_signal_partials(const P2PArgs& a, cudaStream_t s) {
+  rs_signal<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_reduce(const P2PArgs& a, int n, int row_vecs, void* out, int32_t* err,
+                              int num_sms, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const size_t work = static_cast<size_t>(n) * row_vecs;
+  const int grid = static_cast<int>(std::min<size_t>(2 * num_sms, (work + 255) / 256));
+  reduce_partials<<<std::max(grid, 1), 256, 0, s>>>(a, n, row_vecs, static_cast<uint4*>(out), err);
+  return cudaGetLastError();
+}
+
+}  // namespace moeshard

@@ -66,12 +66,19 @@ class MoEShardLayer:
         self._wbytes = C.moeshard_weight_storage_size(self.cfg, world)
         self._storage: List[Optional[torch.Tensor]] = [None] * n_layers
         uid = None
-        if world > 1 or (flags & C.MOESHARD_FLAG_FORCE_COLLECTIVES):
+        p2p = bool(flags & C.MOESHARD_FLAG_P2P)
+        if not p2p and (world > 1 or (flags & C.MOESHARD_FLAG_FORCE_COLLECTIVES)):
             uid = C.moeshard_get_unique_id() if rank == 0 else None
             if world > 1:
                 uid = broadcast_uid(uid, rank, group)
         self.ctx = C.moeshard_init(self.cfg, rank, world, uid, self.workspace.data_ptr(), ws,
                                    self.device)
+        if p2p and world > 1:
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized():
+                self.p2p_connect_group(group)     # one process per rank
+        elif p2p:
+            self.p2p_connect([self.p2p_region()])
 
     @staticmethod
     def _stream() -> int:
@@ -92,9 +99,36 @@ class MoEShardLayer:
         torch.cuda.current_stream().synchronize()  # inputs may be freed by the caller afterwards
         self._storage[layer] = st
 
+    # ---------------------------------------------------------- peer-memory exchange
+    def p2p_region(self) -> int:
+        """Device pointer of this rank's exchange region (MOESHARD_FLAG_P2P)."""
+        return C.moeshard_p2p_region(self.ctx)[0]
+
+    def p2p_connect(self, regions):
+        """regions[g] = rank g's exchange region as mapped in this process."""
+        C.moeshard_p2p_connect(self.ctx, list(regions))
+
+    def p2p_connect_group(self, group=None):
+        """One process per rank: exchange CUDA IPC handles over torch.distributed
+        (host bytes only), map every peer's region, connect."""
+        import torch.distributed as dist
+        mine = C.moeshard_p2p_export(self.ctx)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, mine, group=group)
+        regions = [self.p2p_region() if g == self.rank else C.moeshard_p2p_open(self.ctx, handles[g])
+                   for g in range(self.world)]
+        self.p2p_connect(regions)
+
+    @staticmethod
+    def p2p_connect_local(layers):
+        """Ranks that share one process (and GPU): connect their regions directly."""
+        regions = [l.p2p_region() for l in layers]
+        for l in layers:
+            l.p2p_connect(regions)
+
     def forward(self, layer: int, hidden: torch.Tensor, router_w: torch.Tensor,
                 forced_expert: Optional[torch.Tensor] = None,
-                out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                out: Optional[torch.Tensor] = None, stages: int = C.MOESHARD_STAGE_ALL) -> torch.Tensor:
         n = hidden.shape[0]
         if hidden.dtype != self.dtype or router_w.dtype != self.dtype:
             raise C.MoEShardError(-1, f"hidden/router_w must be {self.dtype}")
@@ -108,8 +142,12 @@ class MoEShardLayer:
         if forced_expert is not None:
             if forced_expert.dtype != torch.int32 or forced_expert.shape != (n,):
                 raise C.MoEShardError(-2, f"forced_expert must be int32 [{n}]")
-        C.moeshard_forward(self.ctx, layer, hidden.data_ptr(), n, router_w.data_ptr(),
-                           out.data_ptr(), _ptr(forced_expert), self._stream())
+        if stages == C.MOESHARD_STAGE_ALL:
+            C.moeshard_forward(self.ctx, layer, hidden.data_ptr(), n, router_w.data_ptr(),
+                               out.data_ptr(), _ptr(forced_expert), self._stream())
+        else:
+            C.moeshard_forward_stages(self.ctx, layer, hidden.data_ptr(), n, router_w.data_ptr(),
+                                      out.data_ptr(), _ptr(forced_expert), stages, self._stream())
         return out
 
     __call__ = forward
@@ -130,7 +168,8 @@ class MoEShardLayer:
         return r
 
     def _collective(self) -> bool:
-        return self.world > 1 or bool(self.cfg.flags & C.MOESHARD_FLAG_FORCE_COLLECTIVES)
+        return self.world > 1 or bool(self.cfg.flags & (C.MOESHARD_FLAG_FORCE_COLLECTIVES |
+                                                         C.MOESHARD_FLAG_P2P))
 
     def stats(self) -> dict:
         return C.moeshard_get_stats(self.ctx, self._stream())

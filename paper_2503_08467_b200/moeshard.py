@@ -29,6 +29,12 @@ MOESHARD_FLAG_FUSED_ROUTE_GROUP = 0x20
 MOESHARD_FLAG_CPASYNC_GATHER = 0x40
 MOESHARD_FLAG_NO_L2_PERSIST = 0x80
 MOESHARD_FLAG_ROW_COPY_IN_FFN = 0x100
+MOESHARD_FLAG_P2P = 0x200
+MOESHARD_STAGE_ROUTE = 0x1
+MOESHARD_STAGE_COMPUTE = 0x2
+MOESHARD_STAGE_REDUCE = 0x4
+MOESHARD_STAGE_ALL = 0x7
+MOESHARD_P2P_HANDLE_BYTES = 64
 
 STATUS = {
     0: "MOESHARD_OK", -1: "MOESHARD_ERR_INVALID_ARG", -2: "MOESHARD_ERR_SHAPE",
@@ -43,6 +49,8 @@ EXPORTS = [
     "moeshard_init", "moeshard_load_expert_shards", "moeshard_forward", "moeshard_get_routing",
     "moeshard_get_stats", "moeshard_check", "moeshard_last_error", "moeshard_status_string",
     "moeshard_destroy", "moeshard_version", "moeshard_profile", "moeshard_get_phase_ms",
+    "moeshard_forward_stages", "moeshard_p2p_region", "moeshard_p2p_export", "moeshard_p2p_open",
+    "moeshard_p2p_connect",
 ]
 PHASES = ["router", "allgather", "grouping", "gemm_up", "gemm_down", "reduce_scatter"]
 
@@ -105,6 +113,11 @@ def load_library() -> ctypes.CDLL:
         "moeshard_profile": ([vp, i32], i32),
         "moeshard_get_phase_ms": ([vp, ctypes.POINTER(ctypes.c_float), i32,
                                    ctypes.POINTER(ctypes.c_int)], i32),
+        "moeshard_forward_stages": ([vp, i32, vp, i32, vp, vp, vp, i32, vp], i32),
+        "moeshard_p2p_region": ([vp, ctypes.POINTER(vp), ctypes.POINTER(sz)], i32),
+        "moeshard_p2p_export": ([vp, ctypes.c_char_p], i32),
+        "moeshard_p2p_open": ([vp, ctypes.c_char_p, ctypes.POINTER(vp)], i32),
+        "moeshard_p2p_connect": ([vp, ctypes.POINTER(vp)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -160,6 +173,36 @@ def moeshard_load_expert_shards(ctx, layer, w_in_ptr, w_out_ptr, storage_ptr, nb
 def moeshard_forward(ctx, layer, hidden_ptr, n_local, router_ptr, out_ptr, forced_ptr, stream):
     _check(_lib.moeshard_forward(ctx, layer, hidden_ptr, n_local, router_ptr, out_ptr, forced_ptr,
                                  stream), ctx)
+
+
+def moeshard_forward_stages(ctx, layer, hidden_ptr, n_local, router_ptr, out_ptr, forced_ptr,
+                            stages, stream):
+    _check(_lib.moeshard_forward_stages(ctx, layer, hidden_ptr, n_local, router_ptr, out_ptr,
+                                        forced_ptr, stages, stream), ctx)
+
+
+def moeshard_p2p_region(ctx):
+    """(device pointer, bytes) of this context's exchange region."""
+    p, n = ctypes.c_void_p(), ctypes.c_size_t()
+    _check(_lib.moeshard_p2p_region(ctx, ctypes.byref(p), ctypes.byref(n)), ctx)
+    return p.value, n.value
+
+
+def moeshard_p2p_export(ctx) -> bytes:
+    buf = ctypes.create_string_buffer(MOESHARD_P2P_HANDLE_BYTES)
+    _check(_lib.moeshard_p2p_export(ctx, buf), ctx)
+    return buf.raw
+
+
+def moeshard_p2p_open(ctx, handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    _check(_lib.moeshard_p2p_open(ctx, handle, ctypes.byref(p)), ctx)
+    return p.value
+
+
+def moeshard_p2p_connect(ctx, regions):
+    arr = (ctypes.c_void_p * len(regions))(*regions)
+    _check(_lib.moeshard_p2p_connect(ctx, arr), ctx)
 
 
 def moeshard_get_routing(ctx, expert_ptr, gate_ptr, counts_ptr, offsets_ptr, perm_ptr, stream):

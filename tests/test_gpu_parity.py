@@ -463,3 +463,77 @@ def test_token_paths_bitwise_equal_and_match_oracle(flag, N, h, d_ff, E, routing
         np.testing.assert_array_equal(routes[0][k], routes[1][k])
     if N <= 3000:
         _check_layer(inp, ys[0], routes[0], tol=BF16_TOL)
+
+
+# --------------------------------------------------------------------- peer-memory exchange
+@pytest.mark.parametrize("G,routing", [(1, "zipf"), (2, "zipf"), (4, "uniform"), (8, "patho")])
+def test_p2p_exchange_virtual_ranks_match_oracle(G, routing):
+    """MOESHARD_FLAG_P2P: G ranks share this GPU, each with its own context, weight
+    shard and exchange region; the regions are connected directly and the ranks are
+    driven in lock-step stages (ROUTE on every rank, then COMPUTE, then REDUCE), so
+    every flag wait inside a stage is already satisfied. Tokens are pushed into every
+    rank's x_all, partial rows are stored by the down-projection epilogues straight
+    into their owner's receive slots, and the owners sum them: the concatenated
+    outputs must match the unsharded oracle and the routing tables must be exact on
+    every rank, over several forwards (the epoch advances) with changing inputs."""
+    from paper_2503_08467_b200 import MoEShardLayer, shard_columns
+    from paper_2503_08467_b200 import moeshard as C
+    N, h, d_ff, E = 1024 * G if G > 1 else 1500, 256, 256 * G, 16
+    n = N // G
+    layers = [MoEShardLayer(h, d_ff, E, max_tokens_per_rank=n, dtype=torch.bfloat16, rank=r,
+                            world=G, flags=C.MOESHARD_FLAG_P2P) for r in range(G)]
+    if G > 1:
+        MoEShardLayer.p2p_connect_local(layers)
+    base = W.make_layer_inputs(31, N, h, d_ff, E, dtype=torch.bfloat16, routing=routing, k=3)
+    for r, L in enumerate(layers):
+        c0, c1 = shard_columns(d_ff, G, r)
+        L.load_expert_shards(0, base.w_i[:, :, c0:c1].cuda(), base.w_o[:, c0:c1, :].cuda())
+    for step, seed in enumerate((31, 32, 31)):
+        # new tokens and routing per step, the same weights
+        inp = W.LayerInputs(W.make_tokens(seed, N, h), base.w_r, base.w_i, base.w_o,
+                            W.draw_experts(seed, N, E, routing, k=3))
+        xs = [inp.x[r * n:(r + 1) * n].cuda().contiguous() for r in range(G)]
+        fs = [inp.forced[r * n:(r + 1) * n].cuda().contiguous() for r in range(G)]
+        ys = [torch.empty_like(x) for x in xs]
+        w_r = inp.w_r.cuda()
+        for stage in (C.MOESHARD_STAGE_ROUTE, C.MOESHARD_STAGE_COMPUTE, C.MOESHARD_STAGE_REDUCE):
+            for r, L in enumerate(layers):
+                L.forward(0, xs[r], w_r, forced_expert=fs[r], out=ys[r], stages=stage)
+        for L in layers:
+            L.check()
+        torch.cuda.synchronize()
+        y = torch.cat(ys).float().cpu().numpy()
+        y_ref, rt, counts, offsets, perm = O.moe_layer(inp.x, inp.w_r, inp.w_i, inp.w_o,
+                                                       forced=inp.forced.cpu().numpy(),
+                                                       return_routing=True)
+        for L in layers:
+            r = {k: v.cpu().numpy() for k, v in L.routing(n).items()}
+            np.testing.assert_array_equal(r["expert"], rt.expert)
+            np.testing.assert_array_equal(r["counts"], counts)
+            np.testing.assert_array_equal(r["perm"], perm)
+        err = O.max_abs_rel(y, y_ref)
+        assert err <= BF16_TOL, f"G={G} step {step}: max-abs-rel {err:.3e}"
+    for L in layers:
+        L.close()
+
+
+def test_p2p_missing_peer_times_out_instead_of_hanging():
+    """A rank whose peer never runs its ROUTE stage must not hang the GPU: the bounded
+    wait gives up and moeshard_check reports a protocol error."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200 import moeshard as C
+    G, n, h, d_ff, E = 2, 256, 128, 256, 8
+    layers = [MoEShardLayer(h, d_ff, E, max_tokens_per_rank=n, dtype=torch.bfloat16, rank=r,
+                            world=G, flags=C.MOESHARD_FLAG_P2P) for r in range(G)]
+    MoEShardLayer.p2p_connect_local(layers)
+    inp = W.make_layer_inputs(33, G * n, h, d_ff, E, dtype=torch.bfloat16, routing="uniform")
+    for r, L in enumerate(layers):
+        L.load_expert_shards(0, inp.w_i[:, :, r * 128:(r + 1) * 128].cuda(),
+                             inp.w_o[:, r * 128:(r + 1) * 128, :].cuda())
+    x = inp.x[:n].cuda().contiguous()
+    layers[0].forward(0, x, inp.w_r.cuda(), forced_expert=inp.forced[:n].cuda().contiguous(),
+                      stages=C.MOESHARD_STAGE_ROUTE | C.MOESHARD_STAGE_COMPUTE)
+    with pytest.raises(C.MoEShardError, match="PROTOCOL"):
+        layers[0].check()
+    for L in layers:
+        L.close()
