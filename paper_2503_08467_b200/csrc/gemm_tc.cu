@@ -28,6 +28,7 @@
 #include "gemm_tc.cuh"
 #include "ptx.cuh"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -48,6 +49,7 @@ constexpr int kThreads = 256;
 
 struct Unit {
   int e, mt, tok0, ntok;
+  int chunk;   // global token-chunk id (pref[e] + chunk of e)
 };
 
 // pref: cumulative chunks [E+1]; pos: internal segment starts; end: pos + count; csz: chunk size
@@ -66,6 +68,7 @@ __device__ __forceinline__ Unit decode(int u, int n_mt, int E, const int32_t* pr
   const int local = u - pref[lo] * n_mt;
   w.mt = local / nch;
   const int c = local - w.mt * nch;
+  w.chunk = pref[lo] + c;
   const int cs = csz[lo];
   w.tok0 = pos[lo] + c * cs;
   w.ntok = min(cs, end[lo] - w.tok0);
@@ -616,7 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // [all up pair-units (expert-major), all down pair-units (expert-major)];
 // cluster c takes units c, c + #clusters, ... A down unit of expert e reads
 // H rows written by the up units of e (every feature tile), so its token
-// producer waits until done[e] == 2 * chunks(e) * n_mp_up (each CTA of each up
+// producer waits until done[chunk] == 2 * n_mp_up (each CTA of each up
 // pair-unit releases one count after its H tile is stored) - acquire, then an
 // async-proxy fence before the TMA reads H. Units earlier in the list never
 // wait on later ones, so with all clusters resident there is no deadlock.
@@ -829,10 +832,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
-      if (down) {   // H rows of expert e complete? (acquire), then order the TMA after it
-        const int target = 2 * (s_pref[w.e + 1] - s_pref[w.e]) * n_mp_up;
+      if (down) {   // H rows of this token chunk complete? (acquire), then order the TMA after it
+        const int target = 2 * n_mp_up;   // both CTAs of every up pair-unit of (e, chunk)
         if (elect_one()) {
-          while (ld_acquire_gpu(fp.done + w.e) < target) __nanosleep(128);
+          uint32_t it = 0;
+          while (ld_acquire_gpu(fp.done + w.chunk) < target) {
+            if (++it > (1u << 24)) {   // a cluster never became resident: report, do not hang
+              atomicOr(fp.up.tb.stats + 3, 8);
+              break;
+            }
+            __nanosleep(128);
+          }
           fence_proxy_async_global();
         }
         __syncwarp();
@@ -998,7 +1008,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (!down) {   // publish this CTA's H tile of expert e
         __threadfence();
         asm volatile("bar.sync 2, 128;" ::: "memory");   // the 4 epilogue warps
-        if (wq == 0 && lane == 0) red_release_gpu_add(fp.done + w.e, 1);
+        if (wq == 0 && lane == 0) red_release_gpu_add(fp.done + w.chunk, 1);
       }
       as ^= 1;
       if (as == 0) aphase ^= 1;

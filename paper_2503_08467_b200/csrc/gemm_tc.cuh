@@ -65,14 +65,14 @@ struct RouteGroupArgs {
 // tmX: x [n][h] box {64, 128}. mn_major: tmW = router_w [h][E] box {64 experts, 64 k}
 // (E % 8 == 0); else router_w is first transposed to wt_r [EP][h] (zero rows E..EP-1)
 // and tmW = wt_r box {64, EP}.
-size_t router_tc_smem_bytes(int EP, bool mn_major);
+size_t router_tc_smem_bytes(int EP, bool mn_major, int tok);
 // pf / pf_bytes / pf_ctas: extra CTAs that prefetch the first pf_bytes of the
 // layer's packed up-projection tiles into L2 (0 CTAs disables).
 cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
                              const void* w_r, void* wt_r, int n, int h, int E, int EP,
                              const int32_t* forced, RouteRec* out, int32_t* hist_out,
                              int32_t* err_flag, const void* pf, long long pf_bytes, int pf_ctas,
-                             cudaStream_t s);
+                             int tok, cudaStream_t s);
 
 // Router + the whole of Step 2 in one launch (world = 1, ceil(n/128) <= SMs,
 // router_w MN-major (E % 8 == 0), h <= 1024): routes 128 tokens per CTA like

@@ -77,8 +77,8 @@ __device__ __forceinline__ void segment_tables(int E, const int* s_tot, const in
     const int tcp = block_excl_scan<kThreads>(nc, s_warp, tot_tc);
     const int smp = block_excl_scan<kThreads>(sc, s_warp, tot_sc);
     block_excl_scan<kThreads>(rows, s_warp, tot_rows);
+    for (int i = threadIdx.x; i < tot_tc; i += kThreads) tb.done[i] = 0;   // per token chunk
     if (e < E) {
-      tb.done[e] = 0;
       tb.copied[e] = 0;
       tb.pos[e] = pos;
       tb.counts[e] = cnt;

@@ -121,7 +121,8 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 // Workspace carve-up, shared by moeshard_workspace_size and moeshard_init.
 struct Layout {
-  size_t wt_r, route, block_hist, block_base, ints, perm, perm_pad, x_all, x_perm, H, partial, total;
+  size_t wt_r, route, block_hist, block_base, ints, done, perm, perm_pad, x_all, x_perm, H, partial,
+      total;
   int n_ints;
   size_t npad;   // rows of the internal expert-ordered layout: N_max + 32 per expert, rounded to 64
 };
@@ -145,9 +146,10 @@ Layout make_layout(const moeshard_config& c, int world) {
   L.route = take(Nmax * sizeof(RouteRec));
   L.block_hist = take(nb * E * 4);
   L.block_base = take(nb * E * 4);
-  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + E + (E + 1) + E);
+  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + E + (E + 1) + E + 4);
   L.npad = (Nmax + kSegAlign * E + 63) / 64 * 64;
   L.ints = take(L.n_ints * 4);
+  L.done = take((Nmax / kTcTokTile + E + 8) * 4);   // per token chunk: <= N/256 + E chunks
   L.perm = take(Nmax * 4);
   L.perm_pad = take(L.npad * 4);
   L.x_all = coll ? take(Nmax * h * elt) : 0;
@@ -176,6 +178,7 @@ struct moeshard_ctx {
   char* ws = nullptr;
   RouteRec* route = nullptr;
   int32_t *block_hist = nullptr, *block_base = nullptr, *block_tot = nullptr, *perm = nullptr;
+  int32_t* gsync = nullptr;
   Tables tb{};
   void *x_all = nullptr, *x_perm = nullptr, *H = nullptr, *partial = nullptr;
   CUtensorMap tm_xperm{}, tm_H{}, tm_xperm16{}, tm_H16{}, tm_Ht{}, tm_wt_r{};
@@ -194,6 +197,7 @@ struct moeshard_ctx {
   int64_t launches = 0;  // cumulative kernel launches of this context
   long long pf_bytes = 0;  // experimental L2 weight prefetch during routing (MOESHARD_L2_PREFETCH_MB)
   int gather_depth = 4;    // cp.async gather: stages in flight (MOESHARD_GATHER_DEPTH, 1..5)
+  int router_tok = 128;    // tokens per tcgen05 router CTA (MOESHARD_ROUTER_TOK: 64 or 128)
   // phase profiling (measurement only)
   bool prof = false;
   static constexpr int kRing = 1024, kEv = 7;
@@ -357,6 +361,8 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->coll = world > 1 || (c->cfg.flags & MOESHARD_FLAG_FORCE_COLLECTIVES) || c->p2p;
   c->use_tc = cfg->dtype == MOESHARD_BF16 && !(c->cfg.flags & MOESHARD_FLAG_SIMT_GEMM);
   if (const char* pf = getenv("MOESHARD_L2_PREFETCH_MB")) c->pf_bytes = atoll(pf) << 20;
+  if (c->cfg.flags & MOESHARD_FLAG_ROUTER_TOK64) c->router_tok = 64;
+  if (const char* rt = getenv("MOESHARD_ROUTER_TOK")) c->router_tok = atoi(rt) == 64 ? 64 : 128;
   if (const char* gd = getenv("MOESHARD_GATHER_DEPTH")) c->gather_depth = std::max(1, std::min(5, atoi(gd)));
   // L2 set-aside for the kernels' evict_last lines (H between the two products, the
   // expert-ordered token rows re-read by every feature tile): without it the
@@ -384,10 +390,11 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->tb.tc_chunk_size = c->tb.tc_chunk_pref + (E + 1);
   c->tb.simt_chunk_pref = c->tb.tc_chunk_size + E;
   c->tb.stats = c->tb.simt_chunk_pref + (E + 1);
-  c->tb.done = c->tb.stats + 8;
-  c->block_tot = c->tb.done + E;
+  c->tb.done = reinterpret_cast<int32_t*>(c->ws + L.done);
+  c->block_tot = c->tb.stats + 8 + E;
   c->tb.pos = c->block_tot + E;
   c->tb.copied = c->tb.pos + (E + 1);
+  c->gsync = c->tb.copied + E;   // 4 ints: the grouping launch's ticket / scan / exit counters
   c->tb.perm_pad = reinterpret_cast<int32_t*>(c->ws + L.perm_pad);
   c->perm = reinterpret_cast<int32_t*>(c->ws + L.perm);
   c->x_all = c->coll && !c->p2p ? c->ws + L.x_all : nullptr;
@@ -396,6 +403,7 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->partial = c->coll && !c->p2p ? c->ws + L.partial : nullptr;
   c->layers.resize(cfg->n_layers);
   cudaError_t e = cudaMemset(ints, 0, L.n_ints * 4);
+  if (e == cudaSuccess) e = cudaMemset(c->tb.done, 0, L.perm - L.done);
   if (e != cudaSuccess) {
     delete c;
     return fail(nullptr, MOESHARD_ERR_CUDA, "cudaMemset: %s", cudaGetErrorString(e));
@@ -536,7 +544,9 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   c->mark(0, s);
   // Step 1: route local tokens
   RouteRec* my_route = c->route + (c->coll ? static_cast<size_t>(c->rank) * n : 0);
-  const int HB = c->use_tc ? 128 : 64;                 // tokens per hist-block
+  // tokens per hist-block = tokens per router CTA (64 for the SIMT router; the
+  // tcgen05 router runs 64 or 128 token rows per CTA, c->router_tok)
+  const int HB = c->use_tc ? c->router_tok : 64;
   const int nbr = (n + HB - 1) / HB;                    // hist-blocks per rank
   const int NB = (c->coll ? c->world : 1) * nbr;
   const int N = (c->coll ? c->world : 1) * n;             // tokens of all ranks
@@ -551,7 +561,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   const bool copy_in_ffn = fused && !gather && (c->cfg.flags & MOESHARD_FLAG_ROW_COPY_IN_FFN);
   // world = 1: the router launch also runs Step 2 (grid barriers need every CTA resident)
   const bool route_group = c->use_tc && !c->coll && (E % 8) == 0 && nbr <= c->num_sms &&
-                           h <= 1024 && c->pf_bytes == 0 &&
+                           h <= 1024 && c->pf_bytes == 0 && HB == 128 &&
                            (c->cfg.flags & MOESHARD_FLAG_FUSED_ROUTE_GROUP);
   if (!st_route) {
     // (routing and the token exchange ran in an earlier call)
@@ -570,17 +580,17 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   } else if (c->use_tc) {
     CUtensorMap tm_x, tm_w;
     const bool mn = (E % 8) == 0;
-    if (!make_tmap(&tm_x, hidden, h, n, 128) ||
+    if (!make_tmap(&tm_x, hidden, h, n, HB) ||
         (mn && !make_tmap(&tm_w, router_w, E, h, 64)))
       return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden/router_w");
     // L2 prefetch of the first up-projection tiles on the SMs the router leaves idle
-    const int tiles = (n + 127) / 128;
+    const int tiles = (n + HB - 1) / HB;
     const int pf_ctas = c->pf_bytes > 0 ? std::max(0, std::min(c->num_sms - tiles, 96)) : 0;
     const long long pf_bytes =
         std::min<long long>(c->pf_bytes, static_cast<long long>(E) * F * h * c->elt);
     CUDA_TRY(c, launch_router_tc(tm_x, mn ? tm_w : c->tm_wt_r, mn, router_w, c->wt_r, n, h, E,
                                  c->EP, forced, my_route, my_hist, err_flag, lw.wt_in, pf_bytes,
-                                 pf_ctas, s));
+                                 pf_ctas, HB, s));
     c->launches += mn ? 1 : 2;
   } else {
     launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, my_hist, err_flag, s);
@@ -614,10 +624,14 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs (the row
     // copy is skipped when the FFN gathers rows itself)
     if (!route_group) {
+      // opt-in: one launch (block scans inside, ticket-ordered); measured ~2 us slower than
+      // the scan launch + PDL (the ticket atomic and the spin sit on the critical path)
+      const bool one = (c->cfg.flags & MOESHARD_FLAG_FUSED_SCAN) != 0;
       launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb,
                           F / kTcFeatTile, h / kTcFeatTile, c->route, x_all, n, nbr, HB,
-                          h * c->elt, c->perm, gather || copy_in_ffn ? nullptr : c->x_perm, s);
-      c->launches += 2;
+                          h * c->elt, c->perm, gather || copy_in_ffn ? nullptr : c->x_perm,
+                          one ? c->gsync : nullptr, s);
+      c->launches += one ? 1 : 2;
     }
     c->mark(3, s);
     // Step 4: expert computation, one grouped product per projection
@@ -808,6 +822,10 @@ int moeshard_check(moeshard_ctx* c, void* stream) {
   }
   if (flag) {
     cudaMemset(c->tb.stats + 3, 0, 4);
+    if (flag & 8)
+      return fail(c, MOESHARD_ERR_CUDA,
+                  "FFN: a down-projection unit waited too long for its H tiles (the kernel's "
+                  "clusters were not all resident - another kernel held SMs?)");
     if (flag & 4)
       return fail(c, MOESHARD_ERR_PROTOCOL,
                   "MOESHARD_FLAG_P2P: a peer's tokens or partial outputs never arrived (wait timed "

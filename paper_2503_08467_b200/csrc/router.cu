@@ -206,7 +206,7 @@ void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int 
 namespace moeshard {
 namespace {
 
-constexpr int RTC_MAX_STAGES = 8;
+constexpr int RTC_MAX_STAGES = 16;   // 64-token CTAs: all 12 k-blocks of h = 768 in flight
 
 // 2^x on the SFU (ex2.approx.ftz: ~2 ulp; exp2(-inf) = +0)
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -215,7 +215,6 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 constexpr int RTC_SMEM_BUDGET = 200 * 1024;
-constexpr int RTC_A_BYTES = 128 * 128;  // 128 tokens x 64 k x 2 B
 
 __global__ void router_transpose(const __nv_bfloat16* __restrict__ w_r, int h, int E, int EP,
                                  __nv_bfloat16* __restrict__ wt) {
@@ -350,11 +349,13 @@ __global__ void __launch_bounds__(256, 1)
                      int n, int h, int E, int EP, const int32_t* __restrict__ forced,
                      RouteRec* __restrict__ out, int32_t* __restrict__ hist_out,
                      int32_t* __restrict__ err_flag, const uint8_t* __restrict__ pf,
-                     long long pf_bytes, RouteGroupArgs ga) {
+                     long long pf_bytes, RouteGroupArgs ga, int tok) {
+  // tok = tokens per CTA (hist-block): 128, or 64 - then only rows 0-63 of the
+  // M=128 A tile are loaded and TMEM lanes 64-127 (stale rows) are never read
   // CTAs beyond the token tiles run on otherwise idle SMs and pull the first
   // weight tiles the FFN kernel will stream into L2 while routing and grouping
   // are latency-bound (the weights do not depend on the routing result).
-  const int n_tiles = (n + 127) / 128;
+  const int n_tiles = (n + tok - 1) / tok;
   if (static_cast<int>(blockIdx.x) >= n_tiles) {
     const int n_pf = gridDim.x - n_tiles, q = blockIdx.x - n_tiles;
     const long long per = ((pf_bytes / n_pf) + 16383) & ~16383LL;
@@ -372,9 +373,10 @@ __global__ void __launch_bounds__(256, 1)
   __shared__ int32_t s_hist[kMaxExperts];
   __shared__ int32_t s_tok_e[128];   // kGroup: expert of each of the CTA's tokens (-1: none)
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
-  const int RTC_STAGES = min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (RTC_A_BYTES + b_bytes));
+  const int a_stage = tok * 128;   // tok rows x 64 k x 2 B
+  const int RTC_STAGES = min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (a_stage + b_bytes));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + RTC_STAGES * RTC_A_BYTES;
+  uint8_t* sB = smem + RTC_STAGES * a_stage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + RTC_STAGES * b_bytes);
   uint64_t* empty = full + RTC_STAGES;
   uint64_t* done = empty + RTC_STAGES;
@@ -406,8 +408,9 @@ __global__ void __launch_bounds__(256, 1)
   // else the dependent FFN's CTAs could take the SMs a not-yet-running CTA needs
   if (!kGroup) griddep_launch_dependents();
   const long long t_setup = clock64();
-  const int tok0 = blockIdx.x * 128;
+  const int tok0 = blockIdx.x * tok;
   const int nkb = h / 64;
+  const uint32_t a_bytes = static_cast<uint32_t>(tok) * 128;
 
   if (warp == 4) {
     {  // TMA producer (warp-uniform loop, one elected lane issues)
@@ -417,14 +420,15 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t ph = 0;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
+        const int kk = kb;
         if (elect_one()) {
-          mbar_arrive_expect_tx(&full[s], RTC_A_BYTES + b_bytes);
-          tma_load_2d(&tmX, &full[s], sA + s * RTC_A_BYTES, kb * 64, tok0, pol_x);
+          mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
+          tma_load_2d(&tmX, &full[s], sA + s * a_stage, kk * 64, tok0, pol_x);
           if (kMN) {
             for (int a = 0; a < n_atoms; ++a)
-              tma_load_2d(&tmW, &full[s], sB + s * b_bytes + a * 8192, a * 64, kb * 64, pol_w);
+              tma_load_2d(&tmW, &full[s], sB + s * b_bytes + a * 8192, a * 64, kk * 64, pol_w);
           } else {
-            tma_load_2d(&tmW, &full[s], sB + s * b_bytes, kb * 64, 0, pol_w);  // box = EP rows
+            tma_load_2d(&tmW, &full[s], sB + s * b_bytes, kk * 64, 0, pol_w);  // box = EP rows
           }
         }
         __syncwarp();
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + s * RTC_A_BYTES));
+        const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + s * a_stage));
         const uint64_t bd = kMN ? smem_desc_mn_sw128(smem_u32(sB + s * b_bytes), 8192)
                                 : smem_desc_k_sw128(smem_u32(sB + s * b_bytes));
         const uint32_t bstep = kMN ? 128 : 2;   // K=16 step: 16 rows x 128 B (MN) or 32 B (K)
@@ -455,8 +459,8 @@ __global__ void __launch_bounds__(256, 1)
       if (elect_one()) mma_commit(done);
       __syncwarp();
     }
-  } else if (warp < 4) {
-    // epilogue: warps 0-3, thread = token (TMEM lane 32*warp + lane)
+  } else if (warp < tok / 32) {
+    // epilogue: warps 0-3 (0-1 for 64-token CTAs), thread = token (TMEM lane 32*warp + lane)
     const int t = tok0 + warp * 32 + lane;
     int sel = -1;
     bool bad = false;
@@ -540,9 +544,9 @@ __global__ void __launch_bounds__(256, 1)
     }
     if (kGroup) s_tok_e[threadIdx.x] = t < n ? (sel >= 0 ? sel : best_e) : -1;
     const long long t_store = clock64();
-    asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+    asm volatile("bar.sync 1, %0;" ::"r"(tok) : "memory");  // the epilogue warps
     const long long t_bar = clock64();
-    for (int e = threadIdx.x; e < E; e += 128) hist_out[(size_t)blockIdx.x * E + e] = s_hist[e];
+    for (int e = threadIdx.x; e < E; e += tok) hist_out[(size_t)blockIdx.x * E + e] = s_hist[e];
     if (kT && !kGroup && (threadIdx.x == 0 || threadIdx.x == 127) && (blockIdx.x == 0 || blockIdx.x == 40))
       printf("[router cta %d t%d] setup %lld mainloop %lld softmax %lld store %lld bar %lld hist %lld\n",
              blockIdx.x, threadIdx.x, t_setup - t_start, t_done - t_setup, t_loop - t_done,
@@ -557,17 +561,18 @@ __global__ void __launch_bounds__(256, 1)
 
 }  // namespace
 
-size_t router_tc_smem_bytes(int EP, bool mn) {
+size_t router_tc_smem_bytes(int EP, bool mn, int tok) {
   const int b = mn ? ((EP + 63) / 64) * 8192 : EP * 128;
-  const int st = std::min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (RTC_A_BYTES + b));
-  return 1024 + st * (RTC_A_BYTES + b) + (2 * st + 1) * 8 + 16;
+  const int a = tok * 128;
+  const int st = std::min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (a + b));
+  return 1024 + st * (a + b) + (2 * st + 1) * 8 + 16;
 }
 
 cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
                              const void* w_r, void* wt_r, int n, int h, int E, int EP,
                              const int32_t* forced, RouteRec* out, int32_t* hist_out,
                              int32_t* err_flag, const void* pf, long long pf_bytes, int pf_ctas,
-                             cudaStream_t s) {
+                             int tok, cudaStream_t s) {
   const auto* pfb = static_cast<const uint8_t*>(pf);
   if (pf == nullptr || pf_bytes < 16384) pf_ctas = 0;
   if (n <= 0) return cudaSuccess;
@@ -587,18 +592,18 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
   if (mn_major && timing) {
     cudaFuncSetAttribute(router_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          RTC_SMEM_BUDGET + 2048);
-    router_tc_kernel<true, true><<<ceil_div(n, 128), 192, router_tc_smem_bytes(EP, true), s>>>(
-        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, 0LL, none);
+    router_tc_kernel<true, true><<<ceil_div(n, tok), 192, router_tc_smem_bytes(EP, true, tok), s>>>(
+        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, 0LL, none, tok);
   } else if (mn_major) {
-    return launch_pdl(router_tc_kernel<true>, dim3(ceil_div(n, 128) + pf_ctas), dim3(192),
-                      router_tc_smem_bytes(EP, true), s, tmX, tmW, n, h, E, EP, forced, out,
-                      hist_out, err_flag, pfb, pf_bytes, none);
+    return launch_pdl(router_tc_kernel<true>, dim3(ceil_div(n, tok) + pf_ctas), dim3(192),
+                      router_tc_smem_bytes(EP, true, tok), s, tmX, tmW, n, h, E, EP, forced, out,
+                      hist_out, err_flag, pfb, pf_bytes, none, tok);
   } else {
     dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
     router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,
                                        static_cast<__nv_bfloat16*>(wt_r));
-    router_tc_kernel<false><<<ceil_div(n, 128) + pf_ctas, 192, router_tc_smem_bytes(EP, false), s>>>(
-        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, pf_bytes, none);
+    router_tc_kernel<false><<<ceil_div(n, tok) + pf_ctas, 192, router_tc_smem_bytes(EP, false, tok), s>>>(
+        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, pf_bytes, none, tok);
   }
   return cudaGetLastError();
 }
@@ -607,6 +612,7 @@ cudaError_t launch_route_group_tc(const CUtensorMap& tmX, const CUtensorMap& tmW
                                   int E, int EP, const int32_t* forced, RouteRec* out,
                                   int32_t* hist_out, int32_t* err_flag, const RouteGroupArgs& ga,
                                   cudaStream_t s) {
+  const int tok = 128;
   if (n <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -621,12 +627,12 @@ cudaError_t launch_route_group_tc(const CUtensorMap& tmX, const CUtensorMap& tmW
     cudaFuncSetAttribute(router_tc_kernel<true, true, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, RTC_SMEM_BUDGET + 2048);
     return launch_pdl(router_tc_kernel<true, true, true>, dim3(ceil_div(n, 128)), dim3(256),
-                      router_tc_smem_bytes(EP, true), s, tmX, tmW, n, h, E, EP, forced, out,
-                      hist_out, err_flag, static_cast<const uint8_t*>(nullptr), 0LL, ga);
+                      router_tc_smem_bytes(EP, true, tok), s, tmX, tmW, n, h, E, EP, forced, out,
+                      hist_out, err_flag, static_cast<const uint8_t*>(nullptr), 0LL, ga, 128);
   }
   return launch_pdl(router_tc_kernel<true, false, true>, dim3(ceil_div(n, 128)), dim3(256),
-                    router_tc_smem_bytes(EP, true), s, tmX, tmW, n, h, E, EP, forced, out,
-                    hist_out, err_flag, static_cast<const uint8_t*>(nullptr), 0LL, ga);
+                    router_tc_smem_bytes(EP, true, tok), s, tmX, tmW, n, h, E, EP, forced, out,
+                    hist_out, err_flag, static_cast<const uint8_t*>(nullptr), 0LL, ga, 128);
 }
 
 }  // namespace moeshard

@@ -30,6 +30,8 @@ MOESHARD_FLAG_CPASYNC_GATHER = 0x40
 MOESHARD_FLAG_NO_L2_PERSIST = 0x80
 MOESHARD_FLAG_ROW_COPY_IN_FFN = 0x100
 MOESHARD_FLAG_P2P = 0x200
+MOESHARD_FLAG_FUSED_SCAN = 0x400
+MOESHARD_FLAG_ROUTER_TOK64 = 0x800
 MOESHARD_STAGE_ROUTE = 0x1
 MOESHARD_STAGE_COMPUTE = 0x2
 MOESHARD_STAGE_REDUCE = 0x4

@@ -390,7 +390,8 @@ def test_route_group_fused_matches_separate_and_oracle(N, h, d_ff, E, routing):
     _check_layer(inp, outs[0], routes[0], tol=BF16_TOL)
 
 
-@pytest.mark.parametrize("flag", ["FUSED_ROUTE_GROUP", "CPASYNC_GATHER", "ROW_COPY_IN_FFN", None])
+@pytest.mark.parametrize("flag", ["FUSED_ROUTE_GROUP", "CPASYNC_GATHER", "ROW_COPY_IN_FFN", "FUSED_SCAN",
+                                  None])
 def test_forward_under_cuda_graph_replay(flag):
     """A captured forward replays correctly with new token values and new routing
     (the grid barrier of the fused route+group launch carries no launch arguments)."""
@@ -432,7 +433,8 @@ def test_forward_under_cuda_graph_replay(flag):
 
 
 # --------------------------------------------------------------------- alternative token paths
-@pytest.mark.parametrize("flag", ["ROW_COPY_IN_FFN", "CPASYNC_GATHER", "TMA_GATHER", "FUSED_ROUTE_GROUP"])
+@pytest.mark.parametrize("flag", ["ROUTER_TOK64", "FUSED_SCAN", "ROW_COPY_IN_FFN", "CPASYNC_GATHER",
+                                  "TMA_GATHER", "FUSED_ROUTE_GROUP"])
 @pytest.mark.parametrize("N,h,d_ff,E,routing", [
     (3000, 512, 1024, 64, "zipf"),       # multi-chunk segments, ragged halves
     (777, 384, 640, 16, "patho"),        # odd tile counts (duplicated last pair), empty experts
