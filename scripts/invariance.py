@@ -22,14 +22,15 @@ CASES = {   # name: (E, h, d_ff, N, G, seed, routings)
 }
 
 
-def time_fwd(L, x, w_r, forced, out, iters=50, warm=5):
-    for _ in range(warm):
-        L.forward(0, x, w_r, forced_expert=forced, out=out)
+def time_fwd(L, x, w_r, forced, out, nw, iters=60, warm=6):
+    # rotate over nw weight sets (>= 3x L2 in total) so every forward streams its weights from HBM
+    for k in range(warm):
+        L.forward(k % nw, x, w_r, forced_expert=forced, out=out)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for _ in range(iters):
-        L.forward(0, x, w_r, forced_expert=forced, out=out)
+    for k in range(iters):
+        L.forward(k % nw, x, w_r, forced_expert=forced, out=out)
     e.record()
     torch.cuda.synchronize()
     return s.elapsed_time(e) / iters * 1e3   # us
@@ -45,21 +46,27 @@ def main():
         w_r = W.make_router_weight(seed, h, E, device="cuda")
         out = torch.empty_like(x)
         layers = []
+        nw = max(1, -(-3 * 126 * 2**20 // (2 * E * h * F * 2)))
         for g in range(G):
             c0, c1 = shard_columns(d_ff, G, g)
-            L = MoEShardLayer(h, F, E, max_tokens_per_rank=N, dtype=torch.bfloat16)
-            wi, wo = W.make_expert_weights(seed, E, h, d_ff, cols=(c0, c1), device="cuda")
-            L.load_expert_shards(0, wi, wo)
-            del wi, wo
+            L = MoEShardLayer(h, F, E, n_layers=nw, max_tokens_per_rank=N, dtype=torch.bfloat16)
+            for j in range(nw):
+                wi, wo = W.make_expert_weights(seed, E, h, d_ff, cols=(c0, c1), device="cuda", layer=j)
+                L.load_expert_shards(j, wi, wo)
+                del wi, wo
             layers.append(L)
-        case = {"E": E, "h": h, "d_ff": d_ff, "N": N, "G": G, "d_ff_per_rank": F, "routings": {}}
+        case = {"E": E, "h": h, "d_ff": d_ff, "N": N, "G": G, "d_ff_per_rank": F, "weight_sets": nw,
+                "note": "each virtual rank = the world-1 layer of all N tokens on its d_ff/G shard "
+                        "(what a rank computes after the AllGather); collectives not included; "
+                        "eager launches, weights rotated over weight_sets copies",
+                "routings": {}}
         for r in routings:
             rname, kw = (r, {}) if isinstance(r, str) else r
             forced = W.draw_experts(seed, N, E, rname, device="cuda", **kw)
             label = rname + "".join(f"_{k}{v}" for k, v in kw.items())
             t, tiles = [], []
             for L in layers:
-                t.append(time_fwd(L, x, w_r, forced, out))
+                t.append(time_fwd(L, x, w_r, forced, out, nw))
                 st = L.stats()
                 tiles.append((st["tiles_up"], st["tiles_down"]))
             case["routings"][label] = {
