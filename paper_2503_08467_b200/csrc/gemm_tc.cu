@@ -634,7 +634,30 @@ struct FusedParams {
   const uint4* cp_src = nullptr;
   uint4* cp_dst = nullptr;
   int cp_row_vecs = 0;
+  bool interleave = false;  // expert-group blocks (MOESHARD_FFN_INTERLEAVE=1); default all up, then all down
 };
+
+// Position u of the fused work list -> (down?, index in the up- or down-unit list).
+// Blocks of S experts (see the kernel): s_bstart[j] = first position of block j.
+struct ListPos {
+  bool down;
+  int idx;
+};
+__device__ __forceinline__ ListPos locate(int u, const int* s_bstart, int nblk, int S,
+                                          const int32_t* pref, int n_mp_up, int n_mp_dn) {
+  int lo = 0, hi = nblk;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_bstart[mid] <= u) lo = mid; else hi = mid;
+  }
+  const int K = nblk / 2;
+  const bool dn = (lo == nblk - 1) || (lo > 0 && (lo & 1) == 0);
+  const int g = lo == 0 ? 0 : lo == nblk - 1 ? K - 1 : dn ? lo / 2 - 1 : (lo + 1) / 2;
+  ListPos p;
+  p.down = dn;
+  p.idx = pref[g * S] * (dn ? n_mp_dn : n_mp_up) + (u - s_bstart[lo]);
+  return p;
+}
 
 // KA: 64-wide k-atoms per ring stage (1 or 2); a stage holds KA weight tiles and KA token tiles.
 template <int AS, int BS, int KA, bool kT = false>
@@ -701,6 +724,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       s_end[i] = fp.up.tb.pos[i] + fp.up.tb.counts[i];
     }
   }
+  // work list: blocks of S experts, U0, [U1, D0], [U2, D1], ..., [U(K-1), D(K-2)], D(K-1)
+  // (U = up units of a group, D = its down units), so a group's H is re-read by its down
+  // units one up block later - while it is still in L2 - instead of after every expert's
+  // up units. S is chosen so an up block spans >= 2 waves of clusters (its down block
+  // then rarely waits); S = E gives the plain [all up][all down] order.
+  int* s_bstart = reinterpret_cast<int*>(
+      (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2 + 128;
+  const int n_mp_up = (fp.up.n_mt + 1) / 2, n_mp_dn = (fp.dn.n_mt + 1) / 2;
+  const int ncl = static_cast<int>(nclusters_x());
+  __syncthreads();   // s_pref complete (S below must be the same in every thread)
+  int S = E;
+  if (fp.interleave) {
+    const long long want = 2LL * ncl * E, per = static_cast<long long>(n_mp_up) * max(1, s_pref[E]);
+    const long long s0 = (want + per - 1) / per, smin = (E + 63) / 64;
+    S = static_cast<int>(s0 < smin ? smin : (s0 > E ? E : s0));
+  }
+  const int K = (E + S - 1) / S, nblk = 2 * K;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int j = 0; j < nblk; ++j) {
+      s_bstart[j] = acc;
+      const bool dn = (j == nblk - 1) || (j > 0 && (j & 1) == 0);
+      const int g = j == 0 ? 0 : j == nblk - 1 ? K - 1 : dn ? j / 2 - 1 : (j + 1) / 2;
+      const int nch = s_pref[min((g + 1) * S, E)] - s_pref[g * S];
+      acc += nch * (dn ? n_mp_dn : n_mp_up);
+    }
+    s_bstart[nblk] = acc;
+  }
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -754,12 +805,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   // pair-units cover m-tiles (2q, 2q+1); with an odd count the last pair has
   // both CTAs on the same m-tile (the follower's copy is computed, not stored)
-  const int n_mp_up = (fp.up.n_mt + 1) / 2, n_mp_dn = (fp.dn.n_mt + 1) / 2;
   const int chunks = s_pref[E];
   const int total_up = chunks * n_mp_up;
   const int total = total_up + chunks * n_mp_dn;
   const int nkb_up = fp.up.K / (BK * KA), nkb_dn = fp.dn.K / (BK * KA);   // stages per unit
-  const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
+  const int cid = static_cast<int>(cluster_id_x());
 
   if (warp == 0) {
     // -------------------------------------------------------------- weight producer (both CTAs)
@@ -768,8 +818,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = cid; u < total; u += ncl) {
-      const bool down = u >= total_up;
-      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
+      const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
+      const bool down = lp.down;
+      const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
       const int n_mt = down ? fp.dn.n_mt : fp.up.n_mt;
       const int nkb = down ? nkb_dn : nkb_up;
       const CUtensorMap* tm = down ? &tmA_dn : &tmA_up;
@@ -819,8 +870,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       while (npend > 0) publish_oldest();
     };
     for (int u = cid; u < total; u += ncl) {
-      const bool down = u >= total_up;
-      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
+      const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
+      const bool down = lp.down;
+      const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
       const int nkb = down ? nkb_dn : nkb_up;
       const CUtensorMap* tm = down ? &tmB_dn : &tmB_up;
       if (down && npend > 0) drain();
@@ -931,9 +983,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       long long t_a = 0, t_b = 0, t_t = 0, t_all = clock64(), t_first_down = 0;
       int n_up = 0, n_dn = 0, kb_total = 0;
       for (int u = cid; u < total; u += ncl) {
-        const bool down = u >= total_up;
+        const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
+        const bool down = lp.down;
         if (kT) { if (down) { if (!n_dn) t_first_down = clock64() - t_all; ++n_dn; } else ++n_up; }
-        const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
+        const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
         const int nkb = down ? nkb_dn : nkb_up;
         const int nmma = (w.ntok + 31) & ~31;
         const bool mn = down && fp.dn.ht;
@@ -988,8 +1041,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int as = 0;
     uint32_t aphase = 0;
     for (int u = cid; u < total; u += ncl) {
-      const bool down = u >= total_up;
-      const Unit w = decode(down ? u - total_up : u, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
+      const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
+      const bool down = lp.down;
+      const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const int mt = 2 * w.mt + static_cast<int>(rank);
@@ -1054,7 +1108,7 @@ int variant() {
 
 size_t smem_bytes_2sm(int E, int as, int bs) {
   return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (4 * E + 2) * 4 +
-         16 + 4 * 1024 + 128 * 4;   // + staging + gather row ids
+         16 + 4 * 1024 + 128 * 4 + (2 * E + 2) * 4;   // + staging + gather row ids + block starts
 }
 
 template <bool kDown, int AS, int BS, bool kT = false>
@@ -1112,8 +1166,12 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  static const bool inter = [] {   // opt-in: measured slower for C2 / C5, faster for C3 only
+    const char* e = getenv("MOESHARD_FFN_INTERLEAVE");
+    return e && e[0] == '1';
+  }();
   FusedParams fp{up, dn, done, static_cast<const uint4*>(cp_src), static_cast<uint4*>(cp_dst),
-                 cp_row_vecs};
+                 cp_row_vecs, inter};
   return launch_pdl(tc_moe_ffn_2sm<AS, BS, KA, kT>, dim3(grid & ~1), dim3(kThreads),
                     smem_bytes_2sm(up.E, AS * KA, BS * KA), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
 }
