@@ -78,6 +78,7 @@ typedef enum {
 #define MOESHARD_FLAG_ROW_COPY_IN_FFN 0x100u  /* bf16 fused mode: copy token rows into expert order inside the FFN launch (per-expert hand-off; experimental, slower) */
 #define MOESHARD_FLAG_ROUTER_TOK64 0x800u     /* tcgen05 router: 64 tokens per CTA (twice the CTAs) instead of 128 */
 #define MOESHARD_FLAG_FUSED_SCAN 0x400u        /* Step 2's per-expert block scans inside the grouping launch (ticket-ordered; experimental, slower) */
+#define MOESHARD_FLAG_DYNAMIC_SCHED 0x1000u   /* fused FFN: clusters take work units from a global counter (correct even when not every cluster is resident, e.g. ranks sharing a GPU); default static round robin */
 #define MOESHARD_FLAG_P2P 0x200u              /* bf16: Steps 3 and 5 by device-initiated stores into peer GPU memory instead of NCCL (see moeshard_p2p_*) */
 
 /* moeshard_forward_stages masks: ROUTE = Step 1 + the token exchange (Step 3 push),

@@ -39,6 +39,7 @@ struct Tables {
   int32_t* pos;            // [E+1] internal segment starts (exclusive scan of round_up(count, 32))
   int32_t* perm_pad;       // [N + 32E] internal row -> global token id (padding rows: stale)
   int32_t* copied;         // [E] 8-row groups of X_perm written per expert (in-FFN row copy), zeroed by Step 2
+  int32_t* next_unit;      // [1] the fused FFN's dynamic work counter, zeroed by Step 2
 };
 
 __device__ __forceinline__ float to_f32(float v) { return v; }

@@ -635,7 +635,12 @@ struct FusedParams {
   uint4* cp_dst = nullptr;
   int cp_row_vecs = 0;
   bool interleave = false;  // expert-group blocks (MOESHARD_FFN_INTERLEAVE=1); default all up, then all down
+  bool dynamic = false;     // units taken from a global counter in list order (MOESHARD_FLAG_DYNAMIC_SCHED)
 };
+
+constexpr int kUQ = 2;             // unit-queue slots (dynamic scheduling): small, so a
+                                   // cluster never sits on units other clusters could run
+constexpr int kUQConsumers = 13;   // warps that read a slot: leader 0,1,3,4-7; follower 0,3,4-7
 
 // Position u of the fused work list -> (down?, index in the up- or down-unit list).
 // Blocks of S experts (see the kernel): s_bstart[j] = first position of block j.
@@ -710,6 +715,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);
     }
+    {  // unit queue barriers (same smem position as computed after the tables below)
+      int* qb = reinterpret_cast<int*>(
+          (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2 + 128 +
+          (2 * E + 2);
+      uint64_t* qf = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(qb + kUQ) + 7) &
+                                                 ~static_cast<uintptr_t>(7));
+      for (int q = 0; q < kUQ; ++q) {
+        mbar_init(&qf[q], 1);
+        mbar_init(&qf[kUQ + q], kUQConsumers);
+      }
+    }
     fence_mbar_init();
   }
   cluster_sync_all();
@@ -741,6 +757,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     S = static_cast<int>(s0 < smin ? smin : (s0 > E ? E : s0));
   }
   const int K = (E + S - 1) / S, nblk = 2 * K;
+  // dynamic unit queue (fp.dynamic): the leader's warp 2 takes units from a global
+  // counter in list order and hands each to every role of both CTAs through a kUQ-slot
+  // ring (slot value + full barrier in each CTA, empty barrier in the leader)
+  int* s_uq = s_bstart + (2 * E + 2);
+  uint64_t* uq_full = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(s_uq + kUQ) + 7) & ~static_cast<uintptr_t>(7));
+  uint64_t* uq_empty = uq_full + kUQ;
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int j = 0; j < nblk; ++j) {
@@ -810,14 +833,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int total = total_up + chunks * n_mp_dn;
   const int nkb_up = fp.up.K / (BK * KA), nkb_dn = fp.dn.K / (BK * KA);   // stages per unit
   const int cid = static_cast<int>(cluster_id_x());
+  const uint32_t leader_uq_empty = mapa_shared(smem_u32(uq_empty), 0);
+  // k-th unit of this cluster: static round robin, or the k-th queue slot (dynamic)
+  auto fetch = [&](int k) -> int {
+    if (!fp.dynamic) return cid + k * ncl;
+    const int slot = k % kUQ;
+    mbar_wait_acquire_cluster(&uq_full[slot], static_cast<uint32_t>((k / kUQ) & 1));
+    const int u = *reinterpret_cast<volatile int*>(&s_uq[slot]);
+    __syncwarp();
+    if (lane == 0) {
+      if (leader) mbar_arrive(&uq_empty[slot]);
+      else mbar_arrive_cluster(leader_uq_empty + slot * 8);
+    }
+    return u;
+  };
 
-  if (warp == 0) {
+  if (warp == 2) {
+    if (fp.dynamic && leader) {
+      // ------------------------------------------------------------ unit scheduler (leader)
+      const uint32_t peer_uq = mapa_shared(smem_u32(s_uq), 1);
+      const uint32_t peer_full = mapa_shared(smem_u32(uq_full), 1);
+      for (int k = 0;; ++k) {
+        const int slot = k % kUQ;
+        mbar_wait(&uq_empty[slot], static_cast<uint32_t>(((k / kUQ) & 1) ^ 1));
+        int u = 0;
+        if (lane == 0) {
+          u = atomicAdd(fp.dn.tb.next_unit, 1);
+          s_uq[slot] = u;
+          st_shared_cluster_u32(peer_uq + slot * 4, static_cast<uint32_t>(u));
+          mbar_arrive(&uq_full[slot]);
+          mbar_arrive_release_cluster(peer_full + slot * 8);
+        }
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= total) break;
+      }
+    }
+  } else if (warp == 0) {
     // -------------------------------------------------------------- weight producer (both CTAs)
     const uint64_t pol_w = policy_evict_first();
     const uint32_t leader_full = mapa_shared(smem_u32(fullA), 0);
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = cid; u < total; u += ncl) {
+    for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
       const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
       const bool down = lp.down;
       const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
@@ -869,7 +926,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       cp_async_wait<0>();
       while (npend > 0) publish_oldest();
     };
-    for (int u = cid; u < total; u += ncl) {
+    for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
       const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
       const bool down = lp.down;
       const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
@@ -982,7 +1039,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t aphase = 0;
       long long t_a = 0, t_b = 0, t_t = 0, t_all = clock64(), t_first_down = 0;
       int n_up = 0, n_dn = 0, kb_total = 0;
-      for (int u = cid; u < total; u += ncl) {
+      for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
         const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
         const bool down = lp.down;
         if (kT) { if (down) { if (!n_dn) t_first_down = clock64() - t_all; ++n_dn; } else ++n_up; }
@@ -1040,7 +1097,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
     int as = 0;
     uint32_t aphase = 0;
-    for (int u = cid; u < total; u += ncl) {
+    for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
       const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
       const bool down = lp.down;
       const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
@@ -1108,7 +1165,8 @@ int variant() {
 
 size_t smem_bytes_2sm(int E, int as, int bs) {
   return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (4 * E + 2) * 4 +
-         16 + 4 * 1024 + 128 * 4 + (2 * E + 2) * 4;   // + staging + gather row ids + block starts
+         16 + 4 * 1024 + 128 * 4 + (2 * E + 2) * 4 + 96;   // + staging + gather row ids + block
+                                                            // starts + unit queue
 }
 
 template <bool kDown, int AS, int BS, bool kT = false>
@@ -1157,7 +1215,7 @@ template <int AS, int BS, int KA, bool kT = false>
 cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                          const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn, const TcParams& up,
                          const TcParams& dn, int32_t* done, const void* cp_src, void* cp_dst,
-                         int cp_row_vecs, int grid, cudaStream_t s) {
+                         int cp_row_vecs, bool dynamic, int grid, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS, KA, kT>,
@@ -1170,8 +1228,12 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
     const char* e = getenv("MOESHARD_FFN_INTERLEAVE");
     return e && e[0] == '1';
   }();
+  static const int dyn_env = [] {   // MOESHARD_FFN_SCHED=dynamic|static overrides the flag
+    const char* e = getenv("MOESHARD_FFN_SCHED");
+    return e ? (e[0] == 'd' ? 1 : 0) : -1;
+  }();
   FusedParams fp{up, dn, done, static_cast<const uint4*>(cp_src), static_cast<uint4*>(cp_dst),
-                 cp_row_vecs, inter};
+                 cp_row_vecs, inter, dyn_env >= 0 ? dyn_env == 1 : dynamic};
   return launch_pdl(tc_moe_ffn_2sm<AS, BS, KA, kT>, dim3(grid & ~1), dim3(kThreads),
                     smem_bytes_2sm(up.E, AS * KA, BS * KA), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
 }
@@ -1180,17 +1242,17 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
 cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
                               const TcParams& up, const TcParams& dn, int32_t* done,
-                              const void* cp_src, void* cp_dst, int cp_row_vecs, int grid,
-                              cudaStream_t s) {
+                              const void* cp_src, void* cp_dst, int cp_row_vecs, bool dynamic,
+                              int grid, cudaStream_t s) {
   // MOESHARD_TC_VARIANT 20: two k-atoms per ring stage (3 + 3 stages of 32 KB)
   if (variant() == 21)
     return launch_fused<6, 6, 1, true>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src,
-                                       cp_dst, cp_row_vecs, grid, s);
+                                       cp_dst, cp_row_vecs, dynamic, grid, s);
   if (variant() == 20 && up.K % 128 == 0 && dn.K % 128 == 0 && !up.gather_cp)
     return launch_fused<3, 3, 2>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src, cp_dst,
-                                 cp_row_vecs, grid, s);
+                                 cp_row_vecs, dynamic, grid, s);
   return launch_fused<6, 6, 1>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src, cp_dst,
-                               cp_row_vecs, grid, s);
+                               cp_row_vecs, dynamic, grid, s);
 }
 
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,

@@ -88,6 +88,7 @@ __device__ __forceinline__ void segment_tables(int E, const int* s_tot, const in
       tb.simt_chunk_pref[e] = smp;
     }
     if (threadIdx.x == 0) {
+      tb.next_unit[0] = 0;
       tb.pos[E] = tot_pad;
       tb.offsets[E] = tot_cnt;
       tb.tc_chunk_pref[E] = tot_tc;

@@ -146,7 +146,7 @@ Layout make_layout(const moeshard_config& c, int world) {
   L.route = take(Nmax * sizeof(RouteRec));
   L.block_hist = take(nb * E * 4);
   L.block_base = take(nb * E * 4);
-  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + E + (E + 1) + E + 4);
+  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + E + (E + 1) + E + 4 + 1);
   L.npad = (Nmax + kSegAlign * E + 63) / 64 * 64;
   L.ints = take(L.n_ints * 4);
   L.done = take((Nmax / kTcTokTile + E + 8) * 4);   // per token chunk: <= N/256 + E chunks
@@ -395,6 +395,7 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->tb.pos = c->block_tot + E;
   c->tb.copied = c->tb.pos + (E + 1);
   c->gsync = c->tb.copied + E;   // 4 ints: the grouping launch's ticket / scan / exit counters
+  c->tb.next_unit = c->gsync + 4;
   c->tb.perm_pad = reinterpret_cast<int32_t*>(c->ws + L.perm_pad);
   c->perm = reinterpret_cast<int32_t*>(c->ws + L.perm);
   c->x_all = c->coll && !c->p2p ? c->ws + L.x_all : nullptr;
@@ -657,7 +658,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
       CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather && !gather_cp ? tm_xg : c->tm_xperm16,
                                     lw.tm_out, ht ? c->tm_Ht : c->tm_H16, up, dn, c->tb.done,
                                     copy_in_ffn ? x_all : nullptr, c->x_perm, h * c->elt / 16,
-                                    c->num_sms, s));
+                                    (c->cfg.flags & MOESHARD_FLAG_DYNAMIC_SCHED) != 0, c->num_sms, s));
       c->mark(4, s);
       c->launches += 1;
       if (c->p2p) {

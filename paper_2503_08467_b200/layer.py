@@ -214,35 +214,39 @@ class HostStreamer:
 
     step(k): the H2D copy of batch k runs on a copy stream, the forward on the
     caller's stream, the D2H copy of its output on a second copy stream, with
-    two device buffers so the copies of neighbouring batches overlap the
+    NBUF device buffers so the copies of neighbouring batches overlap the
     forward of this one (PCIe is full duplex). join() makes the caller's stream
     wait for every copy issued so far. Marshalling only: the forward is the
     library's."""
+
+    NBUF = 3   # device buffers per direction: H2D of k+2 never waits for forward k
 
     def __init__(self, layer: MoEShardLayer, n_local: int):
         self.layer = layer
         dev = f"cuda:{layer.device}"
         self.h2d = torch.cuda.Stream(device=dev)
         self.d2h = torch.cuda.Stream(device=dev)
-        self.din = [torch.empty(n_local, layer.h, dtype=layer.dtype, device=dev) for _ in range(2)]
-        self.dout = [torch.empty_like(self.din[0]) for _ in range(2)]
-        self.in_ready = [torch.cuda.Event() for _ in range(2)]
-        self.fwd_done = [torch.cuda.Event() for _ in range(2)]
-        self.out_free = [torch.cuda.Event() for _ in range(2)]
+        nb = self.NBUF
+        self.din = [torch.empty(n_local, layer.h, dtype=layer.dtype, device=dev) for _ in range(nb)]
+        self.dout = [torch.empty_like(self.din[0]) for _ in range(nb)]
+        self.in_ready = [torch.cuda.Event() for _ in range(nb)]
+        self.fwd_done = [torch.cuda.Event() for _ in range(nb)]
+        self.out_free = [torch.cuda.Event() for _ in range(nb)]
         self.k = 0
 
     def step(self, layer_idx: int, host_in: torch.Tensor, router_w: torch.Tensor,
              host_out: torch.Tensor, forced_expert: Optional[torch.Tensor] = None) -> torch.Tensor:
-        b = self.k % 2
+        nb = self.NBUF
+        b = self.k % nb
         comp = torch.cuda.current_stream()
-        if self.k >= 2:
-            self.h2d.wait_event(self.fwd_done[b])      # forward(k-2) finished reading din[b]
+        if self.k >= nb:
+            self.h2d.wait_event(self.fwd_done[b])      # forward(k-nb) finished reading din[b]
         with torch.cuda.stream(self.h2d):
             self.din[b].copy_(host_in, non_blocking=True)
             self.in_ready[b].record(self.h2d)
         comp.wait_event(self.in_ready[b])
-        if self.k >= 2:
-            comp.wait_event(self.out_free[b])          # D2H(k-2) finished reading dout[b]
+        if self.k >= nb:
+            comp.wait_event(self.out_free[b])          # D2H(k-nb) finished reading dout[b]
         self.layer.forward(layer_idx, self.din[b], router_w, forced_expert=forced_expert,
                            out=self.dout[b])
         self.fwd_done[b].record(comp)

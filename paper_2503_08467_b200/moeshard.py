@@ -32,6 +32,7 @@ MOESHARD_FLAG_ROW_COPY_IN_FFN = 0x100
 MOESHARD_FLAG_P2P = 0x200
 MOESHARD_FLAG_FUSED_SCAN = 0x400
 MOESHARD_FLAG_ROUTER_TOK64 = 0x800
+MOESHARD_FLAG_DYNAMIC_SCHED = 0x1000
 MOESHARD_STAGE_ROUTE = 0x1
 MOESHARD_STAGE_COMPUTE = 0x2
 MOESHARD_STAGE_REDUCE = 0x4

@@ -391,7 +391,7 @@ def test_route_group_fused_matches_separate_and_oracle(N, h, d_ff, E, routing):
 
 
 @pytest.mark.parametrize("flag", ["FUSED_ROUTE_GROUP", "CPASYNC_GATHER", "ROW_COPY_IN_FFN", "FUSED_SCAN",
-                                  None])
+                                  "DYNAMIC_SCHED", None])
 def test_forward_under_cuda_graph_replay(flag):
     """A captured forward replays correctly with new token values and new routing
     (the grid barrier of the fused route+group launch carries no launch arguments)."""
@@ -433,7 +433,7 @@ def test_forward_under_cuda_graph_replay(flag):
 
 
 # --------------------------------------------------------------------- alternative token paths
-@pytest.mark.parametrize("flag", ["ROUTER_TOK64", "FUSED_SCAN", "ROW_COPY_IN_FFN", "CPASYNC_GATHER",
+@pytest.mark.parametrize("flag", ["DYNAMIC_SCHED", "ROUTER_TOK64", "FUSED_SCAN", "ROW_COPY_IN_FFN", "CPASYNC_GATHER",
                                   "TMA_GATHER", "FUSED_ROUTE_GROUP"])
 @pytest.mark.parametrize("N,h,d_ff,E,routing", [
     (3000, 512, 1024, 64, "zipf"),       # multi-chunk segments, ragged halves
@@ -537,5 +537,48 @@ def test_p2p_missing_peer_times_out_instead_of_hanging():
                       stages=C.MOESHARD_STAGE_ROUTE | C.MOESHARD_STAGE_COMPUTE)
     with pytest.raises(C.MoEShardError, match="PROTOCOL"):
         layers[0].check()
+    for L in layers:
+        L.close()
+
+
+def test_p2p_exchange_concurrent_streams():
+    """MOESHARD_FLAG_P2P with two ranks sharing this GPU, each driving whole forwards on its
+    own CUDA stream (no lock-step): the cross-rank waits inside the kernels resolve while
+    both ranks' kernels run concurrently, over several forwards (epochs) - the closest
+    one-GPU stand-in for two processes on two GPUs."""
+    from paper_2503_08467_b200 import MoEShardLayer, shard_columns
+    from paper_2503_08467_b200 import moeshard as C
+    G, N, h, d_ff, E = 2, 2048, 256, 512, 16
+    n = N // G
+    # dynamic FFN scheduling: the two ranks' persistent FFN grids share the SMs, and a
+    # static schedule would let a resident cluster wait on work of a non-resident one
+    layers = [MoEShardLayer(h, d_ff, E, max_tokens_per_rank=n, dtype=torch.bfloat16, rank=r,
+                            world=G, flags=C.MOESHARD_FLAG_P2P | C.MOESHARD_FLAG_DYNAMIC_SCHED)
+              for r in range(G)]
+    MoEShardLayer.p2p_connect_local(layers)
+    base = W.make_layer_inputs(41, N, h, d_ff, E, dtype=torch.bfloat16, routing="zipf")
+    for r, L in enumerate(layers):
+        c0, c1 = shard_columns(d_ff, G, r)
+        L.load_expert_shards(0, base.w_i[:, :, c0:c1].cuda(), base.w_o[:, c0:c1, :].cuda())
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    w_r = base.w_r.cuda()
+    for seed in (41, 42, 43, 44):
+        x = W.make_tokens(seed, N, h)
+        f = W.draw_experts(seed, N, E, "zipf")
+        xs = [x[r * n:(r + 1) * n].cuda().contiguous() for r in range(G)]
+        fs = [f[r * n:(r + 1) * n].cuda().contiguous() for r in range(G)]
+        ys = [torch.empty_like(v) for v in xs]
+        torch.cuda.synchronize()
+        for r in range(G):   # rank 0's whole forward is enqueued before rank 1 starts
+            with torch.cuda.stream(streams[r]):
+                layers[r].forward(0, xs[r], w_r, forced_expert=fs[r], out=ys[r])
+        torch.cuda.synchronize()
+        for r, L in enumerate(layers):
+            with torch.cuda.stream(streams[r]):
+                L.check()
+        y_ref = O.moe_layer(x, base.w_r, base.w_i, base.w_o, forced=f.cpu().numpy())
+        err = O.max_abs_rel(torch.cat(ys).float().cpu().numpy(), y_ref)
+        assert err <= BF16_TOL, f"seed {seed}: max-abs-rel {err:.3e}"
     for L in layers:
         L.close()
