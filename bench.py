@@ -459,7 +459,7 @@ def main():
         e2e = {"value": N / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": n * h * 2 * G, "d2h_bytes_per_step": n * h * 2 * G,
                "path": "MoEShardLayer.host_streamer: pinned H2D (copy stream) -> moeshard_forward "
-                       "-> D2H (copy stream), double-buffered, per rank"}
+                       "-> D2H (copy stream), 3 device buffers per direction, per rank"}
 
     hbm, tf_burst, tf_sust, peak_src = peaks()
     # algorithmic bytes per launch
