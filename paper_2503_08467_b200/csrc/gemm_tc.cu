@@ -636,6 +636,7 @@ struct FusedParams {
   int cp_row_vecs = 0;
   bool interleave = false;  // expert-group blocks (MOESHARD_FFN_INTERLEAVE=1); default all up, then all down
   bool dynamic = false;     // units taken from a global counter in list order (MOESHARD_FLAG_DYNAMIC_SCHED)
+  bool light_release = true;  // H hand-off: bar.sync + one release (MOESHARD_LIGHT_RELEASE=0: + per-thread fences)
 };
 
 constexpr int kUQ = 2;             // unit-queue slots (dynamic scheduling): small, so a
@@ -1116,8 +1117,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + as * 8);
-      if (!down) {   // publish this CTA's H tile of expert e
-        __threadfence();
+      if (!down) {   // publish this CTA's H tile of the chunk
+        // bar.sync orders every epilogue thread's H stores before thread 0's release
+        // (cumulative at gpu scope), so the other warps need no fence of their own and
+        // go straight on to the next tile (light_release; else every thread fences first)
+        if (!fp.light_release) __threadfence();
         asm volatile("bar.sync 2, 128;" ::: "memory");   // the 4 epilogue warps
         if (wq == 0 && lane == 0) red_release_gpu_add(fp.done + w.chunk, 1);
       }
@@ -1228,12 +1232,16 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
     const char* e = getenv("MOESHARD_FFN_INTERLEAVE");
     return e && e[0] == '1';
   }();
+  static const bool light = [] {
+    const char* e = getenv("MOESHARD_LIGHT_RELEASE");
+    return !(e && e[0] == '0');
+  }();
   static const int dyn_env = [] {   // MOESHARD_FFN_SCHED=dynamic|static overrides the flag
     const char* e = getenv("MOESHARD_FFN_SCHED");
     return e ? (e[0] == 'd' ? 1 : 0) : -1;
   }();
   FusedParams fp{up, dn, done, static_cast<const uint4*>(cp_src), static_cast<uint4*>(cp_dst),
-                 cp_row_vecs, inter, dyn_env >= 0 ? dyn_env == 1 : dynamic};
+                 cp_row_vecs, inter, dyn_env >= 0 ? dyn_env == 1 : dynamic, light};
   return launch_pdl(tc_moe_ffn_2sm<AS, BS, KA, kT>, dim3(grid & ~1), dim3(kThreads),
                     smem_bytes_2sm(up.E, AS * KA, BS * KA), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
 }
