@@ -36,7 +36,8 @@
  *   - moeshard_forward is enqueue-only on `stream`: no host synchronisation,
  *     no data-dependent launch geometry, CUDA-graph capturable.
  *   - Collective calls (moeshard_init, moeshard_forward) must be made by all
- *     `world` ranks in the same order with the same `layer` and `n_local`.
+ *     `world` ranks in the same order with the same `layer` and `n_local`
+ *     (with MOESHARD_FLAG_UNEVEN_TOKENS n_local may differ between ranks).
  */
 #ifndef MOESHARD_H
 #define MOESHARD_H
@@ -79,6 +80,7 @@ typedef enum {
 #define MOESHARD_FLAG_ROUTER_TOK64 0x800u     /* tcgen05 router: 64 tokens per CTA (twice the CTAs) instead of 128 */
 #define MOESHARD_FLAG_FUSED_SCAN 0x400u        /* Step 2's per-expert block scans inside the grouping launch (ticket-ordered; experimental, slower) */
 #define MOESHARD_FLAG_DYNAMIC_SCHED 0x1000u   /* fused FFN: clusters take work units from a global counter (correct even when not every cluster is resident, e.g. ranks sharing a GPU); default static round robin */
+#define MOESHARD_FLAG_UNEVEN_TOKENS 0x2000u   /* world > 1: ranks may pass different n_local each forward; token slots of max_tokens_per_rank rows per rank, routing tables [world * max_tokens_per_rank] with expert -1 in unused slots */
 #define MOESHARD_FLAG_P2P 0x200u              /* bf16: Steps 3 and 5 by device-initiated stores into peer GPU memory instead of NCCL (see moeshard_p2p_*) */
 
 /* moeshard_forward_stages masks: ROUTE = Step 1 + the token exchange (Step 3 push),
@@ -154,7 +156,11 @@ int moeshard_load_expert_shards(moeshard_ctx* ctx, int layer, const void* w_in_s
  *                outside [0, E) are clamped and raise the sticky device error
  *                reported by moeshard_check().
  * n_local must satisfy 0 <= n_local <= max_tokens_per_rank and be equal on
- * all ranks (v1). Enqueue-only on `stream`. Errors: BOUNDS, NOT_LOADED,
+ * all ranks - unless the context has MOESHARD_FLAG_UNEVEN_TOKENS: then every
+ * rank passes its own n_local (0 included, and every rank must still call),
+ * tokens travel in slots of max_tokens_per_rank rows per rank and the unused
+ * tail of a slot is routed nowhere (the per-GPU sizes of Alg. 1 Step 2,
+ * PAPER.md:191-195). Enqueue-only on `stream`. Errors: BOUNDS, NOT_LOADED,
  * INVALID_ARG, CUDA, NCCL. */
 int moeshard_forward(moeshard_ctx* ctx, int layer, const void* hidden, int n_local,
                      const void* router_w, void* hidden_out, const int32_t* forced_expert,
@@ -163,6 +169,8 @@ int moeshard_forward(moeshard_ctx* ctx, int layer, const void* hidden, int n_loc
 /* Routing of the most recent forward (Steps 1-2), copied on `stream` into
  * caller device buffers (any may be NULL):
  *   expert_all [dev] int32 [world*n_local]  e_t for all global tokens t = r*n + i
+ *              (MOESHARD_FLAG_UNEVEN_TOKENS: [world*max_tokens_per_rank], t = r*cap + i,
+ *              -1 where slot r has no token i; gate_all / perm likewise)
  *   gate_all   [dev] fp32  [world*n_local]  g_t
  *   counts     [dev] int32 [E]              m_sizes summed over ranks
  *   offsets    [dev] int32 [E+1]            exclusive scan of counts

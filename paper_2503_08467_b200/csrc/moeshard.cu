@@ -536,7 +536,13 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     return fail(c, MOESHARD_ERR_PROTOCOL, "n_local=%d differs from the ROUTE stage's %d", n,
                 c->last_n);
   c->last_n = n;
-  if (n == 0) return MOESHARD_OK;
+  // MOESHARD_FLAG_UNEVEN_TOKENS: ranks may pass different n_local (the paper's Step 2
+  // exchanges the per-GPU sizes): every rank's tokens occupy a slot of
+  // ns = max_tokens_per_rank rows, the unused tail of a slot is marked invalid (expert -1)
+  // and routes nowhere. Without the flag every rank passes the same n and ns = n.
+  const bool uneven = c->coll && (c->cfg.flags & MOESHARD_FLAG_UNEVEN_TOKENS);
+  if (n == 0 && !uneven) return MOESHARD_OK;
+  const int ns = uneven ? c->cfg.max_tokens_per_rank : n;   // rows per rank slot
   const bool st_route = stages & MOESHARD_STAGE_ROUTE, st_compute = stages & MOESHARD_STAGE_COMPUTE,
              st_reduce = stages & MOESHARD_STAGE_REDUCE;
   const ncclDataType_t ndt = c->cfg.dtype == MOESHARD_BF16 ? ncclBfloat16 : ncclFloat32;
@@ -544,13 +550,14 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
 
   c->mark(0, s);
   // Step 1: route local tokens
-  RouteRec* my_route = c->route + (c->coll ? static_cast<size_t>(c->rank) * n : 0);
+  RouteRec* my_route = c->route + (c->coll ? static_cast<size_t>(c->rank) * ns : 0);
   // tokens per hist-block = tokens per router CTA (64 for the SIMT router; the
   // tcgen05 router runs 64 or 128 token rows per CTA, c->router_tok)
   const int HB = c->use_tc ? c->router_tok : 64;
-  const int nbr = (n + HB - 1) / HB;                    // hist-blocks per rank
+  const int nbr_own = (n + HB - 1) / HB;                // hist-blocks this rank's router fills
+  const int nbr = (ns + HB - 1) / HB;                   // hist-blocks per rank slot
   const int NB = (c->coll ? c->world : 1) * nbr;
-  const int N = (c->coll ? c->world : 1) * n;             // tokens of all ranks
+  const int N = (c->coll ? c->world : 1) * ns;            // token slots of all ranks
   int32_t* my_hist = c->block_hist + (c->coll ? static_cast<size_t>(c->rank) * nbr * E : 0);
   const bool fused = c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_UNFUSED_GEMM) &&
                      F % kTcFeatTile == 0 && h % kTcFeatTile == 0;   // odd tile counts: see FFN kernel
@@ -564,8 +571,8 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   const bool route_group = c->use_tc && !c->coll && (E % 8) == 0 && nbr <= c->num_sms &&
                            h <= 1024 && c->pf_bytes == 0 && HB == 128 &&
                            (c->cfg.flags & MOESHARD_FLAG_FUSED_ROUTE_GROUP);
-  if (!st_route) {
-    // (routing and the token exchange ran in an earlier call)
+  if (!st_route || n == 0) {
+    // (routing ran in an earlier call, or this rank has no tokens this time)
   } else if (route_group) {
     CUtensorMap tm_x, tm_w;
     if (!make_tmap(&tm_x, hidden, h, n, 128) || !make_tmap(&tm_w, router_w, E, h, 64))
@@ -597,17 +604,33 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, my_hist, err_flag, s);
     c->launches += 1;
   }
+  if (st_route && uneven) {
+    // the rest of this rank's slot: no token (expert -1), empty hist-blocks
+    if (ns > n)
+      CUDA_TRY(c, cudaMemsetAsync(my_route + n, 0xFF, static_cast<size_t>(ns - n) * sizeof(RouteRec), s));
+    if (nbr > nbr_own)
+      CUDA_TRY(c, cudaMemsetAsync(my_hist + static_cast<size_t>(nbr_own) * E, 0,
+                                  static_cast<size_t>(nbr - nbr_own) * E * 4, s));
+  }
   c->mark(1, s);
   // Steps 2+3: metadata + token scatter (replicate all tokens on all GPUs)
   const void* x_all = c->coll ? c->x_all : hidden;
   if (st_route && c->p2p) {
     // Step 3 over peer memory: push this rank's tokens / records / histograms to every rank
-    CUDA_TRY(c, launch_p2p_push(c->pa, hidden, n, h * c->elt / 16, nbr, E, c->num_sms, s));
+    CUDA_TRY(c, launch_p2p_push(c->pa, hidden, n, ns, h * c->elt / 16, nbr, E, c->num_sms, s));
     c->launches += 1;
   } else if (st_route && c->coll) {
+    const void* xsend = hidden;
+    if (uneven) {   // the slot's n rows in place, the AllGather sends the whole slot
+      char* slot = static_cast<char*>(c->x_all) + static_cast<size_t>(c->rank) * ns * h * c->elt;
+      if (n > 0)
+        CUDA_TRY(c, cudaMemcpyAsync(slot, hidden, static_cast<size_t>(n) * h * c->elt,
+                                    cudaMemcpyDeviceToDevice, s));
+      xsend = slot;
+    }
     NCCL_TRY(c, nccl().GroupStart());
-    NCCL_TRY(c, nccl().AllGather(hidden, c->x_all, static_cast<size_t>(n) * h, ndt, c->comm, s));
-    NCCL_TRY(c, nccl().AllGather(my_route, c->route, static_cast<size_t>(n) * 2, ncclInt32,
+    NCCL_TRY(c, nccl().AllGather(xsend, c->x_all, static_cast<size_t>(ns) * h, ndt, c->comm, s));
+    NCCL_TRY(c, nccl().AllGather(my_route, c->route, static_cast<size_t>(ns) * 2, ncclInt32,
                                  c->comm, s));
     NCCL_TRY(c, nccl().AllGather(my_hist, c->block_hist, static_cast<size_t>(nbr) * E, ncclInt32,
                                  c->comm, s));
@@ -629,7 +652,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
       // the scan launch + PDL (the ticket atomic and the spin sit on the critical path)
       const bool one = (c->cfg.flags & MOESHARD_FLAG_FUSED_SCAN) != 0;
       launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb,
-                          F / kTcFeatTile, h / kTcFeatTile, c->route, x_all, n, nbr, HB,
+                          F / kTcFeatTile, h / kTcFeatTile, c->route, x_all, ns, nbr, HB,
                           h * c->elt, c->perm, gather || copy_in_ffn ? nullptr : c->x_perm,
                           one ? c->gsync : nullptr, s);
       c->launches += one ? 1 : 2;
@@ -649,7 +672,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
       TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
                   static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route, nullptr, 0, ht, np};
       if (c->p2p) {   // Step 5 send: partial rows go straight to their owner's receive slot
-        dn.p2p_n = n;
+        dn.p2p_n = ns;
         for (int g = 0; g < c->world; ++g)
           dn.p2p_out[g] = reinterpret_cast<__nv_bfloat16*>(
               c->pa.peers[g] + c->PL.off_recv +
@@ -688,9 +711,17 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   if (st_reduce && c->p2p) {
     CUDA_TRY(c, launch_p2p_reduce(c->pa, n, h * c->elt / 16, hidden_out, err_flag, c->num_sms, s));
     c->launches += 1;
-  } else if (st_reduce && c->coll) {
+  } else if (st_reduce && c->coll && !uneven) {
     NCCL_TRY(c, nccl().ReduceScatter(c->partial, hidden_out, static_cast<size_t>(n) * h, ndt,
                                      ncclSum, c->comm, s));
+  } else if (st_reduce && c->coll) {
+    // whole slots, then this rank's n rows (x_all's slot is free once the FFN has run)
+    char* slot = static_cast<char*>(c->x_all) + static_cast<size_t>(c->rank) * ns * h * c->elt;
+    NCCL_TRY(c, nccl().ReduceScatter(c->partial, slot, static_cast<size_t>(ns) * h, ndt, ncclSum,
+                                     c->comm, s));
+    if (n > 0)
+      CUDA_TRY(c, cudaMemcpyAsync(hidden_out, slot, static_cast<size_t>(n) * h * c->elt,
+                                  cudaMemcpyDeviceToDevice, s));
   }
   c->mark(6, s);
   if (c->prof) c->prof_count++;
@@ -747,7 +778,9 @@ int moeshard_get_routing(moeshard_ctx* c, int32_t* expert_all, float* gate_all, 
                          int32_t* offsets, int32_t* perm, void* stream) {
   if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "ctx is NULL");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const size_t N = static_cast<size_t>(c->coll ? c->world : 1) * c->last_n;
+  const bool uneven = c->coll && (c->cfg.flags & MOESHARD_FLAG_UNEVEN_TOKENS);
+  const size_t N = static_cast<size_t>(c->coll ? c->world : 1) *
+                   (uneven ? c->cfg.max_tokens_per_rank : c->last_n);
   if (N > 0) {
     if (expert_all)
       CUDA_TRY(c, cudaMemcpy2DAsync(expert_all, 4, &c->route[0].expert, sizeof(RouteRec), 4, N,

@@ -57,11 +57,12 @@ __device__ __forceinline__ void wait_flags(const int32_t* flags, int world, int 
 // Step 3 push: this rank's n rows / records / block histograms into slot `rank`
 // of every peer region. 16-B vectors, grid-stride.
 __global__ void __launch_bounds__(256) push_tokens(P2PArgs a, const uint4* __restrict__ x, int n,
-                                                   int row_vecs, int nbr, int E) {
+                                                   int ns, int row_vecs, int nbr, int E) {
   ptx::griddep_wait();   // x / route / hist come from the router
   const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
-  const size_t nx = static_cast<size_t>(n) * row_vecs;
-  const size_t nrec = static_cast<size_t>(n);              // RouteRec = 8 B -> half vectors
+  const size_t nx = static_cast<size_t>(n) * row_vecs;    // this rank's rows
+  const size_t sx = static_cast<size_t>(ns) * row_vecs;   // slot stride (ns >= n)
+  const size_t nrec = static_cast<size_t>(ns);            // the whole slot (tail marked invalid)
   const size_t nh = static_cast<size_t>(nbr) * E;          // int32
   const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(256) push_tokens(P2PArgs a, const uint4* __res
   const int32_t* my_hist = reinterpret_cast<const int32_t*>(a.self + a.off_hist) + a.rank * nh;
   for (int g = 0; g < a.world; ++g) {
     char* peer = a.peers[g];
-    uint4* dx = reinterpret_cast<uint4*>(peer + a.off_x) + a.rank * nx;
+    uint4* dx = reinterpret_cast<uint4*>(peer + a.off_x) + a.rank * sx;
     for (size_t i = tid; i < nx; i += stride) dx[i] = __ldg(x + i);
     if (g != a.rank) {   // the router already wrote its own slot of route / hist
       RouteRec* dr = reinterpret_cast<RouteRec*>(peer + a.off_route) + a.rank * nrec;
@@ -172,13 +173,13 @@ P2PLayout p2p_layout(int world, int n_max, int h, int E, int nbr_max) {
   return L;
 }
 
-cudaError_t launch_p2p_push(const P2PArgs& a, const void* x, int n, int row_vecs, int nbr, int E,
-                            int num_sms, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  const size_t work = static_cast<size_t>(n) * row_vecs;
+cudaError_t launch_p2p_push(const P2PArgs& a, const void* x, int n, int ns, int row_vecs, int nbr,
+                            int E, int num_sms, cudaStream_t s) {
+  if (ns <= 0) return cudaSuccess;
+  const size_t work = static_cast<size_t>(std::max(n, 1)) * row_vecs;
   const int grid = static_cast<int>(std::min<size_t>(2 * num_sms, (work + 255) / 256));
   return launch_pdl(push_tokens, dim3(std::max(grid, 1)), dim3(256), 0, s, a,
-                    static_cast<const uint4*>(x), n, row_vecs, nbr, E);
+                    static_cast<const uint4*>(x), n, ns, row_vecs, nbr, E);
 }
 
 cudaError_t launch_p2p_wait_tokens(const P2PArgs& a, int32_t* err, cudaStream_t s) {
@@ -193,7 +194,7 @@ cudaError_t launch_p2p_signal_partials(const P2PArgs& a, cudaStream_t s) {
 
 cudaError_t launch_p2p_reduce(const P2PArgs& a, int n, int row_vecs, void* out, int32_t* err,
                               int num_sms, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
+  // runs even for n = 0 (uneven token counts): it consumes the flags and advances the epoch
   const size_t work = static_cast<size_t>(n) * row_vecs;
   const int grid = static_cast<int>(std::min<size_t>(2 * num_sms, (work + 255) / 256));
   reduce_partials<<<std::max(grid, 1), 256, 0, s>>>(a, n, row_vecs, static_cast<uint4*>(out), err);

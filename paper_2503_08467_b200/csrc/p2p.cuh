@@ -23,8 +23,8 @@ struct P2PArgs {
 
 // Step 3: copy x [n][row_vecs x 16 B], this rank's route records and block histograms
 // (already in its own region slot) into slot `rank` of every region; publish flags_ag.
-cudaError_t launch_p2p_push(const P2PArgs& a, const void* x, int n, int row_vecs, int nbr, int E,
-                            int num_sms, cudaStream_t s);
+cudaError_t launch_p2p_push(const P2PArgs& a, const void* x, int n, int ns, int row_vecs, int nbr,
+                            int E, int num_sms, cudaStream_t s);
 // wait until every rank's Step-3 data has landed in this rank's region (bounded; err bit 4)
 cudaError_t launch_p2p_wait_tokens(const P2PArgs& a, int32_t* err, cudaStream_t s);
 // after the FFN wrote its partial rows into the owners' recv slots: publish flags_rs

@@ -153,6 +153,10 @@ class MoEShardLayer:
     __call__ = forward
 
     def routing(self, n_local: int) -> dict:
+        """Routing tables of the last forward. With MOESHARD_FLAG_UNEVEN_TOKENS the token
+        index space is world slots of max_tokens_per_rank (unused slot entries: expert -1)."""
+        if self._collective() and (self.cfg.flags & C.MOESHARD_FLAG_UNEVEN_TOKENS):
+            n_local = self.cfg.max_tokens_per_rank
         N = n_local * (self.world if self._collective() else 1)
         dev = f"cuda:{self.device}"
         r = {

@@ -33,6 +33,7 @@ MOESHARD_FLAG_P2P = 0x200
 MOESHARD_FLAG_FUSED_SCAN = 0x400
 MOESHARD_FLAG_ROUTER_TOK64 = 0x800
 MOESHARD_FLAG_DYNAMIC_SCHED = 0x1000
+MOESHARD_FLAG_UNEVEN_TOKENS = 0x2000
 MOESHARD_STAGE_ROUTE = 0x1
 MOESHARD_STAGE_COMPUTE = 0x2
 MOESHARD_STAGE_REDUCE = 0x4

@@ -582,3 +582,59 @@ def test_p2p_exchange_concurrent_streams():
         assert err <= BF16_TOL, f"seed {seed}: max-abs-rel {err:.3e}"
     for L in layers:
         L.close()
+
+
+# --------------------------------------------------------------------- uneven token counts
+@pytest.mark.parametrize("transport", ["P2P", "FORCE_COLLECTIVES"])
+@pytest.mark.parametrize("ns_local", [(700, 300), (512, 0, 130, 61), (1000,)])
+def test_uneven_tokens_per_rank(transport, ns_local):
+    """MOESHARD_FLAG_UNEVEN_TOKENS: ranks pass different n_local (one may pass 0); the
+    result for every rank's tokens equals the unsharded oracle on the concatenation, and
+    the routing tables (slots of max_tokens_per_rank, expert -1 in unused entries) match
+    the oracle's on every real token. P2P: ranks share this GPU in lock-step stages;
+    NCCL: one rank (a 1-rank communicator) exercises the slot AllGather / ReduceScatter."""
+    from paper_2503_08467_b200 import MoEShardLayer, shard_columns
+    from paper_2503_08467_b200 import moeshard as C
+    G = len(ns_local)
+    if transport == "FORCE_COLLECTIVES" and G > 1:
+        pytest.skip("NCCL needs one GPU per rank")
+    h, E, cap = 256, 16, 1024
+    d_ff = 256 * G
+    N = sum(ns_local)
+    flags = C.MOESHARD_FLAG_UNEVEN_TOKENS | getattr(C, f"MOESHARD_FLAG_{transport}")
+    layers = [MoEShardLayer(h, d_ff, E, max_tokens_per_rank=cap, dtype=torch.bfloat16, rank=r,
+                            world=G, flags=flags) for r in range(G)]
+    if transport == "P2P" and G > 1:
+        MoEShardLayer.p2p_connect_local(layers)
+    base = W.make_layer_inputs(61, N, h, d_ff, E, dtype=torch.bfloat16, routing="zipf")
+    for r, L in enumerate(layers):
+        c0, c1 = shard_columns(d_ff, G, r)
+        L.load_expert_shards(0, base.w_i[:, :, c0:c1].cuda(), base.w_o[:, c0:c1, :].cuda())
+    offs = np.cumsum((0,) + tuple(ns_local))
+    w_r = base.w_r.cuda()
+    for step in range(2):   # twice: slots / flags / epochs reused
+        xs = [base.x[offs[r]:offs[r + 1]].cuda().contiguous() for r in range(G)]
+        fs = [base.forced[offs[r]:offs[r + 1]].cuda().contiguous() for r in range(G)]
+        ys = [torch.empty_like(x) for x in xs]
+        if G == 1:
+            layers[0].forward(0, xs[0], w_r, forced_expert=fs[0], out=ys[0])
+        else:
+            for stage in (C.MOESHARD_STAGE_ROUTE, C.MOESHARD_STAGE_COMPUTE, C.MOESHARD_STAGE_REDUCE):
+                for r, L in enumerate(layers):
+                    L.forward(0, xs[r], w_r, forced_expert=fs[r], out=ys[r], stages=stage)
+        for L in layers:
+            L.check()
+        torch.cuda.synchronize()
+        y_ref, rt, counts, offsets, perm = O.moe_layer(base.x, base.w_r, base.w_i, base.w_o,
+                                                       forced=base.forced.numpy(), return_routing=True)
+        err = O.max_abs_rel(torch.cat(ys).float().cpu().numpy(), y_ref)
+        assert err <= BF16_TOL, f"step {step}: max-abs-rel {err:.3e}"
+        for L in layers:
+            r = {k: v.cpu().numpy() for k, v in L.routing(0).items()}
+            assert r["expert"].shape == (G * cap,)
+            real = np.concatenate([np.arange(g * cap, g * cap + ns_local[g]) for g in range(G)])
+            np.testing.assert_array_equal(r["expert"][real], rt.expert)
+            assert (r["expert"][np.setdiff1d(np.arange(G * cap), real)] == -1).all()
+            np.testing.assert_array_equal(r["counts"], counts)
+    for L in layers:
+        L.close()
