@@ -217,7 +217,7 @@ ENCODERS = {
 }
 
 
-def encoder_ttft(name, G, rank, local, barrier, dist, reps=10):
+def encoder_ttft(name, G, rank, local, barrier, dist, reps=10, oracle_sample=2048):
     """TTFT = one encoder forward over the batch, max over ranks:
     torch attention / dense FFN replicated data-parallel, MoE FFNs through the
     library. Also the MoE-layer share (TTFT_MoE) and the Zipf(1.2)-skewed TTFT."""
@@ -268,10 +268,24 @@ def encoder_ttft(name, G, rank, local, barrier, dist, reps=10):
     moe_only = run(lambda: [enc.moe.forward(j, y, enc.layers[i]["w_r"])
                             for j, i in enumerate(enc.moe_ids)])
     enc.moe.close()
-    return {"workload": title, "ttft_ms": ttft, "ttft_ms_zipf": ttft_skew,
-            "ttft_moe_ms": moe_only, "moe_layers": len(enc.moe_ids), "reps": reps,
-            "tokens": N, "note": "non-MoE blocks are torch (cuBLAS/SDPA) replicated on every rank; "
-                                 "MoE FFNs are libmoeshard; T5 relative bias omitted"}
+    res = {"workload": title, "ttft_ms": ttft, "ttft_ms_zipf": ttft_skew,
+           "ttft_moe_ms": moe_only, "moe_layers": len(enc.moe_ids), "reps": reps,
+           "tokens": N, "note": "non-MoE blocks are torch (cuBLAS/SDPA) replicated on every rank; "
+                                "MoE FFNs are libmoeshard; T5 relative bias omitted"}
+    if rank == 0 and oracle_sample > 0:
+        # the oracle's MoE part of the same encoder: one MoE layer timed on
+        # a sample of tokens on the host cores, extrapolated to N tokens x the MoE layers
+        import oracle
+        cfg_l = dict(E=cfg.n_experts, h=cfg.d_model, d_ff=cfg.d_ff, N=min(N, oracle_sample))
+        xo, wro, wio, woo = _oracle_weights(cfg_l, seed, dev)
+        t0 = time.perf_counter()
+        oracle.moe_layer(xo, wro, wio, woo)
+        dt = time.perf_counter() - t0
+        res["oracle_ttft_moe_ms_extrapolated"] = dt * 1e3 * (N / cfg_l["N"]) * len(enc.moe_ids)
+        res["oracle_sample"] = (f"one MoE layer on {cfg_l['N']} of {N} tokens, fp64 numpy oracle "
+                                f"({_blas_threads()} BLAS threads), x {N / cfg_l['N']:.0f} tokens "
+                                f"x {len(enc.moe_ids)} layers")
+    return res
 
 
 # ------------------------------------------------------------------ our arm
@@ -544,7 +558,8 @@ def main():
     if e2e is not None:
         line["e2e"] = e2e
     if args.encoder != "none":
-        line["encoder_ttft"] = encoder_ttft(args.encoder, G, rank, local, barrier, dist)
+        line["encoder_ttft"] = encoder_ttft(args.encoder, G, rank, local, barrier, dist,
+                                            oracle_sample=0 if args.no_cpu_baseline else 2048)
     if args.sustained > 0:
         # long run at the end: after ~50-100 ms of this load the board reaches its power
         # limit and sw_power_cap lowers SM clocks; reported, not the value
