@@ -1,16 +1,10 @@
 #!/bin/bash
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q --timeout 200 -p no:cacheprovider > gpurun_out/pytest_quick.log 2>&1; rc=$?; echo "pytest rc=$rc"; tail -3 gpurun_out/pytest_quick.log | grep -E "passed|failed"
-[ $rc -ne 0 ] && exit 1
-b() { timeout 300 python bench.py --steps 300 --warmup 20 --no-cpu-baseline --no-e2e --encoder none --sustained 0 > gpurun_out/ab.json 2>/dev/null
-  python -c "
-import json; d=json.load(open('gpurun_out/ab.json')); k=d['kernels_us']; print('$1 step', round(d['ms_per_step']*1e3,2), 'skew', round(d['skewed']['ms_per_step']*1e3,2), d['clocks']['sm_mhz'])"; }
-for rep in 1 2 3; do
-b "early"
-MOESHARD_GROUP_EARLY_LOADS=0 b "late"
-done
+MOESHARD_TC_VARIANT=22 timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -x -q --timeout 120 -p no:cacheprovider -k "c2_full or tcgen05_parity" 2>&1 | tail -1
 run() { timeout 200 python scripts/shape_probe.py $SHAPE 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', {r: (d[r]['step_us'], d[r]['phases_us']['gemm_up']) for r in ('uniform','zipf')})"; }
-for sh in "64 768 3072 8192 8" "128 1024 4096 32768 8"; do
-  SHAPE="$sh" run "[$sh] early"; SHAPE="$sh" MOESHARD_GROUP_EARLY_LOADS=0 run "[$sh] late"
+for rep in 1 2; do
+for sh in "128 1024 4096 32768 1 60" "64 768 3072 8192 1" "128 1024 4096 32768 8"; do
+  for v in 0 22 23 24; do SHAPE="$sh" MOESHARD_TC_VARIANT=$v run "[$sh] v$v"; done
+done
 done
