@@ -638,3 +638,43 @@ def test_uneven_tokens_per_rank(transport, ns_local):
             np.testing.assert_array_equal(r["counts"], counts)
     for L in layers:
         L.close()
+
+
+@pytest.mark.parametrize("routing", ["uniform", "zipf"])
+def test_p2p_g8_at_c2_full_size(routing):
+    """The north-star shape at G = 8 through the peer-memory transport: Switch-Base-64,
+    8192 tokens split over 8 ranks (1024 each), d_ff/G = 384 per rank, all eight ranks'
+    contexts, shards and regions on this GPU in lock-step stages. Routing tables exact
+    on every rank; the concatenated output vs the fp64 oracle of the unsharded layer."""
+    from paper_2503_08467_b200 import MoEShardLayer, shard_columns
+    from paper_2503_08467_b200 import moeshard as C
+    G, N, h, d_ff, E = 8, 8192, 768, 3072, 64
+    n = N // G
+    inp = W.make_layer_inputs(2, N, h, d_ff, E, dtype=torch.bfloat16, routing=routing, s=1.2)
+    layers = [MoEShardLayer(h, d_ff, E, max_tokens_per_rank=n, dtype=torch.bfloat16, rank=r,
+                            world=G, flags=C.MOESHARD_FLAG_P2P) for r in range(G)]
+    MoEShardLayer.p2p_connect_local(layers)
+    for r, L in enumerate(layers):
+        c0, c1 = shard_columns(d_ff, G, r)
+        L.load_expert_shards(0, inp.w_i[:, :, c0:c1].cuda(), inp.w_o[:, c0:c1, :].cuda())
+    xs = [inp.x[r * n:(r + 1) * n].cuda().contiguous() for r in range(G)]
+    fs = [inp.forced[r * n:(r + 1) * n].cuda().contiguous() for r in range(G)]
+    ys = [torch.empty_like(x) for x in xs]
+    w_r = inp.w_r.cuda()
+    for stage in (C.MOESHARD_STAGE_ROUTE, C.MOESHARD_STAGE_COMPUTE, C.MOESHARD_STAGE_REDUCE):
+        for r, L in enumerate(layers):
+            L.forward(0, xs[r], w_r, forced_expert=fs[r], out=ys[r], stages=stage)
+    for L in layers:
+        L.check()
+    torch.cuda.synchronize()
+    y_ref, rt, counts, offsets, perm = O.moe_layer(inp.x, inp.w_r, inp.w_i, inp.w_o,
+                                                   forced=inp.forced.numpy(), return_routing=True)
+    for L in layers:
+        r = {k: v.cpu().numpy() for k, v in L.routing(n).items()}
+        np.testing.assert_array_equal(r["expert"], rt.expert)
+        np.testing.assert_array_equal(r["counts"], counts)
+        np.testing.assert_array_equal(r["perm"], perm)
+    err = O.max_abs_rel(torch.cat(ys).float().cpu().numpy(), y_ref)
+    assert err <= BF16_TOL, f"max-abs-rel {err:.3e}"
+    for L in layers:
+        L.close()
