@@ -68,10 +68,22 @@ __global__ void __launch_bounds__(256) push_tokens(P2PArgs a, const uint4* __res
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   const RouteRec* my_route = reinterpret_cast<const RouteRec*>(a.self + a.off_route) + a.rank * nrec;
   const int32_t* my_hist = reinterpret_cast<const int32_t*>(a.self + a.off_hist) + a.rank * nh;
+  // token rows: 4 vectors per thread in flight, each read once and stored to every rank
+  constexpr int kU = 4;
+  for (size_t i0 = tid; i0 < nx; i0 += kU * stride) {
+    uint4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * stride < nx) v[u] = __ldg(x + i0 + u * stride);
+    for (int g = 0; g < a.world; ++g) {
+      uint4* dx = reinterpret_cast<uint4*>(a.peers[g] + a.off_x) + a.rank * sx;
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (i0 + u * stride < nx) dx[i0 + u * stride] = v[u];
+    }
+  }
   for (int g = 0; g < a.world; ++g) {
     char* peer = a.peers[g];
-    uint4* dx = reinterpret_cast<uint4*>(peer + a.off_x) + a.rank * sx;
-    for (size_t i = tid; i < nx; i += stride) dx[i] = __ldg(x + i);
     if (g != a.rank) {   // the router already wrote its own slot of route / hist
       RouteRec* dr = reinterpret_cast<RouteRec*>(peer + a.off_route) + a.rank * nrec;
       for (size_t i = tid; i < nrec; i += stride) dr[i] = my_route[i];
@@ -79,9 +91,11 @@ __global__ void __launch_bounds__(256) push_tokens(P2PArgs a, const uint4* __res
       for (size_t i = tid; i < nh; i += stride) dh[i] = my_hist[i];
     }
   }
-  __threadfence_system();
+  // bar.sync, then one system-scope fence by the counting thread (cumulative over the
+  // CTA's stores ordered before it by the barrier) instead of a fence in every thread
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence_system();
     int32_t* ctr = reinterpret_cast<int32_t*>(a.self) + 1;
     if (atomicAdd(ctr, 1) == static_cast<int>(gridDim.x) - 1) {   // every CTA's stores fenced
       *ctr = 0;
@@ -115,24 +129,41 @@ __global__ void __launch_bounds__(256) reduce_partials(P2PArgs a, int n, int row
   const size_t nv = static_cast<size_t>(n) * row_vecs;
   const size_t slot = static_cast<size_t>(a.n_max) * row_vecs;
   const uint4* recv = reinterpret_cast<const uint4*>(a.self + a.off_recv);
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nv;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int g = 0; g < a.world; ++g) {
-      const uint4 v = __ldcg(recv + g * slot + i);   // written by peers: bypass L1
-      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  constexpr int kU = 2;   // vectors per thread per pass; all G slots' loads of a pass in flight
+  for (size_t i0 = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i0 < nv;
+       i0 += kU * stride) {
+    float acc[kU][8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __bfloat1622float2(b[k]);
-        acc[2 * k] += f.x;
-        acc[2 * k + 1] += f.y;
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[u][k] = 0.f;
+    for (int g = 0; g < a.world; ++g) {   // ascending rank: a fixed summation order
+      uint4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (i0 + u * stride < nv) v[u] = __ldcg(recv + g * slot + i0 + u * stride);   // peers' writes: L2
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (i0 + u * stride >= nv) continue;
+        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(b[k]);
+          acc[u][2 * k] += f.x;
+          acc[u][2 * k + 1] += f.y;
+        }
       }
     }
-    uint4 o;
-    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) ob[k] = __floats2bfloat162_rn(acc[2 * k], acc[2 * k + 1]);
-    out[i] = o;
+    for (int u = 0; u < kU; ++u) {
+      if (i0 + u * stride >= nv) continue;
+      uint4 o;
+      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ob[k] = __floats2bfloat162_rn(acc[u][2 * k], acc[u][2 * k + 1]);
+      out[i0 + u * stride] = o;
+    }
   }
   // the last CTA out advances the epoch (every CTA has read it by now)
   __syncthreads();
@@ -177,7 +208,7 @@ cudaError_t launch_p2p_push(const P2PArgs& a, const void* x, int n, int ns, int 
                             int E, int num_sms, cudaStream_t s) {
   if (ns <= 0) return cudaSuccess;
   const size_t work = static_cast<size_t>(std::max(n, 1)) * row_vecs;
-  const int grid = static_cast<int>(std::min<size_t>(2 * num_sms, (work + 255) / 256));
+  const int grid = static_cast<int>(std::min<size_t>(4 * num_sms, (work + 1023) / 1024));
   return launch_pdl(push_tokens, dim3(std::max(grid, 1)), dim3(256), 0, s, a,
                     static_cast<const uint4*>(x), n, ns, row_vecs, nbr, E);
 }
@@ -196,7 +227,7 @@ cudaError_t launch_p2p_reduce(const P2PArgs& a, int n, int row_vecs, void* out, 
                               int num_sms, cudaStream_t s) {
   // runs even for n = 0 (uneven token counts): it consumes the flags and advances the epoch
   const size_t work = static_cast<size_t>(n) * row_vecs;
-  const int grid = static_cast<int>(std::min<size_t>(2 * num_sms, (work + 255) / 256));
+  const int grid = static_cast<int>(std::min<size_t>(4 * num_sms, (work + 511) / 512));
   reduce_partials<<<std::max(grid, 1), 256, 0, s>>>(a, n, row_vecs, static_cast<uint4*>(out), err);
   return cudaGetLastError();
 }
