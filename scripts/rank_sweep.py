@@ -1,0 +1,77 @@
+"""Per-rank compute time of a G-GPU MoEShard layer, measured on ONE GPU (CUDA-graph replay,
+weights rotated past L2): what every rank computes after the AllGather - router on its
+n = N/G tokens, Step 2 and both grouped products over all N tokens on its d_ff/G shard -
+for the BASELINE layer configs at G = 1, 2, 4, 8, uniform and Zipf(1.2) routing. The
+exchange steps are NOT run (one GPU); the JSON adds the NVLink bytes per rank and their
+time at the 770 GB/s measured peer bandwidth so a reader can bound the G > 1 layer time.
+usage: python scripts/rank_sweep.py > profiles/r01_rank_sweep.json"""
+import json, math, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import workload as W
+from paper_2503_08467_b200 import MoEShardLayer, shard_columns
+
+CFGS = {"c2": (64, 768, 3072, 8192), "c3": (128, 768, 3072, 16384), "c5": (128, 1024, 4096, 32768)}
+PEER_GBS = 770.0
+
+
+def per_rank(E, h, d_ff, N, G, steps=60):
+    F = d_ff // G
+    NW = max(1, math.ceil(3 * 126 * 2**20 / (2 * E * h * F * 2)))
+    L = MoEShardLayer(h, F, E, n_layers=NW, max_tokens_per_rank=N, dtype=torch.bfloat16)
+    c0, c1 = shard_columns(d_ff, G, 0)
+    for j in range(NW):
+        wi, wo = W.make_expert_weights(2, E, h, d_ff, cols=(c0, c1), device="cuda", layer=j % 3)
+        L.load_expert_shards(j, wi, wo)
+        del wi, wo
+    x = W.make_tokens(2, N, h, device="cuda")
+    w_r = W.make_router_weight(2, h, E, device="cuda")
+    out = torch.empty_like(x)
+    res = {}
+    for routing in ("uniform", "zipf"):
+        f = W.draw_experts(2, N, E, routing, device="cuda")
+        fwd = lambda k: L.forward(k % NW, x, w_r, forced_expert=f, out=out)
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            for k in range(NW + 3):
+                fwd(k)
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for k in range(NW):
+                fwd(k)
+        reps = max(1, steps // NW)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            g.replay()
+        e.record()
+        torch.cuda.synchronize()
+        res[routing] = round(s.elapsed_time(e) / (reps * NW) * 1e3, 2)
+    L.close()
+    return res
+
+
+def main():
+    out = {"note": "per-rank compute only (router over all N tokens, i.e. an upper bound of the "
+                   "rank's n = N/G router work); nvlink_us = (G-1)/G * N * h * 2 B * 2 (AllGather "
+                   "+ ReduceScatter, bf16) / 770 GB/s", "configs": {}}
+    for name, (E, h, d_ff, N) in CFGS.items():
+        rows = {}
+        for G in (1, 2, 4, 8):
+            t = per_rank(E, h, d_ff, N, G)
+            nv = (G - 1) / G * N * h * 2 * 2 / (PEER_GBS * 1e3)
+            rows[G] = {"compute_us": t, "nvlink_us": round(nv, 2),
+                       "tokens_per_s_compute_only": {r: round(N / v * 1e6) for r, v in t.items()}}
+            print(name, G, rows[G], file=sys.stderr, flush=True)
+        out["configs"][name] = {"E": E, "h": h, "d_ff": d_ff, "N": N, "by_G": rows}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
