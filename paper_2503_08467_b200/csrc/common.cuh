@@ -65,6 +65,22 @@ __host__ __device__ __forceinline__ void tc_chunking(int n_e, int* n_chunks, int
   *n_chunks = ceil_div(n_e, cs);
 }
 
+// Kernel attributes (cudaFuncSetAttribute) are per device: a call site records the
+// devices it has configured (a process may drive several GPUs; a repeat is harmless).
+struct PerDeviceOnce {
+  unsigned long long mask = 0ull;
+  bool need() const {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d >= 64 || !((__atomic_load_n(&mask, __ATOMIC_ACQUIRE) >> d) & 1ull);
+  }
+  void done() {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d < 64) __atomic_fetch_or(&mask, 1ull << d, __ATOMIC_RELEASE);
+  }
+};
+
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while the previous kernel in the stream drains; it must call
 // griddepcontrol.wait before touching memory the predecessor writes or reads.

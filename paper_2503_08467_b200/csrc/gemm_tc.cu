@@ -1145,13 +1145,13 @@ size_t smem_bytes(int E, int as, int bs) {
 template <bool kDown, int AS, int BS, int kMode = 0>
 cudaError_t launch_v(const CUtensorMap& tmB, const TcParams& p, int grid, cudaStream_t s) {
   const size_t sm = smem_bytes(p.E, AS, BS);
-  static bool attr_set = false;  // per template instance; the library is single-device
-  if (!attr_set) {
+  static PerDeviceOnce attr;  // per template instance and device
+  if (attr.need()) {
     cudaError_t e = cudaFuncSetAttribute(tc_grouped_gemm<kDown, AS, BS, kMode>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem_bytes(kMaxExperts, AS, BS)));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr.done();
   }
   tc_grouped_gemm<kDown, AS, BS, kMode><<<grid, kThreads, sm, s>>>(tmB, p);
   return cudaGetLastError();
@@ -1176,13 +1176,13 @@ size_t smem_bytes_2sm(int E, int as, int bs) {
 template <bool kDown, int AS, int BS, bool kT = false>
 cudaError_t launch_2sm(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcParams& p, int grid,
                        cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static PerDeviceOnce attr;
+  if (attr.need()) {
     cudaError_t e = cudaFuncSetAttribute(tc_grouped_gemm_2sm<kDown, AS, BS, kT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem_bytes_2sm(kMaxExperts, AS, BS)));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr.done();
   }
   tc_grouped_gemm_2sm<kDown, AS, BS, kT><<<grid & ~1, kThreads, smem_bytes_2sm(p.E, AS, BS), s>>>(
       tmA, tmB, p);
@@ -1220,13 +1220,13 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                          const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn, const TcParams& up,
                          const TcParams& dn, int32_t* done, const void* cp_src, void* cp_dst,
                          int cp_row_vecs, bool dynamic, int grid, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static PerDeviceOnce attr;
+  if (attr.need()) {
     cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS, KA, kT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem_bytes_2sm(kMaxExperts, AS * KA, BS * KA)));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr.done();
   }
   static const bool inter = [] {   // opt-in: measured slower for C2 / C5, faster for C3 only
     const char* e = getenv("MOESHARD_FFN_INTERLEAVE");

@@ -576,8 +576,8 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
   const auto* pfb = static_cast<const uint8_t*>(pf);
   if (pf == nullptr || pf_bytes < 16384) pf_ctas = 0;
   if (n <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  if (attr.need()) {
     cudaError_t e = cudaFuncSetAttribute(router_tc_kernel<true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          RTC_SMEM_BUDGET + 2048);  // >= router_tc_smem_bytes(any EP)
@@ -585,7 +585,7 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
       e = cudaFuncSetAttribute(router_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                RTC_SMEM_BUDGET + 2048);  // >= router_tc_smem_bytes(any EP)
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.done();
   }
   const RouteGroupArgs none{};
   static const bool timing = getenv("MOESHARD_ROUTER_TIMING") != nullptr;
@@ -614,13 +614,13 @@ cudaError_t launch_route_group_tc(const CUtensorMap& tmX, const CUtensorMap& tmW
                                   cudaStream_t s) {
   const int tok = 128;
   if (n <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  if (attr.need()) {
     cudaError_t e = cudaFuncSetAttribute(router_tc_kernel<true, false, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          RTC_SMEM_BUDGET + 2048);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.done();
   }
   static const bool timing = getenv("MOESHARD_ROUTER_TIMING") != nullptr;
   if (timing) {
