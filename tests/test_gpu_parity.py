@@ -678,3 +678,38 @@ def test_p2p_g8_at_c2_full_size(routing):
     assert err <= BF16_TOL, f"max-abs-rel {err:.3e}"
     for L in layers:
         L.close()
+
+
+# --------------------------------------------------------------------- fp32 validation mode at scale
+@pytest.mark.parametrize("flags", [0, "FORCE_COLLECTIVES"])
+def test_fp32_validation_mode_c2_shape(flags):
+    """The fp32 validation mode (CUDA-core FFMA, fp32 partials) at the C2 layer shape - 8192
+    tokens, E = 64, h = 768, d_ff = 3072 - with the natural router: outputs within 1e-4 of the
+    fp64 oracle (BASELINE.json), routing exact wherever the fp64 top-2 gap is unambiguous;
+    also through the NCCL exchange (one rank), which then reduces fp32 partials."""
+    from paper_2503_08467_b200 import moeshard as C
+    f = getattr(C, f"MOESHARD_FLAG_{flags}") if flags else 0
+    inp = W.make_layer_inputs(2, 8192, 768, 3072, 64, dtype=torch.float32, routing="natural")
+    L, y, r = _run(inp, dtype=torch.float32, flags=f)
+    err = _check_layer(inp, y, r, tol=FP32_TOL)
+    print(f"fp32 C2 max-abs-rel {err:.2e}")
+    L.close()
+
+
+def test_staged_forward_protocol_errors():
+    """moeshard_forward_stages: a COMPUTE stage whose n_local differs from its ROUTE stage,
+    or an empty stage mask, is refused with PROTOCOL / INVALID_ARG (no kernels run)."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200 import moeshard as C
+    inp = W.make_layer_inputs(71, 256, 128, 256, 8, dtype=torch.bfloat16, routing="uniform")
+    L = MoEShardLayer(128, 256, 8, max_tokens_per_rank=256, dtype=torch.bfloat16)
+    L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
+    x, w_r = inp.x.cuda(), inp.w_r.cuda()
+    L.forward(0, x, w_r, stages=C.MOESHARD_STAGE_ROUTE)
+    with pytest.raises(C.MoEShardError, match="PROTOCOL"):
+        L.forward(0, x[:100].contiguous(), w_r, stages=C.MOESHARD_STAGE_COMPUTE)
+    with pytest.raises(C.MoEShardError, match="INVALID_ARG"):
+        L.forward(0, x, w_r, stages=0)
+    L.forward(0, x, w_r, stages=C.MOESHARD_STAGE_COMPUTE | C.MOESHARD_STAGE_REDUCE)
+    L.check()
+    L.close()
