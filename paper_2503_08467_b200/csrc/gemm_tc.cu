@@ -636,6 +636,7 @@ struct FusedParams {
   int cp_row_vecs = 0;
   bool interleave = false;  // expert-group blocks (MOESHARD_FFN_INTERLEAVE=1); default all up, then all down
   bool dynamic = false;     // units taken from a global counter in list order (MOESHARD_FLAG_DYNAMIC_SCHED)
+  int sibling_policy = 1;   // weight tiles of multi-chunk experts: 0 evict_first, 1 normal, 2 evict_last
   bool light_release = true;  // H hand-off: bar.sync + one release (MOESHARD_LIGHT_RELEASE=0: + per-thread fences)
 };
 
@@ -871,7 +872,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 0) {
     // -------------------------------------------------------------- weight producer (both CTAs)
-    const uint64_t pol_w = policy_evict_first();
+    // weight tiles are streamed once (evict_first) - except an expert's tiles when it has
+    // several token chunks: its sibling units read the same tile at nearly the same time,
+    // and evict_first would let the trailing reader miss L2 and re-read it from DRAM
+    const uint64_t pol_once = policy_evict_first();
+    const uint64_t pol_shared = fp.sibling_policy == 2 ? policy_evict_last()
+                                : fp.sibling_policy == 1 ? policy_evict_normal() : pol_once;
     const uint32_t leader_full = mapa_shared(smem_u32(fullA), 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -884,6 +890,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const CUtensorMap* tm = down ? &tmA_dn : &tmA_up;
       const int mt = min(2 * w.mt + static_cast<int>(rank), n_mt - 1);
       const int row0 = ((w.e * n_mt + mt) * nkb * KA) * BM;
+      const uint64_t pol_w = (s_pref[w.e + 1] - s_pref[w.e] > 1) ? pol_shared : pol_once;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&emptyA[stage], phase ^ 1);
         const uint32_t fb = leader_full + stage * 8;
@@ -1232,6 +1239,10 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
     const char* e = getenv("MOESHARD_FFN_INTERLEAVE");
     return e && e[0] == '1';
   }();
+  static const int sib = [] {   // MOESHARD_SIBLING_POLICY=first|normal|last (A/B)
+    const char* e = getenv("MOESHARD_SIBLING_POLICY");
+    return e ? (e[0] == 'f' ? 0 : e[0] == 'l' ? 2 : 1) : 1;
+  }();
   static const bool light = [] {
     const char* e = getenv("MOESHARD_LIGHT_RELEASE");
     return !(e && e[0] == '0');
@@ -1241,7 +1252,7 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
     return e ? (e[0] == 'd' ? 1 : 0) : -1;
   }();
   FusedParams fp{up, dn, done, static_cast<const uint4*>(cp_src), static_cast<uint4*>(cp_dst),
-                 cp_row_vecs, inter, dyn_env >= 0 ? dyn_env == 1 : dynamic, light};
+                 cp_row_vecs, inter, dyn_env >= 0 ? dyn_env == 1 : dynamic, sib, light};
   return launch_pdl(tc_moe_ffn_2sm<AS, BS, KA, kT>, dim3(grid & ~1), dim3(kThreads),
                     smem_bytes_2sm(up.E, AS * KA, BS * KA), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
 }

@@ -1,6 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-OURS='regex:router_tc|group_|tc_moe_ffn'
-timeout 900 ncu --set full --clock-control none --import-source on -k "$OURS" -s 8 -c 4 -o gpurun_out/prof_final_c2 python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-e2e --encoder none --sustained 0 > gpurun_out/ncu_final_c2.log 2>&1; echo "ncu c2 rc=$?"
-timeout 900 ncu --set full --clock-control none -k "regex:tc_moe_ffn" -s 2 -c 1 -o gpurun_out/prof_final_c5 python bench.py --config c5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --encoder none --sustained 0 > gpurun_out/ncu_final_c5.log 2>&1; echo "ncu c5 rc=$?"
+for pol in first normal; do
+MOESHARD_SIBLING_POLICY=$pol timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k "regex:tc_moe_ffn" -s 3 -c 2 --csv python bench.py --config c5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --encoder none --sustained 0 2>/dev/null | grep -E "tc_moe" | awk -F'","' -v p=$pol '{print p, $(NF-2), $NF}'
+MOESHARD_SIBLING_POLICY=$pol timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k "regex:tc_moe_ffn" -s 3 -c 2 --csv python scripts/shape_probe.py 64 768 3072 8192 1 3 2>/dev/null | grep -E "tc_moe" | tail -6 | awk -F'","' -v p=$pol '{print "c2probe", p, $(NF-2), $NF}'
+done
