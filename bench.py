@@ -439,6 +439,22 @@ def main():
     e_active_u = int((counts > 0).sum())
     max_tok_u = int(counts.max())
 
+    # --- skewed routing (Zipf 1.2, paper's replaced-router hook), right after the main
+    # region with its own clock samples, then uniform and skewed blocks interleaved so that
+    # clock / power drift over the run cancels in their ratio
+    clk_skew = ClockSampler(local)
+    ms_skew = timed(fwd_skew, args.steps, args.warmup, sampler=clk_skew)
+    counts_z = layer.routing(n)["counts"].cpu()
+    st_skew = layer.stats()
+    blk = max(10, args.steps // 4)
+    ratios = []
+    for _ in range(4):
+        a = timed(fwd, blk, 3)
+        b = timed(fwd_skew, blk, 3)
+        ratios.append(b / a)
+    ratios.sort()
+    skew_interleaved = round(0.5 * (ratios[1] + ratios[2]), 4)
+
     # --- per-step distribution (event pair around every step, separate pass) and the
     # eager-launch time of the same loop (median / p10 / p90, eager and graph)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -455,10 +471,6 @@ def main():
                "note": "per-step event pairs, separate pass (includes ~1-2 us event overhead)"}
     ms_eager = timed(fwd_eager, args.steps, args.warmup) if not args.eager else ms
 
-    # --- skewed routing (Zipf 1.2, paper's replaced-router hook)
-    ms_skew = timed(fwd_skew, args.steps, args.warmup)
-    counts_z = layer.routing(n)["counts"].cpu()
-    st_skew = layer.stats()
 
     # --- per-kernel phase times (separate eager pass, phase events on the launch stream)
     layer.profile(True)
@@ -552,6 +564,8 @@ def main():
                             "tiles_up": st_uniform["tiles_up"], "tiles_down": st_uniform["tiles_down"]},
         "skewed": {"routing": "Zipf(s=1.2) forced", "value": N / (ms_skew * 1e-3),
                    "ms_per_step": ms_skew, "skew_over_uniform_time": round(ms_skew / ms, 4),
+                   "skew_over_uniform_interleaved": skew_interleaved,
+                   "clocks": clk_skew.summary(),
                    "experts_active": int((counts_z > 0).sum()),
                    "max_tokens_per_expert": int(counts_z.max()),
                    "tiles_up": st_skew["tiles_up"], "tiles_down": st_skew["tiles_down"]},

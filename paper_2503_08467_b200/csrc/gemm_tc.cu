@@ -637,6 +637,7 @@ struct FusedParams {
   bool interleave = false;  // expert-group blocks (MOESHARD_FFN_INTERLEAVE=1); default all up, then all down
   bool dynamic = false;     // units taken from a global counter in list order (MOESHARD_FLAG_DYNAMIC_SCHED)
   int sibling_policy = 1;   // weight tiles of multi-chunk experts: 0 evict_first, 1 normal, 2 evict_last
+  int xpol = 2, hpol = 2;   // X_perm / H reads: 0 evict_first, 1 normal, 2 evict_last
   bool light_release = true;  // H hand-off: bar.sync + one release (MOESHARD_LIGHT_RELEASE=0: + per-thread fences)
 };
 
@@ -908,7 +909,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 3) {
     // -------------------------------------------------------------- token producer (both CTAs)
-    const uint64_t pol_x = policy_evict_last();
+    // L2 policies of the activation reads (A/B knobs): X_perm rows (re-read by the up units'
+    // feature pair-tiles at nearly the same time) and H rows (read by the down units)
+    auto make_pol = [](int k) {
+      return k == 0 ? policy_evict_first() : k == 1 ? policy_evict_normal() : policy_evict_last();
+    };
+    const uint64_t pol_xp = make_pol(fp.xpol), pol_h = make_pol(fp.hpol);
     const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
     int* s_rows = reinterpret_cast<int*>(
         (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2;
@@ -940,6 +946,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
       const int nkb = down ? nkb_dn : nkb_up;
       const CUtensorMap* tm = down ? &tmB_dn : &tmB_up;
+      const uint64_t pol_x = down ? pol_h : pol_xp;
       if (down && npend > 0) drain();
       if (!down && fp.cp_src != nullptr) {   // this expert's rows copied into X_perm? (acquire)
         const int target = (s_end[w.e] - s_off[w.e] + 7) / 8;
@@ -1243,6 +1250,14 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
     const char* e = getenv("MOESHARD_SIBLING_POLICY");
     return e ? (e[0] == 'f' ? 0 : e[0] == 'l' ? 2 : 1) : 1;
   }();
+  static const int xpol = [] {   // MOESHARD_XPOL / MOESHARD_HPOL = first|normal|last (A/B)
+    const char* e = getenv("MOESHARD_XPOL");
+    return e ? (e[0] == 'f' ? 0 : e[0] == 'n' ? 1 : 2) : 2;
+  }();
+  static const int hpol = [] {
+    const char* e = getenv("MOESHARD_HPOL");
+    return e ? (e[0] == 'f' ? 0 : e[0] == 'n' ? 1 : 2) : 2;
+  }();
   static const bool light = [] {
     const char* e = getenv("MOESHARD_LIGHT_RELEASE");
     return !(e && e[0] == '0');
@@ -1252,7 +1267,7 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
     return e ? (e[0] == 'd' ? 1 : 0) : -1;
   }();
   FusedParams fp{up, dn, done, static_cast<const uint4*>(cp_src), static_cast<uint4*>(cp_dst),
-                 cp_row_vecs, inter, dyn_env >= 0 ? dyn_env == 1 : dynamic, sib, light};
+                 cp_row_vecs, inter, dyn_env >= 0 ? dyn_env == 1 : dynamic, sib, xpol, hpol, light};
   return launch_pdl(tc_moe_ffn_2sm<AS, BS, KA, kT>, dim3(grid & ~1), dim3(kThreads),
                     smem_bytes_2sm(up.E, AS * KA, BS * KA), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
 }

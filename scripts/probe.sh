@@ -1,7 +1,12 @@
 #!/bin/bash
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-timeout 1200 python -m pytest tests -m gpu -q --timeout 400 -p no:cacheprovider > gpurun_out/pytest_all.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_all.log
-timeout 600 python bench.py > gpurun_out/bench_r01g.json 2> gpurun_out/bench_r01g.err; echo "bench rc=$?"
-timeout 900 python bench.py --config c5 --steps 100 --warmup 10 --no-e2e --encoder c5 --sustained 0 > gpurun_out/bench_c5g.json 2> gpurun_out/bench_c5g.err; echo "c5 rc=$?"
-timeout 600 python bench.py --config c3 --steps 200 --warmup 20 --no-e2e --encoder none --sustained 0 > gpurun_out/bench_c3g.json 2> gpurun_out/bench_c3g.err; echo "c3 rc=$?"
+run() { timeout 200 python scripts/shape_probe.py $SHAPE 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', {r: (d[r]['step_us'], d[r]['phases_us']['gemm_up']) for r in ('uniform','zipf')})"; }
+for rep in 1 2; do
+for sh in "64 768 3072 8192 1" "128 768 3072 16384 1" "128 1024 4096 32768 1 60"; do
+  SHAPE="$sh" run "[$sh] x=last h=last"
+  SHAPE="$sh" MOESHARD_XPOL=normal run "[$sh] x=normal h=last"
+  SHAPE="$sh" MOESHARD_HPOL=first run "[$sh] x=last h=first"
+  SHAPE="$sh" MOESHARD_XPOL=normal MOESHARD_HPOL=first run "[$sh] x=normal h=first"
+done
+done
