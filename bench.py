@@ -546,7 +546,9 @@ def main():
     t_hbm = (e_active_u * 2 * h * F * 2 + N * h * 2 + N * h * 2) / (hbm * 1e9) * 1e6
     t_nv = (G - 1) / G * N * h * 4 / 770e9 * 1e6 if G > 1 else 0.0
     roof3 = max(t_tc, t_hbm, t_nv)
-    layer_roof = {"T_tc_us": round(t_tc, 2), "T_hbm_us": round(t_hbm, 2), "T_nv_us": round(t_nv, 2),
+    layer_roof = {"T_tc_us": round(t_tc, 2),
+                  "T_tc_sustained_us": round(4 * N * h * F / (tf_sust * 1e12) * 1e6, 2),
+                  "T_hbm_us": round(t_hbm, 2), "T_nv_us": round(t_nv, 2),
                   "roof_us": round(roof3, 2), "roof_ns_us": round(max(t_tc, t_nv), 2),
                   "frac": round(roof3 / (ms * 1e3), 4),
                   "note": "roof = max(T_tc at bf16 burst peak, T_hbm weights+x+out at measured HBM, "
@@ -570,6 +572,10 @@ def main():
                    "max_tokens_per_expert": int(counts_z.max()),
                    "tiles_up": st_skew["tiles_up"], "tiles_down": st_skew["tiles_down"]},
         "roofline": roofline,
+        "tensor_frac": {"burst": round(4 * N * h * F / (ms * 1e-3) / (tf_burst * 1e12), 4),
+                        "sustained": round(4 * N * h * F / (ms * 1e-3) / (tf_sust * 1e12), 4),
+                        "note": "layer FLOPs (both products) / layer time vs the measured bf16 "
+                                "peaks - the layer is HBM-bound, this is context, not a target"},
         "layer_roofline": layer_roof,
         "kernels_us": kernels,
         "gpu_launches": launches,
