@@ -118,8 +118,9 @@ int moeshard_workspace_size(const moeshard_config* cfg, int world, size_t* bytes
 int moeshard_weight_storage_size(const moeshard_config* cfg, int world, size_t* bytes_per_layer);
 
 /* Create a context for `rank` of `world` on CUDA `device`.
- * uid: [host] 128 bytes from moeshard_get_unique_id (ignored when world == 1
- *      without FORCE_COLLECTIVES; may be NULL then).
+ * uid: [host] 128 bytes from moeshard_get_unique_id (ignored - may be NULL - when
+ *      no NCCL communicator is needed: world == 1 without FORCE_COLLECTIVES, or
+ *      MOESHARD_FLAG_P2P).
  * workspace: [dev] caller-owned, >= moeshard_workspace_size bytes, 256-B
  *      aligned, must stay alive until moeshard_destroy.
  * Errors: DIVISIBILITY (d_ff % world), CONFIG (shape limits, device not
