@@ -1,20 +1,24 @@
 // moeshard.cu - host orchestrator behind the C ABI (include/moeshard.h).
 //
 // Owns: the context, the carve-up of the caller's workspace, the per-layer
-// K-major weight views and their TMA descriptors, and (world > 1) an NCCL
-// communicator (libnccl is dlopen'ed; with torch loaded this is the same
-// library torch.distributed uses). moeshard_forward enqueues Alg. 1
-// on the caller's stream:
+// packed weight tiles and their TMA descriptors, and either an NCCL
+// communicator (world > 1; libnccl is dlopen'ed - with torch loaded this is the
+// same library torch.distributed uses) or, with MOESHARD_FLAG_P2P, one exchange
+// region mapped by every rank (p2p.cu). moeshard_forward(_stages) enqueues
+// Alg. 1 on the caller's stream, kernels chained with
+// programmatic dependent launch:
 //
-//   1 router kernel (local tokens)                          Step 1
-//   2 ncclGroup{ AllGather(tokens), AllGather(route recs) }  Steps 2+3 (metadata folded
-//                                                           into the token exchange)
-//   3 group_scatter_gather (router-emitted per-block         Step 2 grouping + Sec. 3.3
-//     histograms -> offsets, stable perm, X_perm)
-//                                                           cross-GPU per-expert concat
-//   4 grouped GEMM up (+ReLU), grouped GEMM down (+gate,    Step 4 (Sec. 3.3 fusion)
-//     +un-permute scatter)
-//   5 ncclReduceScatter(sum)                                Step 5 gather + aggregateTokens
+//   ROUTE    1 router_tc_kernel (local tokens: logits, softmax, top-1, block    Step 1
+//              histograms)
+//            2 ncclGroup{AllGather tokens, route records, histograms} or       Steps 2+3
+//              push_tokens into every rank's region (P2P)
+//   COMPUTE  3 group_block_scan + group_scatter_gather (offsets, stable perm,  Step 2 + Sec. 3.3
+//              X_perm)                                                         concatenation
+//            4 tc_moe_ffn_2sm: both grouped products in one persistent launch  Step 4
+//              (ReLU; gate + un-permute scatter; P2P: partial rows stored into
+//              their owner's receive slot)
+//   REDUCE   5 ncclReduceScatter(sum), or reduce_partials over the receive     Step 5
+//              slots (P2P)
 //
 // No host synchronisation and no allocation inside forward.
 #include <cuda.h>
