@@ -638,6 +638,7 @@ struct FusedParams {
   bool dynamic = false;     // units taken from a global counter in list order (MOESHARD_FLAG_DYNAMIC_SCHED)
   int sibling_policy = 1;   // weight tiles of multi-chunk experts: 0 evict_first, 1 normal, 2 evict_last
   int xpol = 2, hpol = 2;   // X_perm / H reads: 0 evict_first, 1 normal, 2 evict_last
+  bool early_tables = false; // tables via a release flag from the grouping launch's CTA 0 (see kernel)
   bool light_release = true;  // H hand-off: bar.sync + one release (MOESHARD_LIGHT_RELEASE=0: + per-thread fences)
 };
 
@@ -733,8 +734,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   cluster_sync_all();
   if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
-  // PDL: everything above overlapped the grouping kernel's tail
-  griddep_wait();
+  // PDL: everything above overlapped the grouping kernel's tail. early_tables: the
+  // grouping launch's CTA 0 publishes the segment tables (release on tb.stats[6]) before
+  // it copies its rows, so only the roles that read X_perm / perm / route wait for the
+  // whole grid (griddepcontrol.wait below); the weight producer starts right away.
+  if (fp.early_tables) {
+    if (threadIdx.x == 0) {
+      uint32_t it = 0;
+      while (ld_acquire_gpu(fp.up.tb.stats + 6) == 0) {
+        if (++it > (1u << 24)) {   // never published: fall back to the grid dependency
+          griddep_wait();
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  } else {
+    griddep_wait();
+  }
   for (int i = threadIdx.x; i <= E; i += kThreads) {
     s_pref[i] = fp.up.tb.tc_chunk_pref[i];
     s_off[i] = fp.up.tb.pos[i];
@@ -915,6 +933,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       return k == 0 ? policy_evict_first() : k == 1 ? policy_evict_normal() : policy_evict_last();
     };
     const uint64_t pol_xp = make_pol(fp.xpol), pol_h = make_pol(fp.hpol);
+    if (fp.early_tables) griddep_wait();   // X_perm rows and the route records are complete
     const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
     int* s_rows = reinterpret_cast<int*>(
         (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2;
@@ -1110,6 +1129,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
     const uint64_t pol_keep = policy_evict_last();
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
+    if (fp.early_tables) griddep_wait();   // perm / route of the grouping launch
     int as = 0;
     uint32_t aphase = 0;
     for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
@@ -1233,7 +1253,7 @@ template <int AS, int BS, int KA, bool kT = false>
 cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                          const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn, const TcParams& up,
                          const TcParams& dn, int32_t* done, const void* cp_src, void* cp_dst,
-                         int cp_row_vecs, bool dynamic, int grid, cudaStream_t s) {
+                         int cp_row_vecs, bool dynamic, bool early_tables, int grid, cudaStream_t s) {
   static PerDeviceOnce attr;
   if (attr.need()) {
     cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS, KA, kT>,
@@ -1267,7 +1287,8 @@ cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
     return e ? (e[0] == 'd' ? 1 : 0) : -1;
   }();
   FusedParams fp{up, dn, done, static_cast<const uint4*>(cp_src), static_cast<uint4*>(cp_dst),
-                 cp_row_vecs, inter, dyn_env >= 0 ? dyn_env == 1 : dynamic, sib, xpol, hpol, light};
+                 cp_row_vecs, inter, dyn_env >= 0 ? dyn_env == 1 : dynamic, sib, xpol, hpol,
+                 early_tables && cp_src == nullptr, light};
   return launch_pdl(tc_moe_ffn_2sm<AS, BS, KA, kT>, dim3(grid & ~1), dim3(kThreads),
                     smem_bytes_2sm(up.E, AS * KA, BS * KA), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
 }
@@ -1277,16 +1298,16 @@ cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
                               const TcParams& up, const TcParams& dn, int32_t* done,
                               const void* cp_src, void* cp_dst, int cp_row_vecs, bool dynamic,
-                              int grid, cudaStream_t s) {
+                              bool early_tables, int grid, cudaStream_t s) {
   // MOESHARD_TC_VARIANT 20: two k-atoms per ring stage (3 + 3 stages of 32 KB)
   if (variant() == 21)
     return launch_fused<6, 6, 1, true>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src,
-                                       cp_dst, cp_row_vecs, dynamic, grid, s);
+                                       cp_dst, cp_row_vecs, dynamic, early_tables, grid, s);
   if (variant() == 20 && up.K % 128 == 0 && dn.K % 128 == 0 && !up.gather_cp)
     return launch_fused<3, 3, 2>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src, cp_dst,
-                                 cp_row_vecs, dynamic, grid, s);
+                                 cp_row_vecs, dynamic, early_tables, grid, s);
   return launch_fused<6, 6, 1>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src, cp_dst,
-                               cp_row_vecs, dynamic, grid, s);
+                               cp_row_vecs, dynamic, early_tables, grid, s);
 }
 
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,

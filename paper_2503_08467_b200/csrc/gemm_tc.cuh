@@ -99,7 +99,7 @@ cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
                               const TcParams& up, const TcParams& dn, int32_t* done,
                               const void* cp_src, void* cp_dst, int cp_row_vecs, bool dynamic,
-                              int grid, cudaStream_t s);
+                              bool early_tables, int grid, cudaStream_t s);
 
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const CUtensorMap& tmB2, const TcParams& p, int grid, cudaStream_t s);

@@ -202,6 +202,8 @@ struct moeshard_ctx {
   long long pf_bytes = 0;  // experimental L2 weight prefetch during routing (MOESHARD_L2_PREFETCH_MB)
   int gather_depth = 4;    // cp.async gather: stages in flight (MOESHARD_GATHER_DEPTH, 1..5)
   int router_tok = 128;    // tokens per tcgen05 router CTA (MOESHARD_ROUTER_TOK: 64 or 128)
+  bool early_tables = true;   // FFN weight stream starts on the grouping launch's table flag
+                              // (MOESHARD_EARLY_TABLES=0: whole-grid dependency)
   // phase profiling (measurement only)
   bool prof = false;
   static constexpr int kRing = 1024, kEv = 7;
@@ -366,6 +368,7 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->use_tc = cfg->dtype == MOESHARD_BF16 && !(c->cfg.flags & MOESHARD_FLAG_SIMT_GEMM);
   if (const char* pf = getenv("MOESHARD_L2_PREFETCH_MB")) c->pf_bytes = atoll(pf) << 20;
   if (c->cfg.flags & MOESHARD_FLAG_ROUTER_TOK64) c->router_tok = 64;
+  if (const char* et = getenv("MOESHARD_EARLY_TABLES")) c->early_tables = atoi(et) != 0;
   if (const char* rt = getenv("MOESHARD_ROUTER_TOK")) c->router_tok = atoi(rt) == 64 ? 64 : 128;
   if (const char* gd = getenv("MOESHARD_GATHER_DEPTH")) c->gather_depth = std::max(1, std::min(5, atoi(gd)));
   // L2 set-aside for the kernels' evict_last lines (H between the two products, the
@@ -685,7 +688,10 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
       CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather && !gather_cp ? tm_xg : c->tm_xperm16,
                                     lw.tm_out, ht ? c->tm_Ht : c->tm_H16, up, dn, c->tb.done,
                                     copy_in_ffn ? x_all : nullptr, c->x_perm, h * c->elt / 16,
-                                    (c->cfg.flags & MOESHARD_FLAG_DYNAMIC_SCHED) != 0, c->num_sms, s));
+                                    (c->cfg.flags & MOESHARD_FLAG_DYNAMIC_SCHED) != 0,
+                                    c->early_tables && !route_group && !gather &&
+                                        !(c->cfg.flags & MOESHARD_FLAG_FUSED_SCAN) && n > 0,
+                                    c->num_sms, s));
       c->mark(4, s);
       c->launches += 1;
       if (c->p2p) {

@@ -178,6 +178,10 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   __syncthreads();
   segment_tables<kThreads>(E, s_tot, s_pre, s_base, s_bpad, s_warp, blockIdx.x == 0, tb,
                            n_mt_up_tc, n_mt_down_tc);
+  if (blockIdx.x == 0) {   // the tables are out: the FFN's weight stream may start (early_tables)
+    __syncthreads();
+    if (threadIdx.x == 0) ptx::st_release_gpu(tb.stats + 6, 1);
+  }
   // 2. stable ranks inside the block
   if (warp < 4) {
     const unsigned peers = __match_any_sync(0xffffffffu, e);

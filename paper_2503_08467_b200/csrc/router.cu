@@ -404,6 +404,9 @@ __global__ void __launch_bounds__(256, 1)
   // PDL: x may come from the previous kernel, and the previous forward's FFN
   // still reads the route records this kernel overwrites
   griddep_wait();
+  // the previous forward's FFN is done with the "tables published" flag (tb.stats[6],
+  // = err_flag + 3): clear it for this forward's grouping launch to set
+  if (blockIdx.x == 0 && threadIdx.x == 0) err_flag[3] = 0;
   // kGroup: only after the first grid barrier (every CTA of this grid resident),
   // else the dependent FFN's CTAs could take the SMs a not-yet-running CTA needs
   if (!kGroup) griddep_launch_dependents();
