@@ -34,7 +34,10 @@
  *   - Pointers marked [dev] are device pointers on the context's device;
  *     [host] are host pointers. `stream` is a cudaStream_t passed as void*.
  *   - moeshard_forward is enqueue-only on `stream`: no host synchronisation,
- *     no data-dependent launch geometry, CUDA-graph capturable.
+ *     no data-dependent launch geometry, CUDA-graph capturable. With a
+ *     communicator the token AllGather runs on a context-owned side stream
+ *     forked from `stream` by an event and joined back before the call
+ *     returns, so `stream` still orders all of the call's work.
  *   - Collective calls (moeshard_init, moeshard_forward) must be made by all
  *     `world` ranks in the same order with the same `layer` and `n_local`
  *     (with MOESHARD_FLAG_UNEVEN_TOKENS n_local may differ between ranks).

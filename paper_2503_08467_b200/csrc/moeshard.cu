@@ -190,6 +190,12 @@ struct moeshard_ctx {
   int EP = 16;
   std::vector<LayerW> layers;
   ncclComm_t comm = nullptr;
+  // Step 3 token AllGather overlapped with Step 1 (x does not depend on the routing): the
+  // AllGather of x runs on s_x, forked from the caller's stream before the router and joined
+  // after the metadata AllGather (MOESHARD_OVERLAP_AG=0: everything on the caller's stream)
+  bool overlap_ag = true;
+  cudaStream_t s_x = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // peer-memory exchange (MOESHARD_FLAG_P2P): this rank's region (library-owned) and
   // every rank's region as mapped here; opened IPC mappings are closed at destroy
   bool p2p = false, connected = false;
@@ -241,6 +247,34 @@ int fail(moeshard_ctx* c, int code, const char* fmt, ...) {
     if (_r != ncclSuccess)                                                                   \
       return fail(ctx, MOESHARD_ERR_NCCL, "%s failed: %s", #expr, nccl().GetErrorString(_r)); \
   } while (0)
+
+// an internal step that already recorded its error: propagate the status code
+#define CUDA_TRY_RET(ctx, expr) \
+  do {                          \
+    const int _st = (expr);     \
+    if (_st != MOESHARD_OK) return _st; \
+  } while (0)
+
+namespace {
+
+// Step 3: replicate every rank's tokens into x_all (rank-major slots of
+// ns rows). With MOESHARD_FLAG_UNEVEN_TOKENS the n rows go to this rank's slot first and the
+// AllGather sends the whole slot in place.
+int allgather_tokens(moeshard_ctx* c, const void* hidden, int n, int ns, bool uneven,
+                     ncclDataType_t ndt, cudaStream_t st) {
+  const void* xsend = hidden;
+  if (uneven) {
+    char* slot = static_cast<char*>(c->x_all) + static_cast<size_t>(c->rank) * ns * c->h * c->elt;
+    if (n > 0)
+      CUDA_TRY(c, cudaMemcpyAsync(slot, hidden, static_cast<size_t>(n) * c->h * c->elt,
+                                  cudaMemcpyDeviceToDevice, st));
+    xsend = slot;
+  }
+  NCCL_TRY(c, nccl().AllGather(xsend, c->x_all, static_cast<size_t>(ns) * c->h, ndt, c->comm, st));
+  return MOESHARD_OK;
+}
+
+}  // namespace
 
 int validate(const moeshard_config* c, int world) {
   if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "config is NULL");
@@ -471,6 +505,14 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
       delete c;
       return fail(nullptr, MOESHARD_ERR_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
     }
+    if (const char* ov = getenv("MOESHARD_OVERLAP_AG")) c->overlap_ag = atoi(ov) != 0;
+    if (c->overlap_ag &&
+        (cudaStreamCreateWithFlags(&c->s_x, cudaStreamNonBlocking) != cudaSuccess ||
+         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+      moeshard_destroy(c);
+      return fail(nullptr, MOESHARD_ERR_CUDA, "side stream / events for the token AllGather");
+    }
   }
   *out = c;
   return MOESHARD_OK;
@@ -556,6 +598,14 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   int32_t* err_flag = c->tb.stats + 3;
 
   c->mark(0, s);
+  // Step 3 (tokens) forked ahead of Step 1: the AllGather of x overlaps the router
+  const bool ag_x_side = st_route && c->coll && !c->p2p && c->overlap_ag;
+  if (ag_x_side) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s_x, c->ev_fork, 0));
+    CUDA_TRY_RET(c, allgather_tokens(c, hidden, n, ns, uneven, ndt, c->s_x));
+    CUDA_TRY(c, cudaEventRecord(c->ev_join, c->s_x));
+  }
   // Step 1: route local tokens
   RouteRec* my_route = c->route + (c->coll ? static_cast<size_t>(c->rank) * ns : 0);
   // tokens per hist-block = tokens per router CTA (64 for the SIMT router; the
@@ -627,21 +677,14 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     CUDA_TRY(c, launch_p2p_push(c->pa, hidden, n, ns, h * c->elt / 16, nbr, E, c->num_sms, s));
     c->launches += 1;
   } else if (st_route && c->coll) {
-    const void* xsend = hidden;
-    if (uneven) {   // the slot's n rows in place, the AllGather sends the whole slot
-      char* slot = static_cast<char*>(c->x_all) + static_cast<size_t>(c->rank) * ns * h * c->elt;
-      if (n > 0)
-        CUDA_TRY(c, cudaMemcpyAsync(slot, hidden, static_cast<size_t>(n) * h * c->elt,
-                                    cudaMemcpyDeviceToDevice, s));
-      xsend = slot;
-    }
+    if (!ag_x_side) CUDA_TRY_RET(c, allgather_tokens(c, hidden, n, ns, uneven, ndt, s));
     NCCL_TRY(c, nccl().GroupStart());
-    NCCL_TRY(c, nccl().AllGather(xsend, c->x_all, static_cast<size_t>(ns) * h, ndt, c->comm, s));
     NCCL_TRY(c, nccl().AllGather(my_route, c->route, static_cast<size_t>(ns) * 2, ncclInt32,
                                  c->comm, s));
     NCCL_TRY(c, nccl().AllGather(my_hist, c->block_hist, static_cast<size_t>(nbr) * E, ncclInt32,
                                  c->comm, s));
     NCCL_TRY(c, nccl().GroupEnd());
+    if (ag_x_side) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_join, 0));
   }
   c->mark(2, s);
   if (st_compute) {
@@ -886,6 +929,9 @@ int moeshard_destroy(moeshard_ctx* c) {
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->region) cudaFree(c->region);
   for (auto& e : c->ev) cudaEventDestroy(e);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->s_x) cudaStreamDestroy(c->s_x);
   delete c;
   return MOESHARD_OK;
 }

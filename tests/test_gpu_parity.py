@@ -391,7 +391,7 @@ def test_route_group_fused_matches_separate_and_oracle(N, h, d_ff, E, routing):
 
 
 @pytest.mark.parametrize("flag", ["FUSED_ROUTE_GROUP", "CPASYNC_GATHER", "ROW_COPY_IN_FFN", "FUSED_SCAN",
-                                  "DYNAMIC_SCHED", None])
+                                  "DYNAMIC_SCHED", "FORCE_COLLECTIVES", None])
 def test_forward_under_cuda_graph_replay(flag):
     """A captured forward replays correctly with new token values and new routing
     (the grid barrier of the fused route+group launch carries no launch arguments)."""
@@ -430,6 +430,43 @@ def test_forward_under_cuda_graph_replay(flag):
         np.testing.assert_array_equal(r["perm"], perm)
         assert O.max_abs_rel(out.float().cpu().numpy(), y_ref) <= BF16_TOL
     L.close()
+
+
+@pytest.mark.parametrize("uneven", [False, True])
+def test_token_allgather_overlap_matches_serial(uneven, monkeypatch):
+    """Step 3's token AllGather forked onto a side stream ahead of the router (default) gives
+    bit-identical routing and outputs to the all-on-one-stream order (MOESHARD_OVERLAP_AG=0),
+    through the NCCL exchange (one rank), eagerly and back to back on the same inputs."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200 import moeshard as C
+    flags = C.MOESHARD_FLAG_FORCE_COLLECTIVES | (C.MOESHARD_FLAG_UNEVEN_TOKENS if uneven else 0)
+    N, h, d_ff, E = 1500, 256, 512, 16
+    inp = W.make_layer_inputs(26, N, h, d_ff, E, dtype=torch.bfloat16, routing="zipf")
+    outs, routes = [], []
+    for ov in ("1", "0"):
+        monkeypatch.setenv("MOESHARD_OVERLAP_AG", ov)
+        L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N + 37 if uneven else N,
+                          dtype=torch.bfloat16, flags=flags)
+        L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
+        x, w_r, f = inp.x.cuda(), inp.w_r.cuda(), inp.forced.cuda()
+        for _ in range(3):
+            y = L.forward(0, x, w_r, forced_expert=f)
+        L.check()
+        torch.cuda.synchronize()
+        outs.append(y.clone())
+        routes.append({k: v.cpu().numpy() for k, v in L.routing(N).items()})
+        L.close()
+    assert torch.equal(outs[0], outs[1])
+    for k in routes[0]:
+        a, b = routes[0][k], routes[1][k]
+        if uneven and a.shape[0] == N + 37:   # the unused slot tail is undefined but expert -1
+            np.testing.assert_array_equal(a[:N], b[:N])
+            if k == "expert":
+                assert (a[N:] == -1).all() and (b[N:] == -1).all()
+        else:
+            np.testing.assert_array_equal(a, b)
+    if not uneven:   # (the uneven path's oracle parity: test_uneven_tokens_per_rank)
+        _check_layer(inp, outs[0], routes[0], tol=BF16_TOL)
 
 
 # --------------------------------------------------------------------- alternative token paths
