@@ -209,7 +209,9 @@ def _config_json(cfg, args, G):
             "tokens_global": cfg["N"], "tokens_per_rank": cfg["N"] // G, "top_k": 1,
             "parallelism": f"moeshard expert-sharding x{G} (each rank: 1/{G} of every expert)",
             "routing": "natural learned-style router (near-uniform); skewed = Zipf(1.2) forced",
-            "transport": ("none (one GPU)" if G == 1 else
+            "transport": ("NCCL, 1-rank communicator (FORCE_COLLECTIVES)"
+                          if G == 1 and getattr(args, "force_collectives", False) else
+                          "none (one GPU)" if G == 1 else
                           "peer-memory stores (MOESHARD_FLAG_P2P)" if getattr(args, "transport", "nccl") == "p2p"
                           else "NCCL AllGather + ReduceScatter")}
 
@@ -307,6 +309,9 @@ def main():
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
                     help="G > 1 token / partial exchange: NCCL collectives, or device-initiated "
                          "stores into peer memory (MOESHARD_FLAG_P2P)")
+    ap.add_argument("--force-collectives", action="store_true",
+                    help="G = 1 only: run the NCCL exchange path with a 1-rank communicator "
+                         "(MOESHARD_FLAG_FORCE_COLLECTIVES; measures its overhead, not a bench line)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sustained", type=int, default=5000,
@@ -351,7 +356,9 @@ def main():
     from paper_2503_08467_b200 import moeshard as C
     layer = MoEShardLayer(h, d_ff, E, n_layers=NW, max_tokens_per_rank=n, dtype=torch.bfloat16,
                           rank=rank, world=G, device=local,
-                          flags=C.MOESHARD_FLAG_P2P if args.transport == "p2p" else 0)
+                          flags=C.MOESHARD_FLAG_P2P if args.transport == "p2p" else
+                          C.MOESHARD_FLAG_FORCE_COLLECTIVES if args.force_collectives and G == 1
+                          else 0)
     for l in range(NW):
         wi, wo = W.make_expert_weights(seed, E, h, d_ff, cols=(c0, c1), device=dev, layer=l)
         layer.load_expert_shards(l, wi, wo)
