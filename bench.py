@@ -499,8 +499,10 @@ def main():
         ms_e2e = timed(fe, args.steps, args.warmup, finish=streamer.join)
         e2e = {"value": N / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": n * h * 2 * G, "d2h_bytes_per_step": n * h * 2 * G,
-               "path": "MoEShardLayer.host_streamer: pinned H2D (copy stream) -> moeshard_forward "
-                       "-> D2H (copy stream), 3 device buffers per direction, per rank"}
+               "path": "MoEShardLayer.host_streamer: lock-step pipeline per rank - step k issues "
+                       "pinned H2D of batch k (copy stream), moeshard_forward of batch k-1 and D2H "
+                       "of batch k-2 (second copy stream); pipeline fill and drain inside the timed "
+                       "region"}
 
     hbm, tf_burst, tf_sust, peak_src = peaks()
     # algorithmic bytes per launch
