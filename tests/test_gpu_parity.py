@@ -214,10 +214,26 @@ def test_host_streamer_matches_device_forward():
         st.step(0, host_in[k], w_r, host_out[k])
     st.join()
     torch.cuda.synchronize()
+    refs = []
     for k in range(5):
-        ref = L.forward(0, xs[k].cuda(), w_r)
+        refs.append(L.forward(0, xs[k].cuda(), w_r).cpu())
         torch.cuda.synchronize()
-        assert torch.equal(host_out[k], ref.cpu())
+        assert torch.equal(host_out[k], refs[k])
+    # pipeline edge cases: one batch then join, a join mid-stream, join with nothing pending
+    for o in host_out:
+        o.zero_()
+    st.join()
+    st.step(0, host_in[0], w_r, host_out[0])
+    st.join()
+    for k in (1, 2):
+        st.step(0, host_in[k], w_r, host_out[k])
+    st.join()
+    for k in (3, 4):
+        st.step(0, host_in[k], w_r, host_out[k])
+    st.join()
+    torch.cuda.synchronize()
+    for k in range(5):
+        assert torch.equal(host_out[k], refs[k])
 
 
 def test_forced_out_of_range_is_reported():
