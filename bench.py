@@ -274,11 +274,34 @@ def encoder_ttft(name, G, rank, local, barrier, dist, reps=10, oracle_sample=204
 
     ttft = run(lambda: enc.forward(x))
     ttft_skew = run(lambda: enc.forward(x, forced=zipf))
+    # the same forward captured once and replayed as a CUDA graph (launch overhead removed;
+    # the torch blocks and the library's launches are all capturable)
+    ttft_graph, graph_err = None, None
+    try:
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            enc.forward(x)
+        stream.wait_stream(cs)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            y_g = enc.forward(x)
+        y_e = enc.forward(x)
+        g.replay()
+        torch.cuda.synchronize()
+        if not torch.equal(y_g, y_e):
+            raise RuntimeError("graph replay output differs from the eager forward")
+        ttft_graph = run(g.replay)
+        del g
+    except Exception as e:   # reported, not fatal: the eager TTFT above stands
+        graph_err = f"{type(e).__name__}: {e}"[:200]
     y = torch.randn(n_local, cfg.d_model, device=dev, dtype=torch.bfloat16)
     moe_only = run(lambda: [enc.moe.forward(j, y, enc.layers[i]["w_r"])
                             for j, i in enumerate(enc.moe_ids)])
     enc.moe.close()
     res = {"workload": title, "ttft_ms": ttft, "ttft_ms_zipf": ttft_skew,
+           "ttft_ms_graph": ttft_graph, **({"graph_error": graph_err} if graph_err else {}),
            "ttft_moe_ms": moe_only, "moe_layers": len(enc.moe_ids), "reps": reps,
            "tokens": N, "note": "non-MoE blocks are torch (cuBLAS/SDPA) replicated on every rank; "
                                 "MoE FFNs are libmoeshard; T5 relative bias omitted"}
