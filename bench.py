@@ -366,6 +366,9 @@ def main():
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
     if G > 1:
+        # communicator init lines (rank / nranks / NVLS) in the log, for the scaling record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device(dev))
     E, h, d_ff, N = cfg["E"], cfg["h"], cfg["d_ff"], cfg["N"]
     n = N // G
@@ -528,25 +531,21 @@ def main():
                        "region"}
 
     hbm, tf_burst, tf_sust, peak_src = peaks()
-    # algorithmic bytes per launch
-    def gemm_bytes(e_act):
-        w = e_act * h * F * 2
-        return {"gemm_up": w + N * h * 2 + N * F * 2, "gemm_down": w + N * F * 2 + N * h * 2}
-    gb = gemm_bytes(e_active_u)
+    # Algorithmic HBM bytes per launch: what the step must
+    # move at least - the active experts' weight shards, the tokens once in, the output once
+    # out. The expert-ordered copy X_perm and the intermediate H are implementation
+    # round-trips, reported separately (`activation_roundtrip_bytes`), never as algorithmic.
     nb_hist = G * math.ceil(n / 128)
-    alg = {   # algorithmic HBM bytes per launch
+    w_bytes = e_active_u * 2 * h * F * 2
+    alg = {
         "router": n * h * 2 + h * E * 2 + n * 8 + math.ceil(n / 128) * E * 4,
-        "grouping": N * 8 + N * 4 + 2 * N * h * 2 + nb_hist * E * 4,
-        "gemm_up": gb["gemm_up"],
-        "gemm_down": gb["gemm_down"],
+        "grouping": N * 8 + N * 4 + N * h * 2 + nb_hist * E * 4,   # tokens read once, tables
+        "expert_ffn": w_bytes + N * h * 2 + N * h * 2,
     }
-    flops = {"gemm_up": 2 * N * h * F, "gemm_down": 2 * N * h * F}
-    # both products run as ONE fused persistent kernel when both tile counts are even
-    fused = not int(os.environ.get("MOESHARD_FLAGS", "0")) & 4
-    if fused:
-        ph_us = {("expert_ffn" if k == "gemm_up" else k): v for k, v in ph_us.items() if k != "gemm_down"}
-        alg["expert_ffn"] = alg.pop("gemm_up") + alg.pop("gemm_down")
-        flops = {"expert_ffn": 4 * N * h * F}
+    roundtrip = {"x_perm_write_read": 2 * N * h * 2, "H_write_read": 2 * N * F * 2}
+    flops = {"expert_ffn": 4 * N * h * F}
+    # both products run as ONE fused persistent kernel (the bench never sets UNFUSED_GEMM)
+    ph_us = {("expert_ffn" if k == "gemm_up" else k): v for k, v in ph_us.items() if k != "gemm_down"}
     kernels = {}
     for k, us in ph_us.items():
         d = {"us": round(us, 3)}
@@ -556,7 +555,7 @@ def main():
         if k in flops and us > 0:
             d["TFLOP_s"] = round(flops[k] / (us * 1e-6) / 1e12, 1)
         kernels[k] = d
-    dom = "expert_ffn" if fused else max(("gemm_up", "gemm_down"), key=lambda k: ph_us[k])
+    dom = "expert_ffn"
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -570,7 +569,13 @@ def main():
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)", "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_source": traffic_src,
-                "algorithmic_bytes": alg[dom], "launch_us": round(ph_us[dom], 3),
+                "algorithmic_bytes": alg[dom],
+                "algorithmic_bytes_def": "SURVEY.md §8(d): active experts' weight shards 2*E_act*h*F*2 "
+                                         "+ tokens in N*h*2 + output out N*h*2",
+                "activation_roundtrip_bytes": roundtrip,
+                "frac_incl_roundtrips": round((alg[dom] + sum(roundtrip.values())) /
+                                              (ph_us[dom] * 1e-6) / 1e9 / hbm, 4),
+                "launch_us": round(ph_us[dom], 3),
                 "timing": "phase CUDA events on the launch stream around the kernel, averaged over "
                           f"{cnt} forwards of a separate profiled pass (includes ~2-3 us event gap)"}
     # whole-layer roofline: T_TC, T_HBM (weights + x + partial), T_NV

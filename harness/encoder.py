@@ -66,8 +66,10 @@ class SwitchEncoder:
             self.layers.append(L)
         self.moe_out = None
 
-    def forward(self, x: torch.Tensor, forced: Optional[List[torch.Tensor]] = None) -> torch.Tensor:
-        """x [b_local, seq, h] -> [b_local, seq, h]."""
+    def forward(self, x: torch.Tensor, forced: Optional[List[torch.Tensor]] = None,
+                capture: Optional[list] = None) -> torch.Tensor:
+        """x [b_local, seq, h] -> [b_local, seq, h]. capture (test hook): a list that receives,
+        per MoE layer, {slot, input, output, routing} copies for teacher-forced parity."""
         cfg = self.cfg
         b, s, h = x.shape
         nh, hd = cfg.n_heads, h // cfg.n_heads
@@ -82,6 +84,9 @@ class SwitchEncoder:
                     self.moe_out = torch.empty_like(y)
                 f = None if forced is None else forced[L["moe_slot"]]
                 z = self.moe.forward(L["moe_slot"], y, L["w_r"], forced_expert=f, out=self.moe_out)
+                if capture is not None:
+                    capture.append({"slot": L["moe_slot"], "input": y.clone(), "output": z.clone(),
+                                    "routing": self.moe.routing(y.shape[0])})
             else:
                 z = torch.relu(y @ L["wi"]) @ L["wf"]
             x = x + z.view(b, s, h)

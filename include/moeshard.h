@@ -70,21 +70,16 @@ typedef enum {
   MOESHARD_FP32 = 1  /* fp32 validation mode: fp32 everywhere, FFMA on CUDA cores */
 } moeshard_dtype;
 
-/* config.flags */
+/* config.flags (any other bit is rejected with MOESHARD_ERR_INVALID_ARG; bits 0x8-0x40,
+ * 0x100, 0x400 and 0x800 held round-1 experiments that measured slower and were removed) */
 #define MOESHARD_FLAG_FORCE_COLLECTIVES 0x1u /* run the AllGather/ReduceScatter path even at world = 1 */
 #define MOESHARD_FLAG_SIMT_GEMM 0x2u         /* bf16 mode: CUDA-core grouped GEMM (ablation / debug) */
 #define MOESHARD_FLAG_UNFUSED_GEMM 0x4u      /* bf16 mode: up and down products as two launches (ablation) */
-#define MOESHARD_FLAG_TMA_GATHER 0x8u        /* bf16 fused mode: gather token rows with TMA gather4 instead of X_perm (experimental, slower) */
-#define MOESHARD_FLAG_H_TRANSPOSED 0x10u     /* bf16 fused mode: keep H transposed, MN-major down operand (experimental, slower) */
-#define MOESHARD_FLAG_FUSED_ROUTE_GROUP 0x20u /* world = 1: run Step 2 inside the router launch (grid barriers; experimental, slower) */
-#define MOESHARD_FLAG_CPASYNC_GATHER 0x40u    /* bf16 fused mode: the FFN gathers token rows with cp.async (no X_perm copy; experimental, slower) */
-#define MOESHARD_FLAG_NO_L2_PERSIST 0x80u     /* bf16 mode: leave the device's persisting-L2 limit alone (see moeshard_init) */
-#define MOESHARD_FLAG_ROW_COPY_IN_FFN 0x100u  /* bf16 fused mode: copy token rows into expert order inside the FFN launch (per-expert hand-off; experimental, slower) */
-#define MOESHARD_FLAG_ROUTER_TOK64 0x800u     /* tcgen05 router: 64 tokens per CTA (twice the CTAs) instead of 128 */
-#define MOESHARD_FLAG_FUSED_SCAN 0x400u        /* Step 2's per-expert block scans inside the grouping launch (ticket-ordered; experimental, slower) */
-#define MOESHARD_FLAG_DYNAMIC_SCHED 0x1000u   /* fused FFN: clusters take work units from a global counter (correct even when not every cluster is resident, e.g. ranks sharing a GPU); default static round robin */
-#define MOESHARD_FLAG_UNEVEN_TOKENS 0x2000u   /* world > 1: ranks may pass different n_local each forward; token slots of max_tokens_per_rank rows per rank, routing tables [world * max_tokens_per_rank] with expert -1 in unused slots */
-#define MOESHARD_FLAG_P2P 0x200u              /* bf16: Steps 3 and 5 by device-initiated stores into peer GPU memory instead of NCCL (see moeshard_p2p_*) */
+#define MOESHARD_FLAG_NO_L2_PERSIST 0x80u    /* bf16 mode: leave the device's persisting-L2 limit alone (see moeshard_init) */
+#define MOESHARD_FLAG_DYNAMIC_SCHED 0x1000u  /* fused FFN: clusters take work units from a global counter (correct even when not every cluster is resident, e.g. ranks sharing a GPU); default static round robin */
+#define MOESHARD_FLAG_UNEVEN_TOKENS 0x2000u  /* world > 1: ranks may pass different n_local each forward; token slots of max_tokens_per_rank rows per rank, routing tables [world * max_tokens_per_rank] with expert -1 in unused slots */
+#define MOESHARD_FLAG_P2P 0x200u             /* bf16: Steps 3 and 5 by device-initiated stores into peer GPU memory instead of NCCL (see moeshard_p2p_*) */
+#define MOESHARD_FLAG_SERIAL_AG 0x4000u      /* NCCL transport: token AllGather on the caller's stream after the router (default: a side stream, overlapping the router) */
 
 /* moeshard_forward_stages masks: ROUTE = Step 1 + the token exchange (Step 3 push),
  * COMPUTE = Steps 2 and 4 (+ the Step 5 send in P2P mode), REDUCE = the Step 5 aggregate. */

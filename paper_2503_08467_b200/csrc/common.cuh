@@ -38,7 +38,6 @@ struct Tables {
   int32_t* done;           // [chunks] up-projection tiles completed per token chunk (fused GEMM), zeroed by Step 2
   int32_t* pos;            // [E+1] internal segment starts (exclusive scan of round_up(count, 32))
   int32_t* perm_pad;       // [N + 32E] internal row -> global token id (padding rows: stale)
-  int32_t* copied;         // [E] 8-row groups of X_perm written per expert (in-FFN row copy), zeroed by Step 2
   int32_t* next_unit;      // [1] the fused FFN's dynamic work counter, zeroed by Step 2
 };
 
@@ -119,7 +118,7 @@ void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int 
 void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int32_t* tot,
                          Tables tb, int n_mt_up_tc, int n_mt_down_tc, const RouteRec* route,
                          const void* x_all, int n, int nbr, int HB, int row_bytes, int32_t* perm,
-                         void* x_perm, int32_t* sync, cudaStream_t s);
+                         void* x_perm, cudaStream_t s);
 
 void launch_transpose(int dtype, const void* src, void* dst, int batch, int rows, int cols,
                       cudaStream_t s);

@@ -84,34 +84,6 @@ template <bool kDown>
 __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok, int nmma,
                                            int fbase, uint32_t taddr, int lane, uint64_t pol_keep,
                                            __nv_bfloat16* stage) {
-  if (!kDown && p.ht) {
-    // H^T row f = fbase + lane: this thread owns it; 32 tokens per TMEM load -> 4 x 16 B
-    __nv_bfloat16* row = p.out + (size_t)(fbase + lane) * p.ld_ht + tok0;
-    for (int c0 = 0; c0 < nmma; c0 += 32) {
-      uint32_t r[32];
-      if (c0 + 16 < nmma) {
-        tmem_ld32(taddr + c0, r);
-      } else {
-        uint32_t (&r16)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[0]);
-        tmem_ld16(taddr + c0, r16);
-      }
-      tmem_ld_wait();
-      uint32_t pk[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const __nv_bfloat162 v = __floats2bfloat162_rn(fmaxf(__uint_as_float(r[2 * j]), 0.f),
-                                                       fmaxf(__uint_as_float(r[2 * j + 1]), 0.f));
-        pk[j] = *reinterpret_cast<const uint32_t*>(&v);
-      }
-      const int nv = min(32, nmma - c0);   // columns written (padding columns are harmless:
-#pragma unroll                              // they lie inside this expert's chunk or the tail)
-      for (int q = 0; q < 4; ++q)
-        if (q * 8 < nv && c0 + q * 8 < ntok)
-          st_v4_hint(row + c0 + q * 8, make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]),
-                     pol_keep);
-    }
-    return;
-  }
   uint16_t* st16 = reinterpret_cast<uint16_t*>(stage);
   // down: the destination rows perm[j] and gates of the unit's tokens are fetched
   // up front (lane holds tokens lane + 32 i), so the loop below has no dependent
@@ -188,16 +160,9 @@ __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok
   }
 }
 
-// kMode (experiments only, MOESHARD_TC_VARIANT 5-10): 0 = normal; 1 = stream A+B, no MMA and
-// no epilogue; 2 = stream A only; 3 = MMA + TMEM reads, no global stores; 4 = MMA, no epilogue;
-// 5 = normal + per-role blocked-time counters printed by CTA 0.
-#define TWAIT(acc, stmt)                        \
-  do {                                          \
-    const long long _t0 = clock64();            \
-    stmt;                                       \
-    acc += clock64() - _t0;                     \
-  } while (0)
-template <bool kDown, int A_STAGES, int B_STAGES, int kMode = 0>
+// One-CTA kernel (M = 128): the unfused two-launch ablation when a projection has an
+// odd number of 128-feature tiles.
+template <bool kDown, int A_STAGES, int B_STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_grouped_gemm(const __grid_constant__ CUtensorMap tmB, TcParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -254,113 +219,93 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nkb = p.K / BK;
 
   if (warp == 0) {
-    {
-      // ------------------------------------------------------------ weight producer
-      const uint64_t pol_w = policy_evict_first();  // weights: streamed, shared only by siblings
-      int stage = 0;
-      uint32_t phase = 0;
-      long long t_blk = 0, t_all = clock64();
-      for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
-        const __nv_bfloat16* tiles =
-            p.a_tiles + (static_cast<size_t>(w.e) * n_mt + w.mt) * nkb * (BM * BK);
-        for (int kb = 0; kb < nkb; ++kb) {
-          TWAIT(t_blk, mbar_wait(&emptyA[stage], phase ^ 1));
-          if (elect_one()) {
-            mbar_arrive_expect_tx(&fullA[stage], A_BYTES);
-            bulk_load(sA + stage * A_BYTES, tiles + static_cast<size_t>(kb) * (BM * BK), A_BYTES,
-                      &fullA[stage], pol_w);
-          }
-          __syncwarp();
-          if (++stage == A_STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+    // -------------------------------------------------------------- weight producer
+    const uint64_t pol_w = policy_evict_first();  // weights: streamed, shared only by siblings
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
+      const __nv_bfloat16* tiles =
+          p.a_tiles + (static_cast<size_t>(w.e) * n_mt + w.mt) * nkb * (BM * BK);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&emptyA[stage], phase ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&fullA[stage], A_BYTES);
+          bulk_load(sA + stage * A_BYTES, tiles + static_cast<size_t>(kb) * (BM * BK), A_BYTES,
+                    &fullA[stage], pol_w);
+        }
+        __syncwarp();
+        if (++stage == A_STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
-      if (kMode == 5 && blockIdx.x == 0 && lane == 0)
-        printf("[A producer] total %lld blocked-on-empty %lld\n", clock64() - t_all, t_blk);
     }
   } else if (warp == 3) {
-    if (kMode != 2) {
-      // ------------------------------------------------------------ token producer
-      const uint64_t pol_x = policy_evict_last();   // activations: re-read by n_mt tiles
-      int stage = 0;
-      uint32_t phase = 0;
-      long long t_blk = 0, t_all = clock64();
-      for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
-        const int nb = (w.ntok + B_BOX - 1) / B_BOX;
-        for (int kb = 0; kb < nkb; ++kb) {
-          TWAIT(t_blk, mbar_wait(&emptyB[stage], phase ^ 1));
-          if (elect_one()) {
-            mbar_arrive_expect_tx(&fullB[stage], nb * B_BOX_BYTES);
-            for (int i = 0; i < nb; ++i)
-              tma_load_2d(&tmB, &fullB[stage], sB + stage * B_BYTES + i * B_BOX_BYTES, kb * BK,
-                          w.tok0 + i * B_BOX, pol_x);
-          }
-          __syncwarp();
-          if (++stage == B_STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+    // -------------------------------------------------------------- token producer
+    const uint64_t pol_x = policy_evict_last();   // activations: re-read by n_mt tiles
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
+      const int nb = (w.ntok + B_BOX - 1) / B_BOX;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&emptyB[stage], phase ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&fullB[stage], nb * B_BOX_BYTES);
+          for (int i = 0; i < nb; ++i)
+            tma_load_2d(&tmB, &fullB[stage], sB + stage * B_BYTES + i * B_BOX_BYTES, kb * BK,
+                        w.tok0 + i * B_BOX, pol_x);
+        }
+        __syncwarp();
+        if (++stage == B_STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
-      if (kMode == 5 && blockIdx.x == 0 && lane == 0)
-        printf("[B producer] total %lld blocked-on-empty %lld\n", clock64() - t_all, t_blk);
     }
   } else if (warp == 1) {
-    {
-      // ------------------------------------------------------------ MMA issuer
-      int sa = 0, sb = 0;
-      uint32_t pa = 0, pb = 0;
-      int as = 0;
-      uint32_t aphase = 0;
-      long long t_a = 0, t_b = 0, t_t = 0, t_all = clock64();
-      int units = 0;
-      for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
-        const int nmma = (w.ntok + 15) & ~15;
-        const uint32_t idesc = idesc_bf16_f32(BM, nmma);
-        ++units;
-        if (kMode == 0 || kMode == 3 || kMode == 5) TWAIT(t_t, mbar_wait(&tempty[as], aphase ^ 1));
+    // -------------------------------------------------------------- MMA issuer
+    int sa = 0, sb = 0;
+    uint32_t pa = 0, pb = 0;
+    int as = 0;
+    uint32_t aphase = 0;
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
+      const int nmma = (w.ntok + 15) & ~15;
+      const uint32_t idesc = idesc_bf16_f32(BM, nmma);
+      mbar_wait(&tempty[as], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + as * BN_MAX;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&fullB[sb], pb);
+        mbar_wait(&fullA[sa], pa);
         tc_fence_after();
-        const uint32_t d = tmem_base + as * BN_MAX;
-        for (int kb = 0; kb < nkb; ++kb) {
-          if (kMode != 2) TWAIT(t_b, mbar_wait(&fullB[sb], pb));
-          TWAIT(t_a, mbar_wait(&fullA[sa], pa));
-          tc_fence_after();
-          const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
-          const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B_BYTES));
-          if (elect_one()) {
-            if (kMode == 0 || kMode >= 3) {
+        const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
+        const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B_BYTES));
+        if (elect_one()) {
 #pragma unroll
-              for (int k = 0; k < BK / 16; ++k)
-                mma_bf16_ss(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-            }
-            mma_commit(&emptyA[sa]);
-            if (kMode != 2) mma_commit(&emptyB[sb]);
-          }
-          __syncwarp();
-          if (++sa == A_STAGES) {
-            sa = 0;
-            pa ^= 1;
-          }
-          if (++sb == B_STAGES) {
-            sb = 0;
-            pb ^= 1;
-          }
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_ss(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          mma_commit(&emptyA[sa]);
+          mma_commit(&emptyB[sb]);
         }
-        if ((kMode == 0 || kMode == 3 || kMode == 5) && elect_one()) mma_commit(&tfull[as]);
         __syncwarp();
-        as ^= 1;
-        if (as == 0) aphase ^= 1;
+        if (++sa == A_STAGES) {
+          sa = 0;
+          pa ^= 1;
+        }
+        if (++sb == B_STAGES) {
+          sb = 0;
+          pb ^= 1;
+        }
       }
-      if (kMode == 5 && blockIdx.x == 0 && lane == 0)
-        printf("[MMA] units %d total %lld waitA %lld waitB %lld waitTMEM %lld\n", units,
-               clock64() - t_all, t_a, t_b, t_t);
+      if (elect_one()) mma_commit(&tfull[as]);
+      __syncwarp();
+      as ^= 1;
+      if (as == 0) aphase ^= 1;
     }
-  } else if (warp >= 4 && (kMode == 0 || kMode == 3 || kMode == 5)) {
+  } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
     const int wq = warp & 3;
     __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(
@@ -368,32 +313,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_keep = policy_evict_last();  // H is re-read by the down product
     int as = 0;
     uint32_t aphase = 0;
-    long long t_w = 0, t_all = clock64();
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
       const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
-      TWAIT(t_w, mbar_wait(&tfull[as], aphase));
+      mbar_wait(&tfull[as], aphase);
       tc_fence_after();
-      const int f = w.mt * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * BN_MAX;
-      if (kMode == 0 || kMode == 5) {
-        store_tile<kDown>(p, w.tok0, w.ntok, (w.ntok + 15) & ~15, w.mt * BM + wq * 32, taddr, lane,
-                          pol_keep, stage);
-      } else {
-        for (int c0 = 0; c0 < ((w.ntok + 15) & ~15); c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16(taddr + c0, r);
-          tmem_ld_wait();
-          if (r[0] == 0x7fc00001u) p.out[f] = __float2bfloat16_rn(0.f);  // keep the loads live
-        }
-      }
+      store_tile<kDown>(p, w.tok0, w.ntok, (w.ntok + 15) & ~15, w.mt * BM + wq * 32, taddr, lane,
+                        pol_keep, stage);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
       as ^= 1;
       if (as == 0) aphase ^= 1;
     }
-    if (kMode == 5 && blockIdx.x == 0 && lane == 0)
-      printf("[epilogue w%d] total %lld waitFull %lld\n", warp, clock64() - t_all, t_w);
   }
 
   tc_fence_before();
@@ -417,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int B2_BOX = 16;                       // token rows per TMA box (2 KB)
 constexpr int B2_BYTES = (BN_MAX / 2) * BK * 2;  // 16 KB: half of a 256-token tile
 
-template <bool kDown, int AS, int BS, bool kTiming = false>
+template <bool kDown, int AS, int BS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_grouped_gemm_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         TcParams p) {
@@ -481,57 +413,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
 
   if (warp == 0) {
-    {
-      // ------------------------------------------------------------ weight producer (both CTAs)
-      const uint64_t pol_w = policy_evict_first();
-      const uint32_t leader_full = mapa_shared(smem_u32(fullA), 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      long long t_blk = 0, t_all = clock64();
-      for (int u = cid; u < total; u += ncl) {
-        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
-        const int mt = 2 * w.mt + static_cast<int>(rank);
-        const int row0 = ((w.e * n_mt + mt) * nkb) * BM;
-        for (int kb = 0; kb < nkb; ++kb) {
-          TWAIT(t_blk, mbar_wait(&emptyA[stage], phase ^ 1));
-          const uint32_t fb = leader_full + stage * 8;
-          if (elect_one()) {
-            if (leader) mbar_arrive_expect_tx(&fullA[stage], 2 * A_BYTES);
-            else mbar_arrive_cluster(fb);
-            tma_load_2d_2sm(&tmA, fb, sA + stage * A_BYTES, 0, row0 + kb * BM, pol_w);
-          }
-          __syncwarp();
-          if (++stage == AS) { stage = 0; phase ^= 1; }
+    // -------------------------------------------------------------- weight producer (both CTAs)
+    const uint64_t pol_w = policy_evict_first();
+    const uint32_t leader_full = mapa_shared(smem_u32(fullA), 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = cid; u < total; u += ncl) {
+      const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
+      const int mt = 2 * w.mt + static_cast<int>(rank);
+      const int row0 = ((w.e * n_mt + mt) * nkb) * BM;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&emptyA[stage], phase ^ 1);
+        const uint32_t fb = leader_full + stage * 8;
+        if (elect_one()) {
+          if (leader) mbar_arrive_expect_tx(&fullA[stage], 2 * A_BYTES);
+          else mbar_arrive_cluster(fb);
+          tma_load_2d_2sm(&tmA, fb, sA + stage * A_BYTES, 0, row0 + kb * BM, pol_w);
         }
+        __syncwarp();
+        if (++stage == AS) { stage = 0; phase ^= 1; }
       }
-      if (kTiming && cid == 0 && lane == 0)
-        printf("[2sm A producer r%u] total %lld blocked %lld\n", rank, clock64() - t_all, t_blk);
     }
   } else if (warp == 3) {
-    {
-      // ------------------------------------------------------------ token producer (both CTAs)
-      const uint64_t pol_x = policy_evict_last();
-      const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = cid; u < total; u += ncl) {
-        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
-        const int half = ((w.ntok + 31) & ~31) / 2;     // rows per CTA
-        const int nb = half / B2_BOX;
-        const int r0 = w.tok0 + static_cast<int>(rank) * half;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&emptyB[stage], phase ^ 1);
-          const uint32_t fb = leader_full + stage * 8;
-          if (elect_one()) {
-            if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * nb * B2_BOX * BK * 2);
-            else mbar_arrive_cluster(fb);
-            for (int i = 0; i < nb; ++i)
-              tma_load_2d_2sm(&tmB, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
-                              r0 + i * B2_BOX, pol_x);
-          }
-          __syncwarp();
-          if (++stage == BS) { stage = 0; phase ^= 1; }
+    // -------------------------------------------------------------- token producer (both CTAs)
+    const uint64_t pol_x = policy_evict_last();
+    const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = cid; u < total; u += ncl) {
+      const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
+      const int half = ((w.ntok + 31) & ~31) / 2;     // rows per CTA
+      const int nb = half / B2_BOX;
+      const int r0 = w.tok0 + static_cast<int>(rank) * half;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&emptyB[stage], phase ^ 1);
+        const uint32_t fb = leader_full + stage * 8;
+        if (elect_one()) {
+          if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * nb * B2_BOX * BK * 2);
+          else mbar_arrive_cluster(fb);
+          for (int i = 0; i < nb; ++i)
+            tma_load_2d_2sm(&tmB, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
+                            r0 + i * B2_BOX, pol_x);
         }
+        __syncwarp();
+        if (++stage == BS) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -541,19 +466,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t pa = 0, pb = 0;
       int as = 0;
       uint32_t aphase = 0;
-      long long t_a = 0, t_b = 0, t_t = 0, t_all = clock64();
-      int units = 0;
       for (int u = cid; u < total; u += ncl) {
         const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
         const int nmma = (w.ntok + 31) & ~31;
         const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
-        ++units;
-        TWAIT(t_t, mbar_wait(&tempty[as], aphase ^ 1));
+        mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + as * BN_MAX;
         for (int kb = 0; kb < nkb; ++kb) {
-          TWAIT(t_b, mbar_wait(&fullB[sb], pb));
-          TWAIT(t_a, mbar_wait(&fullA[sa], pa));
+          mbar_wait(&fullB[sb], pb);
+          mbar_wait(&fullA[sa], pa);
           tc_fence_after();
           const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
           const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B2_BYTES));
@@ -573,9 +495,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         as ^= 1;
         if (as == 0) aphase ^= 1;
       }
-      if (kTiming && cid == 0 && lane == 0)
-        printf("[2sm MMA] units %d total %lld waitA %lld waitB %lld waitTMEM %lld\n", units,
-               clock64() - t_all, t_a, t_b, t_t);
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
@@ -586,25 +505,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
     int as = 0;
     uint32_t aphase = 0;
-    long long t_w = 0, t_all = clock64();
     for (int u = cid; u < total; u += ncl) {
       const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
-      TWAIT(t_w, mbar_wait(&tfull[as], aphase));
+      mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const int mt = 2 * w.mt + static_cast<int>(rank);
-      const int f = mt * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * BN_MAX;
       store_tile<kDown>(p, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
                         pol_keep, stage);
-      (void)f;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + as * 8);
       as ^= 1;
       if (as == 0) aphase ^= 1;
     }
-    if (kTiming && cid == 0 && lane == 0 && wq == 0)
-      printf("[2sm epilogue r%u] total %lld waitFull %lld\n", rank, clock64() - t_all, t_w);
   }
 
   tc_fence_before();
@@ -617,10 +531,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // ===========================================================================
 // Both projections in ONE persistent CTA-pair kernel. The work list is
 // [all up pair-units (expert-major), all down pair-units (expert-major)];
-// cluster c takes units c, c + #clusters, ... A down unit of expert e reads
-// H rows written by the up units of e (every feature tile), so its token
-// producer waits until done[chunk] == 2 * n_mp_up (each CTA of each up
-// pair-unit releases one count after its H tile is stored) - acquire, then an
+// cluster c takes units c, c + #clusters, ... A down unit of token chunk q
+// reads H rows written by every up unit of q (each feature tile), so its token
+// producer waits until done[q] == 2 * n_mp_up (each CTA of each up pair-unit
+// releases one count after its H tile is stored) - acquire, then an
 // async-proxy fence before the TMA reads H. Units earlier in the list never
 // wait on later ones, so with all clusters resident there is no deadlock.
 // This removes the down-projection's wave-quantisation tail and the launch gap
@@ -628,48 +542,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // ===========================================================================
 struct FusedParams {
   TcParams up, dn;
-  int32_t* done;  // [E], zeroed by Step 2 before every forward
-  // in-kernel row copy (Sec. 3.3 per-expert concatenation): X_perm[j] = x_all[perm_pad[j]]
-  // by the epilogue warps before their first tile; cp_src == nullptr: X_perm is ready
-  const uint4* cp_src = nullptr;
-  uint4* cp_dst = nullptr;
-  int cp_row_vecs = 0;
-  bool interleave = false;  // expert-group blocks (MOESHARD_FFN_INTERLEAVE=1); default all up, then all down
-  bool dynamic = false;     // units taken from a global counter in list order (MOESHARD_FLAG_DYNAMIC_SCHED)
-  int sibling_policy = 1;   // weight tiles of multi-chunk experts: 0 evict_first, 1 normal, 2 evict_last
-  int xpol = 2, hpol = 2;   // X_perm / H reads: 0 evict_first, 1 normal, 2 evict_last
-  bool early_tables = false; // tables via a release flag from the grouping launch's CTA 0 (see kernel)
-  bool light_release = true;  // H hand-off: bar.sync + one release (MOESHARD_LIGHT_RELEASE=0: + per-thread fences)
+  int32_t* done;       // [token chunks], zeroed by Step 2 before every forward
+  bool dynamic;        // units taken from a global counter in list order (MOESHARD_FLAG_DYNAMIC_SCHED)
+  bool early_tables;   // tables via a release flag from the grouping launch's CTA 0 (see kernel)
 };
 
 constexpr int kUQ = 2;             // unit-queue slots (dynamic scheduling): small, so a
                                    // cluster never sits on units other clusters could run
 constexpr int kUQConsumers = 13;   // warps that read a slot: leader 0,1,3,4-7; follower 0,3,4-7
 
-// Position u of the fused work list -> (down?, index in the up- or down-unit list).
-// Blocks of S experts (see the kernel): s_bstart[j] = first position of block j.
-struct ListPos {
-  bool down;
-  int idx;
-};
-__device__ __forceinline__ ListPos locate(int u, const int* s_bstart, int nblk, int S,
-                                          const int32_t* pref, int n_mp_up, int n_mp_dn) {
-  int lo = 0, hi = nblk;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (s_bstart[mid] <= u) lo = mid; else hi = mid;
-  }
-  const int K = nblk / 2;
-  const bool dn = (lo == nblk - 1) || (lo > 0 && (lo & 1) == 0);
-  const int g = lo == 0 ? 0 : lo == nblk - 1 ? K - 1 : dn ? lo / 2 - 1 : (lo + 1) / 2;
-  ListPos p;
-  p.down = dn;
-  p.idx = pref[g * S] * (dn ? n_mp_dn : n_mp_up) + (u - s_bstart[lo]);
-  return p;
-}
-
-// KA: 64-wide k-atoms per ring stage (1 or 2); a stage holds KA weight tiles and KA token tiles.
-template <int AS, int BS, int KA, bool kT = false>
+template <int AS, int BS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_moe_ffn_2sm(const __grid_constant__ CUtensorMap tmA_up, const __grid_constant__ CUtensorMap tmB_up,
                    const __grid_constant__ CUtensorMap tmA_dn, const __grid_constant__ CUtensorMap tmB_dn,
@@ -679,9 +561,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int E = fp.up.E;
   uint8_t* sA = smem;
-  constexpr int SA_BYTES = KA * A_BYTES, SB_BYTES = KA * B2_BYTES;   // per stage
-  uint8_t* sB = smem + AS * SA_BYTES;
-  uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + BS * SB_BYTES);
+  uint8_t* sB = smem + AS * A_BYTES;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + BS * B2_BYTES);
   uint64_t* emptyA = fullA + AS;
   uint64_t* fullB = emptyA + AS;
   uint64_t* emptyB = fullB + BS;
@@ -692,10 +573,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   int32_t* s_off = s_pref + (E + 1);     // internal segment starts (pos)
   int32_t* s_cs = s_off + (E + 1);
   int32_t* s_end = s_cs + E;             // pos + count
+  // per-warp epilogue staging (4 x 1 KB), then the unit queue (slots + barriers)
+  __nv_bfloat16* s_stage = reinterpret_cast<__nv_bfloat16*>(
+      (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15));
+  int* s_uq = reinterpret_cast<int*>(s_stage + 4 * 512);
+  uint64_t* uq_full = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(s_uq + kUQ) + 7) & ~static_cast<uintptr_t>(7));
+  uint64_t* uq_empty = uq_full + kUQ;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t g_entry = 0, g_ready = 0;
-  if (kT) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
@@ -719,16 +605,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);
     }
-    {  // unit queue barriers (same smem position as computed after the tables below)
-      int* qb = reinterpret_cast<int*>(
-          (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2 + 128 +
-          (2 * E + 2);
-      uint64_t* qf = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(qb + kUQ) + 7) &
-                                                 ~static_cast<uintptr_t>(7));
-      for (int q = 0; q < kUQ; ++q) {
-        mbar_init(&qf[q], 1);
-        mbar_init(&qf[kUQ + q], kUQConsumers);
-      }
+    for (int q = 0; q < kUQ; ++q) {
+      mbar_init(&uq_full[q], 1);
+      mbar_init(&uq_empty[q], kUQConsumers);
     }
     fence_mbar_init();
   }
@@ -761,98 +640,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       s_end[i] = fp.up.tb.pos[i] + fp.up.tb.counts[i];
     }
   }
-  // work list: blocks of S experts, U0, [U1, D0], [U2, D1], ..., [U(K-1), D(K-2)], D(K-1)
-  // (U = up units of a group, D = its down units), so a group's H is re-read by its down
-  // units one up block later - while it is still in L2 - instead of after every expert's
-  // up units. S is chosen so an up block spans >= 2 waves of clusters (its down block
-  // then rarely waits); S = E gives the plain [all up][all down] order.
-  int* s_bstart = reinterpret_cast<int*>(
-      (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2 + 128;
   const int n_mp_up = (fp.up.n_mt + 1) / 2, n_mp_dn = (fp.dn.n_mt + 1) / 2;
   const int ncl = static_cast<int>(nclusters_x());
-  __syncthreads();   // s_pref complete (S below must be the same in every thread)
-  int S = E;
-  if (fp.interleave) {
-    const long long want = 2LL * ncl * E, per = static_cast<long long>(n_mp_up) * max(1, s_pref[E]);
-    const long long s0 = (want + per - 1) / per, smin = (E + 63) / 64;
-    S = static_cast<int>(s0 < smin ? smin : (s0 > E ? E : s0));
-  }
-  const int K = (E + S - 1) / S, nblk = 2 * K;
-  // dynamic unit queue (fp.dynamic): the leader's warp 2 takes units from a global
-  // counter in list order and hands each to every role of both CTAs through a kUQ-slot
-  // ring (slot value + full barrier in each CTA, empty barrier in the leader)
-  int* s_uq = s_bstart + (2 * E + 2);
-  uint64_t* uq_full = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(s_uq + kUQ) + 7) & ~static_cast<uintptr_t>(7));
-  uint64_t* uq_empty = uq_full + kUQ;
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int j = 0; j < nblk; ++j) {
-      s_bstart[j] = acc;
-      const bool dn = (j == nblk - 1) || (j > 0 && (j & 1) == 0);
-      const int g = j == 0 ? 0 : j == nblk - 1 ? K - 1 : dn ? j / 2 - 1 : (j + 1) / 2;
-      const int nch = s_pref[min((g + 1) * S, E)] - s_pref[g * S];
-      acc += nch * (dn ? n_mp_dn : n_mp_up);
-    }
-    s_bstart[nblk] = acc;
-  }
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch_dependents();
-  if (kT) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_ready));
-  if (warp >= 4 && fp.cp_src != nullptr) {
-    // Step 2 row copy, 8 expert-ordered rows per warp iteration (segments start on
-    // multiples of 32 rows, so a group never straddles experts), earliest rows
-    // first - the first units' experts are released first. A group is published
-    // with a release add on copied[e]; the token producer acquires it.
-    const int nw = gridDim.x * 4, gw = blockIdx.x * 4 + (warp - 4);
-    const int rv = fp.cp_row_vecs;
-    const int rows_end = s_off[E];
-    for (int q = gw; q * 8 < rows_end; q += nw) {
-      const int j0 = q * 8;
-      int lo = 0, hi = E;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_off[mid] <= j0) lo = mid; else hi = mid;
-      }
-      const int jend = s_end[lo];
-      if (j0 >= jend) continue;   // segment padding only
-      int tok[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) tok[r] = j0 + r < jend ? __ldg(fp.up.tb.perm_pad + j0 + r) : -1;
-      for (int c0 = 0; c0 < rv; c0 += 128) {
-        uint4 v[8][4];
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int col = c0 + lane + 32 * c;
-            if (tok[r] >= 0 && col < rv) v[r][c] = __ldg(fp.cp_src + static_cast<size_t>(tok[r]) * rv + col);
-          }
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int col = c0 + lane + 32 * c;
-            if (tok[r] >= 0 && col < rv) fp.cp_dst[static_cast<size_t>(j0 + r) * rv + col] = v[r][c];
-          }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        red_release_gpu_add(fp.up.tb.copied + lo, 1);
-      }
-    }
-  }
 
   // pair-units cover m-tiles (2q, 2q+1); with an odd count the last pair has
   // both CTAs on the same m-tile (the follower's copy is computed, not stored)
   const int chunks = s_pref[E];
   const int total_up = chunks * n_mp_up;
   const int total = total_up + chunks * n_mp_dn;
-  const int nkb_up = fp.up.K / (BK * KA), nkb_dn = fp.dn.K / (BK * KA);   // stages per unit
+  const int nkb_up = fp.up.K / BK, nkb_dn = fp.dn.K / BK;   // k-blocks per unit
   const int cid = static_cast<int>(cluster_id_x());
   const uint32_t leader_uq_empty = mapa_shared(smem_u32(uq_empty), 0);
   // k-th unit of this cluster: static round robin, or the k-th queue slot (dynamic)
@@ -867,6 +668,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       else mbar_arrive_cluster(leader_uq_empty + slot * 8);
     }
     return u;
+  };
+  // list position u -> (down?, decoded unit)
+  auto unit_at = [&](int u, bool& down) -> Unit {
+    down = u >= total_up;
+    return down ? decode(u - total_up, n_mp_dn, E, s_pref, s_off, s_end, s_cs)
+                : decode(u, n_mp_up, E, s_pref, s_off, s_end, s_cs);
   };
 
   if (warp == 2) {
@@ -895,31 +702,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // several token chunks: its sibling units read the same tile at nearly the same time,
     // and evict_first would let the trailing reader miss L2 and re-read it from DRAM
     const uint64_t pol_once = policy_evict_first();
-    const uint64_t pol_shared = fp.sibling_policy == 2 ? policy_evict_last()
-                                : fp.sibling_policy == 1 ? policy_evict_normal() : pol_once;
+    const uint64_t pol_shared = policy_evict_normal();
     const uint32_t leader_full = mapa_shared(smem_u32(fullA), 0);
     int stage = 0;
     uint32_t phase = 0;
     for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
-      const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
-      const bool down = lp.down;
-      const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
+      bool down;
+      const Unit w = unit_at(u, down);
       const int n_mt = down ? fp.dn.n_mt : fp.up.n_mt;
       const int nkb = down ? nkb_dn : nkb_up;
       const CUtensorMap* tm = down ? &tmA_dn : &tmA_up;
       const int mt = min(2 * w.mt + static_cast<int>(rank), n_mt - 1);
-      const int row0 = ((w.e * n_mt + mt) * nkb * KA) * BM;
+      const int row0 = ((w.e * n_mt + mt) * nkb) * BM;
       const uint64_t pol_w = (s_pref[w.e + 1] - s_pref[w.e] > 1) ? pol_shared : pol_once;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&emptyA[stage], phase ^ 1);
         const uint32_t fb = leader_full + stage * 8;
         if (elect_one()) {
-          if (leader) mbar_arrive_expect_tx(&fullA[stage], 2 * SA_BYTES);
+          if (leader) mbar_arrive_expect_tx(&fullA[stage], 2 * A_BYTES);
           else mbar_arrive_cluster(fb);
-#pragma unroll
-          for (int a = 0; a < KA; ++a)
-            tma_load_2d_2sm(tm, fb, sA + stage * SA_BYTES + a * A_BYTES, 0, row0 + (kb * KA + a) * BM,
-                            pol_w);
+          tma_load_2d_2sm(tm, fb, sA + stage * A_BYTES, 0, row0 + kb * BM, pol_w);
         }
         __syncwarp();
         if (++stage == AS) { stage = 0; phase ^= 1; }
@@ -927,54 +729,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 3) {
     // -------------------------------------------------------------- token producer (both CTAs)
-    // L2 policies of the activation reads (A/B knobs): X_perm rows (re-read by the up units'
-    // feature pair-tiles at nearly the same time) and H rows (read by the down units)
-    auto make_pol = [](int k) {
-      return k == 0 ? policy_evict_first() : k == 1 ? policy_evict_normal() : policy_evict_last();
-    };
-    const uint64_t pol_xp = make_pol(fp.xpol), pol_h = make_pol(fp.hpol);
+    // X_perm rows (re-read by the up units' feature pair-tiles at nearly the same time) and
+    // H rows (read by the down units) are kept in L2 (evict_last, persisting set-aside)
+    const uint64_t pol_x = policy_evict_last();
     if (fp.early_tables) griddep_wait();   // X_perm rows and the route records are complete
     const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
-    int* s_rows = reinterpret_cast<int*>(
-        (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + 4 * 512 / 2;
     int stage = 0;
     uint32_t phase = 0;
-    // cp.async gather (fp.up.gather_cp): a stage is published to the MMA (arrive on
-    // the leader's full barrier) kGD stages after its copies were issued, once they
-    // have landed and been fenced for the tensor core; npend stages are in flight
-    const int kGD = fp.up.gather_depth;   // 1 .. BS - 1
-    int npend = 0;
-    auto publish_oldest = [&]() {
-      fence_proxy_async_shared();
-      __syncwarp();
-      const int st = (stage - npend + BS) % BS;
-      if (elect_one()) {
-        if (leader) mbar_arrive(&fullB[st]);
-        else mbar_arrive_cluster(leader_full + st * 8);
-      }
-      __syncwarp();
-      --npend;
-    };
-    auto drain = [&]() {
-      cp_async_wait<0>();
-      while (npend > 0) publish_oldest();
-    };
     for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
-      const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
-      const bool down = lp.down;
-      const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
+      bool down;
+      const Unit w = unit_at(u, down);
       const int nkb = down ? nkb_dn : nkb_up;
       const CUtensorMap* tm = down ? &tmB_dn : &tmB_up;
-      const uint64_t pol_x = down ? pol_h : pol_xp;
-      if (down && npend > 0) drain();
-      if (!down && fp.cp_src != nullptr) {   // this expert's rows copied into X_perm? (acquire)
-        const int target = (s_end[w.e] - s_off[w.e] + 7) / 8;
-        if (elect_one()) {
-          while (ld_acquire_gpu(fp.up.tb.copied + w.e) < target) __nanosleep(64);
-          fence_proxy_async_global();
-        }
-        __syncwarp();
-      }
       if (down) {   // H rows of this token chunk complete? (acquire), then order the TMA after it
         const int target = 2 * n_mp_up;   // both CTAs of every up pair-unit of (e, chunk)
         if (elect_one()) {
@@ -993,77 +759,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int half = ((w.ntok + 31) & ~31) / 2;
       const int nb = half / B2_BOX;
       const int r0 = w.tok0 + static_cast<int>(rank) * half;
-      const bool gather = !down && fp.up.gather != nullptr;
-      const bool mn = down && fp.dn.ht;   // H^T: MN-major token tile, 64-token x 64-feature boxes
-      const int nbx = (half + 63) / 64;
-      const uint32_t stage_bytes = KA * (mn ? nbx * 8192 : nb * B2_BOX * BK * 2);
-      const bool gcp = gather && fp.up.gather_cp;
-      if (gather) {   // this CTA's token ids for the unit (padding rows: row 0 for gather4,
-        __syncwarp(); // -1 = zero fill for cp.async; masked in the epilogue either way)
-        for (int i = lane; i < half; i += 32)
-          s_rows[i] = (r0 + i < w.tok0 + w.ntok) ? __ldg(fp.up.gather + r0 + i) : (gcp ? -1 : 0);
-        __syncwarp();
-      }
-      if (gcp) {
-        // rows of x_all gathered by 16-B cp.async into the 128-B-swizzled K-major image:
-        // row i, 16-B chunk c -> i * 128 + ((c ^ (i & 7)) * 16); 4 rows per warp instruction
-        const int c = lane & 7;
-        const __nv_bfloat16* src0 = fp.up.gsrc + c * 8;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&emptyB[stage], phase ^ 1);
-          const uint32_t dst0 = smem_u32(sB + stage * SB_BYTES);
-          for (int i = lane >> 3; i < half; i += 4) {
-            const int row = s_rows[i];
-            cp_async_16(dst0 + i * 128 + ((c ^ (i & 7)) << 4),
-                        src0 + static_cast<size_t>(row < 0 ? 0 : row) * fp.up.K + kb * BK,
-                        row < 0 ? 0u : 16u, pol_x);
-          }
-          cp_async_commit();
-          ++npend;
-          if (++stage == BS) { stage = 0; phase ^= 1; }
-          if (npend > kGD) {
-            switch (kGD) {   // cp.async.wait_group takes an immediate
-              case 1: cp_async_wait<1>(); break;
-              case 2: cp_async_wait<2>(); break;
-              case 3: cp_async_wait<3>(); break;
-              case 4: cp_async_wait<4>(); break;
-              default: cp_async_wait<5>(); break;
-            }
-            publish_oldest();
-          }
-        }
-        continue;
-      }
+      const uint32_t stage_bytes = nb * B2_BOX * BK * 2;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&emptyB[stage], phase ^ 1);
         const uint32_t fb = leader_full + stage * 8;
         if (elect_one()) {
           if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * stage_bytes);
           else mbar_arrive_cluster(fb);
-          if (gather) {
-            // .shared::cta form: the leader's barrier is addressed by clearing the peer bit
-            const uint32_t fb_cta = smem_u32(&fullB[stage]) & 0xFEFFFFFFu;
-            for (int a = 0; a < KA; ++a)
-              for (int i = 0; i < half; i += 4)
-                tma_gather4_2sm(tm, fb_cta, sB + stage * SB_BYTES + a * B2_BYTES + i * (BK * 2),
-                                (kb * KA + a) * BK, *reinterpret_cast<const int4*>(s_rows + i), pol_x);
-          } else if (mn) {
-            for (int a = 0; a < KA; ++a)
-              for (int j = 0; j < nbx; ++j)
-                tma_load_2d_2sm(tm, fb, sB + stage * SB_BYTES + a * B2_BYTES + j * 8192, r0 + 64 * j,
-                                (kb * KA + a) * BK, pol_x);
-          } else {
-            for (int a = 0; a < KA; ++a)
-              for (int i = 0; i < nb; ++i)
-                tma_load_2d_2sm(tm, fb, sB + stage * SB_BYTES + a * B2_BYTES + i * (B2_BOX * BK * 2),
-                                (kb * KA + a) * BK, r0 + i * B2_BOX, pol_x);
-          }
+          for (int i = 0; i < nb; ++i)
+            tma_load_2d_2sm(tm, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
+                            r0 + i * B2_BOX, pol_x);
         }
         __syncwarp();
         if (++stage == BS) { stage = 0; phase ^= 1; }
       }
     }
-    if (npend > 0) drain();
   } else if (warp == 1) {
     if (leader) {
       // ------------------------------------------------------------ MMA issuer (leader only)
@@ -1071,36 +781,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t pa = 0, pb = 0;
       int as = 0;
       uint32_t aphase = 0;
-      long long t_a = 0, t_b = 0, t_t = 0, t_all = clock64(), t_first_down = 0;
-      int n_up = 0, n_dn = 0, kb_total = 0;
       for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
-        const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
-        const bool down = lp.down;
-        if (kT) { if (down) { if (!n_dn) t_first_down = clock64() - t_all; ++n_dn; } else ++n_up; }
-        const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
+        bool down;
+        const Unit w = unit_at(u, down);
         const int nkb = down ? nkb_dn : nkb_up;
         const int nmma = (w.ntok + 31) & ~31;
-        const bool mn = down && fp.dn.ht;
-        const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma, mn);
-        const uint32_t bstep = mn ? 128 : 2;   // K=16 step: 16 rows x 128 B (MN) or 32 B (K)
-        if (kT) { TWAIT(t_t, mbar_wait(&tempty[as], aphase ^ 1)); } else mbar_wait(&tempty[as], aphase ^ 1);
+        const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
+        mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + as * BN_MAX;
-        if (kT) kb_total += nkb;
         for (int kb = 0; kb < nkb; ++kb) {
-          if (kT) { TWAIT(t_b, mbar_wait(&fullB[sb], pb)); TWAIT(t_a, mbar_wait(&fullA[sa], pa)); }
-          else { mbar_wait(&fullB[sb], pb); mbar_wait(&fullA[sa], pa); }
+          mbar_wait(&fullB[sb], pb);
+          mbar_wait(&fullA[sa], pa);
           tc_fence_after();
           if (elect_one()) {
+            const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
+            const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B2_BYTES));
 #pragma unroll
-            for (int a = 0; a < KA; ++a) {
-              const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * SA_BYTES + a * A_BYTES));
-              const uint32_t baddr = smem_u32(sB + sb * SB_BYTES + a * B2_BYTES);
-              const uint64_t bd = mn ? smem_desc_mn_sw128(baddr, 8192) : smem_desc_k_sw128(baddr);
-#pragma unroll
-              for (int k = 0; k < BK / 16; ++k)
-                mma_bf16_ss_2sm(d, ad + 2 * k, bd + bstep * k, idesc, (kb | a | k) != 0);
-            }
+            for (int kk = 0; kk < BK / 16; ++kk)
+              mma_bf16_ss_2sm(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
             mma_commit_2sm(&emptyA[sa], 0x3);
             mma_commit_2sm(&emptyB[sb], 0x3);
           }
@@ -1113,29 +812,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         as ^= 1;
         if (as == 0) aphase ^= 1;
       }
-      if (kT && lane == 0) {
-        uint64_t g_end;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
-        printf("[ffn c%02d] up %d dn %d kb %d total %lld first_down %lld waitA %lld waitB %lld waitT %lld "
-               "g_entry %llu g_ready %llu g_end %llu\n",
-               cid, n_up, n_dn, kb_total, clock64() - t_all, t_first_down, t_a, t_b, t_t,
-               (unsigned long long)g_entry, (unsigned long long)g_ready, (unsigned long long)g_end);
-      }
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
     const int wq = warp & 3;
-    __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(
-        (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15)) + wq * 512;
+    __nv_bfloat16* stage = s_stage + wq * 512;
     const uint64_t pol_keep = policy_evict_last();
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
     if (fp.early_tables) griddep_wait();   // perm / route of the grouping launch
     int as = 0;
     uint32_t aphase = 0;
     for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
-      const ListPos lp = locate(u, s_bstart, nblk, S, s_pref, n_mp_up, n_mp_dn);
-      const bool down = lp.down;
-      const Unit w = decode(lp.idx, down ? n_mp_dn : n_mp_up, E, s_pref, s_off, s_end, s_cs);
+      bool down;
+      const Unit w = unit_at(u, down);
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const int mt = 2 * w.mt + static_cast<int>(rank);
@@ -1154,8 +843,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (!down) {   // publish this CTA's H tile of the chunk
         // bar.sync orders every epilogue thread's H stores before thread 0's release
         // (cumulative at gpu scope), so the other warps need no fence of their own and
-        // go straight on to the next tile (light_release; else every thread fences first)
-        if (!fp.light_release) __threadfence();
+        // go straight on to the next tile
         asm volatile("bar.sync 2, 128;" ::: "memory");   // the 4 epilogue warps
         if (wq == 0 && lane == 0) red_release_gpu_add(fp.done + w.chunk, 1);
       }
@@ -1176,138 +864,68 @@ size_t smem_bytes(int E, int as, int bs) {
          16 + 4 * 1024;
 }
 
-template <bool kDown, int AS, int BS, int kMode = 0>
-cudaError_t launch_v(const CUtensorMap& tmB, const TcParams& p, int grid, cudaStream_t s) {
-  const size_t sm = smem_bytes(p.E, AS, BS);
+size_t smem_bytes_2sm(int E, int as, int bs) {
+  return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (4 * E + 2) * 4 +
+         16 + 4 * 1024 + 96;   // + epilogue staging + unit queue
+}
+
+template <bool kDown, int AS, int BS>
+cudaError_t launch_1sm(const CUtensorMap& tmB, const TcParams& p, int grid, cudaStream_t s) {
   static PerDeviceOnce attr;  // per template instance and device
   if (attr.need()) {
-    cudaError_t e = cudaFuncSetAttribute(tc_grouped_gemm<kDown, AS, BS, kMode>,
+    cudaError_t e = cudaFuncSetAttribute(tc_grouped_gemm<kDown, AS, BS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem_bytes(kMaxExperts, AS, BS)));
     if (e != cudaSuccess) return e;
     attr.done();
   }
-  tc_grouped_gemm<kDown, AS, BS, kMode><<<grid, kThreads, sm, s>>>(tmB, p);
+  tc_grouped_gemm<kDown, AS, BS><<<grid, kThreads, smem_bytes(p.E, AS, BS), s>>>(tmB, p);
   return cudaGetLastError();
 }
 
-// ring depths (A stages x 16 KB, B stages x 32 KB); MOESHARD_TC_VARIANT selects for experiments
-int variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MOESHARD_TC_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
-size_t smem_bytes_2sm(int E, int as, int bs) {
-  return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (4 * E + 2) * 4 +
-         16 + 4 * 1024 + 128 * 4 + (2 * E + 2) * 4 + 96;   // + staging + gather row ids + block
-                                                            // starts + unit queue
-}
-
-template <bool kDown, int AS, int BS, bool kT = false>
+template <bool kDown, int AS, int BS>
 cudaError_t launch_2sm(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcParams& p, int grid,
                        cudaStream_t s) {
   static PerDeviceOnce attr;
   if (attr.need()) {
-    cudaError_t e = cudaFuncSetAttribute(tc_grouped_gemm_2sm<kDown, AS, BS, kT>,
+    cudaError_t e = cudaFuncSetAttribute(tc_grouped_gemm_2sm<kDown, AS, BS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem_bytes_2sm(kMaxExperts, AS, BS)));
     if (e != cudaSuccess) return e;
     attr.done();
   }
-  tc_grouped_gemm_2sm<kDown, AS, BS, kT><<<grid & ~1, kThreads, smem_bytes_2sm(p.E, AS, BS), s>>>(
+  tc_grouped_gemm_2sm<kDown, AS, BS><<<grid & ~1, kThreads, smem_bytes_2sm(p.E, AS, BS), s>>>(
       tmA, tmB, p);
   return cudaGetLastError();
 }
 
+// ring depths: (6, 6) for the CTA pair (A 16 KB, B 16 KB stages), (4, 4) for one CTA
+// (B 32 KB stages); profiles/r01_gemm_experiments.md §3
 template <bool kDown>
 cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmB2,
                      const TcParams& p, int grid, cudaStream_t s) {
-  if (p.n_mt % 2 == 0 && variant() == 0) return launch_2sm<kDown, 6, 6>(tmA, tmB2, p, grid, s);
-  if (p.n_mt % 2 == 0 && variant() == 11) return launch_2sm<kDown, 6, 6, true>(tmA, tmB2, p, grid, s);
-  if (p.n_mt % 2 == 0 && variant() == 12) return launch_2sm<kDown, 8, 4>(tmA, tmB2, p, grid, s);
-  if (p.n_mt % 2 == 0 && variant() == 13) return launch_2sm<kDown, 9, 3>(tmA, tmB2, p, grid, s);
-  if (p.n_mt % 2 == 0 && variant() == 14) return launch_2sm<kDown, 7, 5>(tmA, tmB2, p, grid, s);
-  if (p.n_mt % 2 == 0 && variant() == 15) return launch_2sm<kDown, 10, 2>(tmA, tmB2, p, grid, s);
-  switch (variant()) {
-    case 1: return launch_v<kDown, 4, 3>(tmB, p, grid, s);
-    case 2: return launch_v<kDown, 4, 4>(tmB, p, grid, s);
-    case 3: return launch_v<kDown, 2, 5>(tmB, p, grid, s);
-    case 4: return launch_v<kDown, 9, 2>(tmB, p, grid, s);
-    case 5: return launch_v<kDown, 4, 4, 1>(tmB, p, grid, s);
-    case 6: return launch_v<kDown, 4, 4, 2>(tmB, p, grid, s);
-    case 8: return launch_v<kDown, 4, 4, 3>(tmB, p, grid, s);
-    case 9: return launch_v<kDown, 4, 4, 4>(tmB, p, grid, s);
-    case 10: return launch_v<kDown, 4, 4, 5>(tmB, p, grid, s);
-    default: return launch_v<kDown, 4, 4>(tmB, p, grid, s);
-  }
+  if (p.n_mt % 2 == 0) return launch_2sm<kDown, 6, 6>(tmA, tmB2, p, grid, s);
+  return launch_1sm<kDown, 4, 4>(tmB, p, grid, s);
 }
 
-}  // namespace
-
-namespace {
-template <int AS, int BS, int KA, bool kT = false>
-cudaError_t launch_fused(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
-                         const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn, const TcParams& up,
-                         const TcParams& dn, int32_t* done, const void* cp_src, void* cp_dst,
-                         int cp_row_vecs, bool dynamic, bool early_tables, int grid, cudaStream_t s) {
-  static PerDeviceOnce attr;
-  if (attr.need()) {
-    cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS, KA, kT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_bytes_2sm(kMaxExperts, AS * KA, BS * KA)));
-    if (e != cudaSuccess) return e;
-    attr.done();
-  }
-  static const bool inter = [] {   // opt-in: measured slower for C2 / C5, faster for C3 only
-    const char* e = getenv("MOESHARD_FFN_INTERLEAVE");
-    return e && e[0] == '1';
-  }();
-  static const int sib = [] {   // MOESHARD_SIBLING_POLICY=first|normal|last (A/B)
-    const char* e = getenv("MOESHARD_SIBLING_POLICY");
-    return e ? (e[0] == 'f' ? 0 : e[0] == 'l' ? 2 : 1) : 1;
-  }();
-  static const int xpol = [] {   // MOESHARD_XPOL / MOESHARD_HPOL = first|normal|last (A/B)
-    const char* e = getenv("MOESHARD_XPOL");
-    return e ? (e[0] == 'f' ? 0 : e[0] == 'n' ? 1 : 2) : 2;
-  }();
-  static const int hpol = [] {
-    const char* e = getenv("MOESHARD_HPOL");
-    return e ? (e[0] == 'f' ? 0 : e[0] == 'n' ? 1 : 2) : 2;
-  }();
-  static const bool light = [] {
-    const char* e = getenv("MOESHARD_LIGHT_RELEASE");
-    return !(e && e[0] == '0');
-  }();
-  static const int dyn_env = [] {   // MOESHARD_FFN_SCHED=dynamic|static overrides the flag
-    const char* e = getenv("MOESHARD_FFN_SCHED");
-    return e ? (e[0] == 'd' ? 1 : 0) : -1;
-  }();
-  FusedParams fp{up, dn, done, static_cast<const uint4*>(cp_src), static_cast<uint4*>(cp_dst),
-                 cp_row_vecs, inter, dyn_env >= 0 ? dyn_env == 1 : dynamic, sib, xpol, hpol,
-                 early_tables && cp_src == nullptr, light};
-  return launch_pdl(tc_moe_ffn_2sm<AS, BS, KA, kT>, dim3(grid & ~1), dim3(kThreads),
-                    smem_bytes_2sm(up.E, AS * KA, BS * KA), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
-}
 }  // namespace
 
 cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
-                              const TcParams& up, const TcParams& dn, int32_t* done,
-                              const void* cp_src, void* cp_dst, int cp_row_vecs, bool dynamic,
+                              const TcParams& up, const TcParams& dn, int32_t* done, bool dynamic,
                               bool early_tables, int grid, cudaStream_t s) {
-  // MOESHARD_TC_VARIANT 20: two k-atoms per ring stage (3 + 3 stages of 32 KB)
-  if (variant() == 21)
-    return launch_fused<6, 6, 1, true>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src,
-                                       cp_dst, cp_row_vecs, dynamic, early_tables, grid, s);
-  if (variant() == 20 && up.K % 128 == 0 && dn.K % 128 == 0 && !up.gather_cp)
-    return launch_fused<3, 3, 2>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src, cp_dst,
-                                 cp_row_vecs, dynamic, early_tables, grid, s);
-  return launch_fused<6, 6, 1>(tmA_up, tmB_up, tmA_dn, tmB_dn, up, dn, done, cp_src, cp_dst,
-                               cp_row_vecs, dynamic, early_tables, grid, s);
+  constexpr int AS = 6, BS = 6;
+  static PerDeviceOnce attr;
+  if (attr.need()) {
+    cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem_bytes_2sm(kMaxExperts, AS, BS)));
+    if (e != cudaSuccess) return e;
+    attr.done();
+  }
+  FusedParams fp{up, dn, done, dynamic, early_tables};
+  return launch_pdl(tc_moe_ffn_2sm<AS, BS>, dim3(grid & ~1), dim3(kThreads),
+                    smem_bytes_2sm(up.E, AS, BS), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
 }
 
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,

@@ -1,8 +1,7 @@
 // group.cuh - device pieces of Step 2 groupPerExpert and the
 // Sec. 3.3 per-expert concatenation shared by the grouping
-// kernels of permute.cu and the fused route+group kernel of router.cu:
-// a CTA-wide exclusive scan, the per-forward segment tables, the stable
-// in-block rank of a token, and a grid-wide barrier for co-resident grids.
+// kernels of permute.cu: a CTA-wide exclusive scan, the per-forward segment
+// tables and the stable in-block rank of a token.
 #pragma once
 
 #include "common.cuh"
@@ -79,7 +78,6 @@ __device__ __forceinline__ void segment_tables(int E, const int* s_tot, const in
     block_excl_scan<kThreads>(rows, s_warp, tot_rows);
     for (int i = threadIdx.x; i < tot_tc; i += kThreads) tb.done[i] = 0;   // per token chunk
     if (e < E) {
-      tb.copied[e] = 0;
       tb.pos[e] = pos;
       tb.counts[e] = cnt;
       tb.tc_chunk_size[e] = cs;
@@ -98,27 +96,6 @@ __device__ __forceinline__ void segment_tables(int E, const int* s_tot, const in
       tb.stats[2] = tot_rows * n_mt_up_tc;
     }
   }
-}
-
-// Grid-wide barrier for a grid whose CTAs are all co-resident (grid <= SMs at
-// one CTA per SM). Self-resetting and launch-argument free, so it survives
-// CUDA-graph replay: bar[0] = arrivals, bar[1] = generation.
-__device__ __forceinline__ void grid_barrier(int32_t* bar, int nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile int32_t* gen = bar + 1;
-    const int g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1) == nblocks - 1) {
-      atomicExch(bar, 0);
-      __threadfence();
-      atomicAdd(bar + 1, 1);
-    } else {
-      while (ptx::ld_acquire_gpu(bar + 1) == g) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
 }
 
 }  // namespace moeshard

@@ -119,7 +119,12 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
   return r == CUDA_SUCCESS;
 }
 
-constexpr int kL2PersistDefaultMB = 64;   // measured best of 0/32/48/64/79 MB on c2
+constexpr int kRouterTok = 128;    // tokens per tcgen05 router CTA (= TMEM lanes)
+constexpr int kL2PersistMB = 64;   // measured best of 0/32/48/64/79 MB on c2
+constexpr uint32_t kKnownFlags =
+    MOESHARD_FLAG_FORCE_COLLECTIVES | MOESHARD_FLAG_SIMT_GEMM | MOESHARD_FLAG_UNFUSED_GEMM |
+    MOESHARD_FLAG_NO_L2_PERSIST | MOESHARD_FLAG_DYNAMIC_SCHED | MOESHARD_FLAG_UNEVEN_TOKENS |
+    MOESHARD_FLAG_P2P | MOESHARD_FLAG_SERIAL_AG;
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -150,7 +155,9 @@ Layout make_layout(const moeshard_config& c, int world) {
   L.route = take(Nmax * sizeof(RouteRec));
   L.block_hist = take(nb * E * 4);
   L.block_base = take(nb * E * 4);
-  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + E + (E + 1) + E + 4 + 1);
+  // counts, offsets, tc_chunk_pref, tc_chunk_size, simt_chunk_pref, stats[8], block_tot, pos,
+  // next_unit
+  L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + (E + 1) + 1);
   L.npad = (Nmax + kSegAlign * E + 63) / 64 * 64;
   L.ints = take(L.n_ints * 4);
   L.done = take((Nmax / kTcTokTile + E + 8) * 4);   // per token chunk: <= N/256 + E chunks
@@ -182,17 +189,16 @@ struct moeshard_ctx {
   char* ws = nullptr;
   RouteRec* route = nullptr;
   int32_t *block_hist = nullptr, *block_base = nullptr, *block_tot = nullptr, *perm = nullptr;
-  int32_t* gsync = nullptr;
   Tables tb{};
   void *x_all = nullptr, *x_perm = nullptr, *H = nullptr, *partial = nullptr;
-  CUtensorMap tm_xperm{}, tm_H{}, tm_xperm16{}, tm_H16{}, tm_Ht{}, tm_wt_r{};
+  CUtensorMap tm_xperm{}, tm_H{}, tm_xperm16{}, tm_H16{}, tm_wt_r{};
   void* wt_r = nullptr;
   int EP = 16;
   std::vector<LayerW> layers;
   ncclComm_t comm = nullptr;
   // Step 3 token AllGather overlapped with Step 1 (x does not depend on the routing): the
   // AllGather of x runs on s_x, forked from the caller's stream before the router and joined
-  // after the metadata AllGather (MOESHARD_OVERLAP_AG=0: everything on the caller's stream)
+  // after the metadata AllGather (MOESHARD_FLAG_SERIAL_AG: everything on the caller's stream)
   bool overlap_ag = true;
   cudaStream_t s_x = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -205,11 +211,6 @@ struct moeshard_ctx {
   std::vector<void*> ipc_opened;
   int last_n = 0;
   int64_t launches = 0;  // cumulative kernel launches of this context
-  long long pf_bytes = 0;  // experimental L2 weight prefetch during routing (MOESHARD_L2_PREFETCH_MB)
-  int gather_depth = 4;    // cp.async gather: stages in flight (MOESHARD_GATHER_DEPTH, 1..5)
-  int router_tok = 128;    // tokens per tcgen05 router CTA (MOESHARD_ROUTER_TOK: 64 or 128)
-  bool early_tables = true;   // FFN weight stream starts on the grouping launch's table flag
-                              // (MOESHARD_EARLY_TABLES=0: whole-grid dependency)
   // phase profiling (measurement only)
   bool prof = false;
   static constexpr int kRing = 1024, kEv = 7;
@@ -293,6 +294,9 @@ int validate(const moeshard_config* c, int world) {
     return fail(nullptr, MOESHARD_ERR_CONFIG, "d_ff/world=%d must be a multiple of 128",
                 c->d_ff / world);
   if (c->n_layers < 1) return fail(nullptr, MOESHARD_ERR_CONFIG, "n_layers=%d < 1", c->n_layers);
+  if (c->flags & ~kKnownFlags)
+    return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "flags=0x%x has unknown bits (0x%x)", c->flags,
+                c->flags & ~kKnownFlags);
   if ((c->flags & MOESHARD_FLAG_P2P) &&
       (c->dtype != MOESHARD_BF16 || world > kMaxWorld ||
        (c->flags & (MOESHARD_FLAG_SIMT_GEMM | MOESHARD_FLAG_UNFUSED_GEMM | MOESHARD_FLAG_FORCE_COLLECTIVES))))
@@ -387,7 +391,6 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
 
   auto* c = new moeshard_ctx();
   c->cfg = *cfg;
-  if (const char* fl = getenv("MOESHARD_FLAGS")) c->cfg.flags |= static_cast<uint32_t>(atoi(fl));
   c->rank = rank;
   c->world = world;
   c->device = device;
@@ -400,17 +403,11 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   // coll: tokens of all ranks are exchanged (rank-major x_all / route / hist buffers)
   c->coll = world > 1 || (c->cfg.flags & MOESHARD_FLAG_FORCE_COLLECTIVES) || c->p2p;
   c->use_tc = cfg->dtype == MOESHARD_BF16 && !(c->cfg.flags & MOESHARD_FLAG_SIMT_GEMM);
-  if (const char* pf = getenv("MOESHARD_L2_PREFETCH_MB")) c->pf_bytes = atoll(pf) << 20;
-  if (c->cfg.flags & MOESHARD_FLAG_ROUTER_TOK64) c->router_tok = 64;
-  if (const char* et = getenv("MOESHARD_EARLY_TABLES")) c->early_tables = atoi(et) != 0;
-  if (const char* rt = getenv("MOESHARD_ROUTER_TOK")) c->router_tok = atoi(rt) == 64 ? 64 : 128;
-  if (const char* gd = getenv("MOESHARD_GATHER_DEPTH")) c->gather_depth = std::max(1, std::min(5, atoi(gd)));
   // L2 set-aside for the kernels' evict_last lines (H between the two products, the
   // expert-ordered token rows re-read by every feature tile): without it the
   // 128-B-line hints lose to the weight stream. Raised, never lowered; device-wide.
   if (c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_NO_L2_PERSIST)) {
-    size_t want = static_cast<size_t>(kL2PersistDefaultMB) << 20, cur = 0;
-    if (const char* pl = getenv("MOESHARD_L2_PERSIST_MB")) want = static_cast<size_t>(atoll(pl)) << 20;
+    size_t want = static_cast<size_t>(kL2PersistMB) << 20, cur = 0;
     want = std::min(want, static_cast<size_t>(prop.persistingL2CacheMaxSize));
     if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur < want)
       cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
@@ -432,11 +429,9 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->tb.simt_chunk_pref = c->tb.tc_chunk_size + E;
   c->tb.stats = c->tb.simt_chunk_pref + (E + 1);
   c->tb.done = reinterpret_cast<int32_t*>(c->ws + L.done);
-  c->block_tot = c->tb.stats + 8 + E;
+  c->block_tot = c->tb.stats + 8;
   c->tb.pos = c->block_tot + E;
-  c->tb.copied = c->tb.pos + (E + 1);
-  c->gsync = c->tb.copied + E;   // 4 ints: the grouping launch's ticket / scan / exit counters
-  c->tb.next_unit = c->gsync + 4;
+  c->tb.next_unit = c->tb.pos + (E + 1);
   c->tb.perm_pad = reinterpret_cast<int32_t*>(c->ws + L.perm_pad);
   c->perm = reinterpret_cast<int32_t*>(c->ws + L.perm);
   c->x_all = c->coll && !c->p2p ? c->ws + L.x_all : nullptr;
@@ -457,7 +452,6 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
         !make_tmap(&c->tm_H, c->H, c->F, np, 32) ||
         !make_tmap(&c->tm_xperm16, c->x_perm, c->h, np, 16) ||
         !make_tmap(&c->tm_H16, c->H, c->F, np, 16) ||
-        !make_tmap(&c->tm_Ht, c->H, np, c->F, 64) ||   // H^T [F][npad], 64 tokens x 64 features
         !make_tmap(&c->tm_wt_r, c->wt_r, c->h, c->EP, c->EP)) {
       delete c;
       return fail(nullptr, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
@@ -505,7 +499,7 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
       delete c;
       return fail(nullptr, MOESHARD_ERR_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
     }
-    if (const char* ov = getenv("MOESHARD_OVERLAP_AG")) c->overlap_ag = atoi(ov) != 0;
+    c->overlap_ag = !(c->cfg.flags & MOESHARD_FLAG_SERIAL_AG);
     if (c->overlap_ag &&
         (cudaStreamCreateWithFlags(&c->s_x, cudaStreamNonBlocking) != cudaSuccess ||
          cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -578,6 +572,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
                 c->cfg.max_tokens_per_rank);
   if (n > 0 && (!hidden || !router_w || !hidden_out))
     return fail(c, MOESHARD_ERR_INVALID_ARG, "NULL hidden/router_w/hidden_out");
+  CUDA_TRY(c, cudaSetDevice(c->device));   // kernel attributes and launches target this device
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const LayerW& lw = c->layers[layer];
   const int h = c->h, F = c->F, E = c->E;
@@ -608,54 +603,24 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   }
   // Step 1: route local tokens
   RouteRec* my_route = c->route + (c->coll ? static_cast<size_t>(c->rank) * ns : 0);
-  // tokens per hist-block = tokens per router CTA (64 for the SIMT router; the
-  // tcgen05 router runs 64 or 128 token rows per CTA, c->router_tok)
-  const int HB = c->use_tc ? c->router_tok : 64;
+  // tokens per hist-block = tokens per router CTA (128 for the tcgen05 router, 64 for SIMT)
+  const int HB = c->use_tc ? kRouterTok : 64;
   const int nbr_own = (n + HB - 1) / HB;                // hist-blocks this rank's router fills
   const int nbr = (ns + HB - 1) / HB;                   // hist-blocks per rank slot
   const int NB = (c->coll ? c->world : 1) * nbr;
-  const int N = (c->coll ? c->world : 1) * ns;            // token slots of all ranks
   int32_t* my_hist = c->block_hist + (c->coll ? static_cast<size_t>(c->rank) * nbr * E : 0);
   const bool fused = c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_UNFUSED_GEMM) &&
                      F % kTcFeatTile == 0 && h % kTcFeatTile == 0;   // odd tile counts: see FFN kernel
-  // token rows gathered by the FFN itself (no X_perm copy): TMA gather4 or cp.async
-  const bool gather_cp = fused && (c->cfg.flags & MOESHARD_FLAG_CPASYNC_GATHER);
-  const bool gather = fused && ((c->cfg.flags & MOESHARD_FLAG_TMA_GATHER) || gather_cp);
-  // opt-in: the Sec. 3.3 row copy inside the FFN launch (per-expert hand-off); measured
-  // slower than copying in the grouping launch (the copy's HBM bytes stay on the path)
-  const bool copy_in_ffn = fused && !gather && (c->cfg.flags & MOESHARD_FLAG_ROW_COPY_IN_FFN);
-  // world = 1: the router launch also runs Step 2 (grid barriers need every CTA resident)
-  const bool route_group = c->use_tc && !c->coll && (E % 8) == 0 && nbr <= c->num_sms &&
-                           h <= 1024 && c->pf_bytes == 0 && HB == 128 &&
-                           (c->cfg.flags & MOESHARD_FLAG_FUSED_ROUTE_GROUP);
   if (!st_route || n == 0) {
     // (routing ran in an earlier call, or this rank has no tokens this time)
-  } else if (route_group) {
-    CUtensorMap tm_x, tm_w;
-    if (!make_tmap(&tm_x, hidden, h, n, 128) || !make_tmap(&tm_w, router_w, E, h, 64))
-      return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden/router_w");
-    RouteGroupArgs ga{c->tb, c->block_base, c->block_tot, c->perm,
-                      static_cast<const uint4*>(hidden),
-                      gather || copy_in_ffn ? nullptr : static_cast<uint4*>(c->x_perm),
-                      h * c->elt / 16,
-                      F / kTcFeatTile, h / kTcFeatTile, c->tb.stats + 4};
-    CUDA_TRY(c, launch_route_group_tc(tm_x, tm_w, n, h, E, c->EP, forced, my_route, my_hist,
-                                      err_flag, ga, s));
-    c->launches += 1;
   } else if (c->use_tc) {
     CUtensorMap tm_x, tm_w;
     const bool mn = (E % 8) == 0;
     if (!make_tmap(&tm_x, hidden, h, n, HB) ||
         (mn && !make_tmap(&tm_w, router_w, E, h, 64)))
       return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden/router_w");
-    // L2 prefetch of the first up-projection tiles on the SMs the router leaves idle
-    const int tiles = (n + HB - 1) / HB;
-    const int pf_ctas = c->pf_bytes > 0 ? std::max(0, std::min(c->num_sms - tiles, 96)) : 0;
-    const long long pf_bytes =
-        std::min<long long>(c->pf_bytes, static_cast<long long>(E) * F * h * c->elt);
     CUDA_TRY(c, launch_router_tc(tm_x, mn ? tm_w : c->tm_wt_r, mn, router_w, c->wt_r, n, h, E,
-                                 c->EP, forced, my_route, my_hist, err_flag, lw.wt_in, pf_bytes,
-                                 pf_ctas, HB, s));
+                                 c->EP, forced, my_route, my_hist, err_flag, s));
     c->launches += mn ? 1 : 2;
   } else {
     launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, my_hist, err_flag, s);
@@ -692,35 +657,19 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
       CUDA_TRY(c, launch_p2p_wait_tokens(c->pa, err_flag, s));
       c->launches += 1;
     }
-    CUtensorMap tm_xg;   // x_all rows for TMA gather4 (box {64, 1})
-    if (gather && !gather_cp && !make_tmap(&tm_xg, x_all, h, N, 1))
-      return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for the gather map");
-    // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs (the row
-    // copy is skipped when the FFN gathers rows itself)
-    if (!route_group) {
-      // opt-in: one launch (block scans inside, ticket-ordered); measured ~2 us slower than
-      // the scan launch + PDL (the ticket atomic and the spin sit on the critical path)
-      const bool one = (c->cfg.flags & MOESHARD_FLAG_FUSED_SCAN) != 0;
-      launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb,
-                          F / kTcFeatTile, h / kTcFeatTile, c->route, x_all, ns, nbr, HB,
-                          h * c->elt, c->perm, gather || copy_in_ffn ? nullptr : c->x_perm,
-                          one ? c->gsync : nullptr, s);
-      c->launches += one ? 1 : 2;
-    }
+    // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs
+    launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb,
+                        F / kTcFeatTile, h / kTcFeatTile, c->route, x_all, ns, nbr, HB,
+                        h * c->elt, c->perm, c->x_perm, s);
+    c->launches += 2;
     c->mark(3, s);
     // Step 4: expert computation, one grouped product per projection
     void* P = c->coll && !c->p2p ? c->partial : hidden_out;
     if (fused) {
-      // MOESHARD_FLAG_H_TRANSPOSED (experimental): H stored as H^T [F][npad]; the up
-      // epilogue writes feature rows directly and the down product reads an MN-major tile
-      const bool ht = (c->cfg.flags & MOESHARD_FLAG_H_TRANSPOSED) != 0;
-      const int np = static_cast<int>(c->L.npad);
       TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
-                  static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr,
-                  gather ? c->tb.perm_pad : nullptr, N, ht, np, gather_cp,
-                  static_cast<const __nv_bfloat16*>(x_all), c->gather_depth};
+                  static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
       TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
-                  static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route, nullptr, 0, ht, np};
+                  static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
       if (c->p2p) {   // Step 5 send: partial rows go straight to their owner's receive slot
         dn.p2p_n = ns;
         for (int g = 0; g < c->world; ++g)
@@ -728,13 +677,9 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
               c->pa.peers[g] + c->PL.off_recv +
               static_cast<size_t>(c->rank) * c->pa.n_max * h * 2);
       }
-      CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, gather && !gather_cp ? tm_xg : c->tm_xperm16,
-                                    lw.tm_out, ht ? c->tm_Ht : c->tm_H16, up, dn, c->tb.done,
-                                    copy_in_ffn ? x_all : nullptr, c->x_perm, h * c->elt / 16,
-                                    (c->cfg.flags & MOESHARD_FLAG_DYNAMIC_SCHED) != 0,
-                                    c->early_tables && !route_group && !gather &&
-                                        !(c->cfg.flags & MOESHARD_FLAG_FUSED_SCAN) && n > 0,
-                                    c->num_sms, s));
+      CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, c->tm_xperm16, lw.tm_out, c->tm_H16, up, dn,
+                                    c->tb.done, (c->cfg.flags & MOESHARD_FLAG_DYNAMIC_SCHED) != 0,
+                                    /*early_tables=*/n > 0, c->num_sms, s));
       c->mark(4, s);
       c->launches += 1;
       if (c->p2p) {

@@ -73,32 +73,26 @@ __global__ void __launch_bounds__(128) group_block_scan(const int32_t* __restric
   if (threadIdx.x == 0) tot[e] = total;
 }
 
-// One CTA per hist-block (HB <= 128 tokens; 1024 threads), the whole of
-// Step 2 in one launch:
+// One CTA group per hist-block (HB <= 128 tokens), the rest of Step 2:
 //  1. totals and earlier-block counts come from group_block_scan; offsets =
 //     exclusive scan of the totals; CTA 0 also publishes counts / offsets /
 //     tile tables / work counters;
 //  2. warps 0-3 give each token its stable rank inside the block
 //     (match_any) -> j = offsets[e] + earlier[e] + rank, perm[j] = t;
-//  3. all 32 warps copy the block's rows to X_perm[j] (16-B vectors, 4 rows
-//     per warp with every load in flight before the stores).
+//  3. the block's rows are copied to X_perm[j] (16-B vectors, 4 rows per warp
+//     with every load of the first VPL*32 vectors in flight before the stores;
+//     wider rows continue in column blocks of VPL*32 vectors).
 // kSplit CTAs share one hist-block: all compute its ranks, each copies
 // 128/kSplit of its rows (spreads the row traffic over more SMs).
-// kScan: the per-expert block scans run inside this launch (no group_block_scan):
-// the first E CTAs to start (atomic ticket, so they are resident) each scan one
-// expert's column of hist and publish base / tot; every CTA then acquires
-// "E scans done" before reading them. sync[0..2] = ticket, scans done, CTAs
-// past the wait (the last one resets all three for the next launch).
-template <int VPL, int kSplit, bool kScan = false>
+template <int VPL, int kSplit>
 __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     const int32_t* __restrict__ bbase, const int32_t* __restrict__ btot, int E, Tables tb,
     int n_mt_up_tc, int n_mt_down_tc, const RouteRec* __restrict__ route,
     const uint4* __restrict__ x_all, int n, int nbr, int HB, int32_t* __restrict__ perm,
-    int row_vecs, uint4* __restrict__ x_perm, const int32_t* __restrict__ hist, int NB,
-    int32_t* sync) {
-  // x_perm == nullptr: the consumer gathers rows itself (TMA gather4); only perm/tables
+    int row_vecs, uint4* __restrict__ x_perm, int NB) {
   constexpr int kThreads = 1024 / kSplit;
   constexpr int kRowsPerWarp = 4;                 // rows copied per warp
+  constexpr int kColBlock = VPL * 32;             // 16-B vectors per column block
   static_assert(kThreads >= 128, "ranks need 128 threads");
   __shared__ int32_t s_tot[kMaxExperts];
   __shared__ int32_t s_pre[kMaxExperts];
@@ -114,17 +108,14 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   const int t1 = min(t0 + HB, (r + 1) * n);
   const int row_base = part * (128 / kSplit);     // this CTA's rows of the block
   ptx::griddep_wait();            // the router's records and histograms
-  __shared__ int s_ticket;
-  if (kScan && threadIdx.x == 0) s_ticket = atomicAdd(sync, 1);
-  ptx::griddep_launch_dependents();   // the FFN's prologue (and L2 prefetch) may start now
+  ptx::griddep_launch_dependents();   // the FFN's prologue may start now
   const bool has_block = b < NB;
   // issue this CTA's row loads first: the sources are known, only the
   // destinations depend on the scan below
-  const bool copy_rows = x_perm != nullptr;
   uint4 v[kRowsPerWarp][VPL];
 #pragma unroll
   for (int u = 0; u < kRowsPerWarp; ++u) {
-    const int tt = copy_rows && has_block ? t0 + row_base + warp * kRowsPerWarp + u : t1;
+    const int tt = has_block ? t0 + row_base + warp * kRowsPerWarp + u : t1;
 #pragma unroll
     for (int c = 0; c < VPL; ++c) {
       const int col = lane + 32 * c;
@@ -136,43 +127,9 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     t = t0 + threadIdx.x;
     e = (t < t1) ? __ldg(&route[t].expert) : -1;
   }
-  if (kScan) {
-    __syncthreads();
-    const int ex = s_ticket;
-    if (ex < E) {   // exclusive scan of hist[.][ex] over the NB blocks
-      int32_t* base_w = const_cast<int32_t*>(bbase);
-      const int q = ceil_div(NB, kThreads);
-      const int b0 = threadIdx.x * q, b1 = min(NB, b0 + q);
-      int sum = 0;
-      for (int bb = b0; bb < b1; ++bb) sum += __ldg(hist + (size_t)bb * E + ex);
-      int total;
-      int run = block_excl_scan<kThreads>(sum, s_warp, total);
-      for (int bb = b0; bb < b1; ++bb) {
-        base_w[(size_t)bb * E + ex] = run;
-        run += __ldg(hist + (size_t)bb * E + ex);
-      }
-      if (threadIdx.x == 0) const_cast<int32_t*>(btot)[ex] = total;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(sync + 1, 1);
-      }
-    }
-    if (threadIdx.x == 0) {
-      while (ptx::ld_acquire_gpu(sync + 1) < E) __nanosleep(32);
-      if (atomicAdd(sync + 2, 1) == static_cast<int>(gridDim.x) - 1) {   // every CTA is past
-        sync[0] = 0;
-        sync[1] = 0;
-        sync[2] = 0;
-      }
-    }
-    __syncthreads();
-    if (!has_block) return;
-  }
   for (int k = threadIdx.x; k < E; k += kThreads) {
-    s_tot[k] = kScan ? __ldcg(btot + k) : __ldg(btot + k);         // tokens of expert k overall
-    s_pre[k] = kScan ? __ldcg(bbase + (size_t)b * E + k)           // ... in blocks before this one
-                     : __ldg(bbase + (size_t)b * E + k);
+    s_tot[k] = __ldg(btot + k);                        // tokens of expert k overall
+    s_pre[k] = __ldg(bbase + (size_t)b * E + k);       // ... in blocks before this one
   }
   for (int k = threadIdx.x; k < 4 * E; k += kThreads) whist[k / E][k % E] = 0;
   __syncthreads();
@@ -205,8 +162,8 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     }
   }
   __syncthreads();
-  // 3. row stores (rows loaded at the top)
-  if (!copy_rows) return;
+  // 3. row stores (first column block loaded at the top)
+  if (x_perm == nullptr || !has_block) return;
   int jj[kRowsPerWarp];
 #pragma unroll
   for (int u = 0; u < kRowsPerWarp; ++u) jj[u] = s_j[row_base + warp * kRowsPerWarp + u];
@@ -217,6 +174,24 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
       const int col = lane + 32 * c;
       if (jj[u] >= 0 && col < row_vecs) x_perm[(size_t)jj[u] * row_vecs + col] = v[u][c];
     }
+  for (int c0 = kColBlock; c0 < row_vecs; c0 += kColBlock) {   // rows wider than one block
+#pragma unroll
+    for (int u = 0; u < kRowsPerWarp; ++u) {
+      const int tt = t0 + row_base + warp * kRowsPerWarp + u;
+#pragma unroll
+      for (int c = 0; c < VPL; ++c) {
+        const int col = c0 + lane + 32 * c;
+        if (jj[u] >= 0 && col < row_vecs) v[u][c] = __ldg(x_all + (size_t)tt * row_vecs + col);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kRowsPerWarp; ++u)
+#pragma unroll
+      for (int c = 0; c < VPL; ++c) {
+        const int col = c0 + lane + 32 * c;
+        if (jj[u] >= 0 && col < row_vecs) x_perm[(size_t)jj[u] * row_vecs + col] = v[u][c];
+      }
+  }
 }
 
 }  // namespace
@@ -224,23 +199,18 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
 void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int32_t* tot,
                          Tables tb, int n_mt_up_tc, int n_mt_down_tc, const RouteRec* route,
                          const void* x_all, int n, int nbr, int HB, int row_bytes, int32_t* perm,
-                         void* x_perm, int32_t* sync, cudaStream_t s) {
+                         void* x_perm, cudaStream_t s) {
   if (NB <= 0) return;
-  // sync != nullptr: the block scans run inside the grouping launch (one launch for Step 2)
-  if (!sync) launch_pdl(group_block_scan, dim3(E), dim3(128), 0, s, hist, NB, E, base, tot);
+  launch_pdl(group_block_scan, dim3(E), dim3(128), 0, s, hist, NB, E, base, tot);
   const int row_vecs = row_bytes / 16;
   const int vpl = ceil_div(row_vecs, 32);
   auto* xs = static_cast<const uint4*>(x_all);
   auto* xd = static_cast<uint4*>(x_perm);
-  const int grid = sync ? std::max(NB * 4, E) : NB * 4;
-  // each hist-block's rows are copied by kSplit = 4 CTAs of 256 threads
-#define SG(V)                                                                                    \
-  (sync ? launch_pdl(group_scatter_gather<V, 4, true>, dim3(grid), dim3(256), 0, s, base, tot, E, \
-                     tb, n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm, row_vecs, xd,     \
-                     hist, NB, sync)                                                              \
-        : launch_pdl(group_scatter_gather<V, 4>, dim3(grid), dim3(256), 0, s, base, tot, E, tb,   \
-                     n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm, row_vecs, xd, hist,   \
-                     NB, sync))
+  // each hist-block's rows are copied by kSplit = 4 CTAs of 256 threads; rows wider
+  // than 8 * 32 vectors (4 KB) are copied in column blocks of 4 KB
+#define SG(V)                                                                                  \
+  launch_pdl(group_scatter_gather<V, 4>, dim3(NB * 4), dim3(256), 0, s, base, tot, E, tb,      \
+             n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm, row_vecs, xd, NB)
   switch (vpl) {
     case 1: SG(1); break;
     case 2: SG(2); break;

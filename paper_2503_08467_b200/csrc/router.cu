@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(256) router_kernel(const T* __restrict__ x, in
       r.gate = expf(lsel - best) / sum;
       out[t] = r;
       atomicAdd(&s_hist[sel], 1);
-      if (bad) atomicExch(err_flag, 1);
+      if (bad) atomicOr(err_flag, 1);
     }
   }
   __syncthreads();
@@ -200,13 +200,13 @@ void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int 
 #include <cstdlib>
 
 #include "gemm_tc.cuh"
-#include "group.cuh"
 #include "ptx.cuh"
 
 namespace moeshard {
 namespace {
 
-constexpr int RTC_MAX_STAGES = 16;   // 64-token CTAs: all 12 k-blocks of h = 768 in flight
+constexpr int RTC_TOK = 128;         // tokens per CTA = hist-block size (TMEM lanes)
+constexpr int RTC_MAX_STAGES = 16;
 
 // 2^x on the SFU (ex2.approx.ftz: ~2 ulp; exp2(-inf) = +0)
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -231,149 +231,26 @@ __global__ void router_transpose(const __nv_bfloat16* __restrict__ w_r, int h, i
   }
 }
 
-// Step 2 (groupPerExpert + the Sec. 3.3 per-expert concatenation,
-// PAPER.md:191-195, 339-341) inside the router launch, world = 1. CTA b owns
-// hist-block b = tokens [128 b, 128 b + 128). Three phases split by grid
-// barriers (all CTAs resident):
-//   1. (routing, above) hist[b][e] and each token's expert in s_tok_e;
-//   2. CTA c scans hist[.][e] over the blocks for experts e = c, c + NB, ... ->
-//      base[b][e] (tokens of e in earlier blocks) and tot[e];
-//   3. every CTA: segment offsets from tot (CTA 0 publishes the tables), the
-//      stable rank of each token inside its block (match_any), perm / perm_pad,
-//      and the copy of its 128 rows x[t] -> X_perm[j] (x is still in L2).
-__device__ __forceinline__ uint64_t gtimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-template <bool kT>
-__device__ __forceinline__ void route_group(const RouteGroupArgs& ga, const int32_t* hist,
-                                            const int32_t* s_tok_e, int n, int E, uint64_t t_entry,
-                                            uint64_t t_routed) {
-  uint64_t ts[6];
-  __shared__ int32_t s_tot[kMaxExperts], s_pre[kMaxExperts], s_base[kMaxExperts],
-      s_bpad[kMaxExperts];
-  __shared__ int32_t whist[4][kMaxExperts];
-  __shared__ int32_t s_j[128];
-  __shared__ int32_t s_warp[33];
-  const int NB = gridDim.x, b = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (kT) ts[0] = gtimer();
-  grid_barrier(ga.bar, NB);               // every block's histogram is in memory
-  ptx::griddep_launch_dependents();       // all CTAs of this grid are resident now
-  if (kT) ts[1] = gtimer();
-  for (int e = b; e < E; e += NB) {       // CTA-uniform loop
-    const int v = threadIdx.x < NB ? __ldcg(hist + static_cast<size_t>(threadIdx.x) * E + e) : 0;
-    int total;
-    const int ex = block_excl_scan<256>(v, s_warp, total);
-    if (threadIdx.x < NB) ga.base[static_cast<size_t>(threadIdx.x) * E + e] = ex;
-    if (threadIdx.x == 0) ga.tot[e] = total;
-  }
-  if (kT) ts[2] = gtimer();
-  grid_barrier(ga.bar, NB);               // base / tot complete
-  if (kT) ts[3] = gtimer();
-  for (int k = threadIdx.x; k < E; k += 256) {
-    s_tot[k] = __ldcg(ga.tot + k);
-    s_pre[k] = __ldcg(ga.base + static_cast<size_t>(b) * E + k);
-  }
-  for (int k = threadIdx.x; k < 4 * E; k += 256) whist[k / E][k % E] = 0;
-  __syncthreads();
-  segment_tables<256>(E, s_tot, s_pre, s_base, s_bpad, s_warp, b == 0, ga.tb, ga.n_mt_up,
-                      ga.n_mt_dn);
-  const int t = b * 128 + threadIdx.x;
-  int e = -1, rank_w = 0;
-  if (warp < 4) {
-    e = s_tok_e[threadIdx.x];
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    rank_w = __popc(peers & lanemask_lt());
-    if (e >= 0 && rank_w == 0) whist[warp][e] = __popc(peers);
-  }
-  __syncthreads();
-  if (warp < 4) {
-    int jp = -1;
-    if (e >= 0) {
-      int before = 0;
-      for (int w = 0; w < warp; ++w) before += whist[w][e];
-      ga.perm[s_base[e] + before + rank_w] = t;            // public, compact
-      jp = s_bpad[e] + before + rank_w;                    // internal, padded segments
-      ga.tb.perm_pad[jp] = t;
-    }
-    s_j[threadIdx.x] = jp;
-  }
-  __syncthreads();
-  if (kT) ts[4] = gtimer();
-  if (ga.x_perm == nullptr) return;
-  // rows: 8 warps x 16 rows, 4 rows in flight per warp (row_vecs <= 128)
-  const int rv = ga.row_vecs;
-  for (int r0 = warp * 16; r0 < warp * 16 + 16; r0 += 4) {
-    uint4 v[4][4];
-    int jj[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      jj[u] = s_j[r0 + u];
-      const uint4* src = ga.x + static_cast<size_t>(b * 128 + r0 + u) * rv;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (jj[u] >= 0 && lane + 32 * c < rv) v[u][c] = __ldcg(src + lane + 32 * c);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      uint4* dst = ga.x_perm + static_cast<size_t>(jj[u]) * rv;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (jj[u] >= 0 && lane + 32 * c < rv) dst[lane + 32 * c] = v[u][c];
-    }
-  }
-  if (kT) {
-    __syncthreads();
-    ts[5] = gtimer();
-    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
-      printf("[route_group cta %d] ns from entry: routed %llu arrive1 %llu pass1 %llu scanned %llu "
-             "pass2 %llu ranked %llu copied %llu\n", blockIdx.x,
-             (unsigned long long)(t_routed - t_entry), (unsigned long long)(ts[0] - t_entry),
-             (unsigned long long)(ts[1] - t_entry), (unsigned long long)(ts[2] - t_entry),
-             (unsigned long long)(ts[3] - t_entry), (unsigned long long)(ts[4] - t_entry),
-             (unsigned long long)(ts[5] - t_entry));
-  }
-}
-
 // kMN: B = router_w [h][E] read directly (MN-major, 64-expert x 64-k TMA boxes);
 // otherwise B = the transposed copy [EP][h] (K-major).
-// kGroup (world = 1 only, grid <= SMs so every CTA is resident): after routing,
-// the same launch runs the whole of Step 2 (see route_group below) - the block
-// histograms never leave the kernel boundary and the row copy re-reads x from L2.
-template <bool kMN, bool kT = false, bool kGroup = false>
-__global__ void __launch_bounds__(256, 1)
+// One CTA = 128 tokens (one hist-block); 6 warps: 0-3 epilogue (thread = token =
+// TMEM lane), 4 TMA producer, 5 MMA issuer.
+template <bool kMN>
+__global__ void __launch_bounds__(192, 1)
     router_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      int n, int h, int E, int EP, const int32_t* __restrict__ forced,
                      RouteRec* __restrict__ out, int32_t* __restrict__ hist_out,
-                     int32_t* __restrict__ err_flag, const uint8_t* __restrict__ pf,
-                     long long pf_bytes, RouteGroupArgs ga, int tok) {
-  // tok = tokens per CTA (hist-block): 128, or 64 - then only rows 0-63 of the
-  // M=128 A tile are loaded and TMEM lanes 64-127 (stale rows) are never read
-  // CTAs beyond the token tiles run on otherwise idle SMs and pull the first
-  // weight tiles the FFN kernel will stream into L2 while routing and grouping
-  // are latency-bound (the weights do not depend on the routing result).
-  const int n_tiles = (n + tok - 1) / tok;
-  if (static_cast<int>(blockIdx.x) >= n_tiles) {
-    const int n_pf = gridDim.x - n_tiles, q = blockIdx.x - n_tiles;
-    const long long per = ((pf_bytes / n_pf) + 16383) & ~16383LL;
-    const long long beg = q * per, end = min(pf_bytes, beg + per);
-    for (long long o = beg + threadIdx.x * 16384LL; o < end; o += blockDim.x * 16384LL)
-      ptx::prefetch_l2_bulk(pf + o, static_cast<uint32_t>(min(16384LL, end - o)));
-    return;
-  }
+                     int32_t* __restrict__ err_flag) {
   using namespace ptx;
+  constexpr int kTok = RTC_TOK;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int n_atoms = (EP + 63) / 64;
   const int b_bytes = kMN ? n_atoms * 8192 : EP * 128;
   __shared__ int32_t s_hist[kMaxExperts];
-  __shared__ int32_t s_tok_e[128];   // kGroup: expert of each of the CTA's tokens (-1: none)
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
-  const int a_stage = tok * 128;   // tok rows x 64 k x 2 B
+  constexpr int a_stage = kTok * 128;   // kTok rows x 64 k x 2 B
   const int RTC_STAGES = min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (a_stage + b_bytes));
   uint8_t* sA = smem;
   uint8_t* sB = smem + RTC_STAGES * a_stage;
@@ -394,8 +271,6 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(done, 1);
     fence_mbar_init();
   }
-  const long long t_start = clock64();
-  const uint64_t g_entry = kT ? gtimer() : 0;
   if (warp == 0) tmem_alloc(tmem_slot, ncols);
   tc_fence_before();
   __syncthreads();
@@ -407,63 +282,56 @@ __global__ void __launch_bounds__(256, 1)
   // the previous forward's FFN is done with the "tables published" flag (tb.stats[6],
   // = err_flag + 3): clear it for this forward's grouping launch to set
   if (blockIdx.x == 0 && threadIdx.x == 0) err_flag[3] = 0;
-  // kGroup: only after the first grid barrier (every CTA of this grid resident),
-  // else the dependent FFN's CTAs could take the SMs a not-yet-running CTA needs
-  if (!kGroup) griddep_launch_dependents();
-  const long long t_setup = clock64();
-  const int tok0 = blockIdx.x * tok;
+  griddep_launch_dependents();
+  const int tok0 = blockIdx.x * kTok;
   const int nkb = h / 64;
-  const uint32_t a_bytes = static_cast<uint32_t>(tok) * 128;
 
   if (warp == 4) {
-    {  // TMA producer (warp-uniform loop, one elected lane issues)
-      const uint64_t pol_x = kGroup ? policy_evict_last() : policy_evict_first();  // kGroup re-reads x
-      const uint64_t pol_w = policy_evict_last();
-      int s = 0;
-      uint32_t ph = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&empty[s], ph ^ 1);
-        const int kk = kb;
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
-          tma_load_2d(&tmX, &full[s], sA + s * a_stage, kk * 64, tok0, pol_x);
-          if (kMN) {
-            for (int a = 0; a < n_atoms; ++a)
-              tma_load_2d(&tmW, &full[s], sB + s * b_bytes + a * 8192, a * 64, kk * 64, pol_w);
-          } else {
-            tma_load_2d(&tmW, &full[s], sB + s * b_bytes, kk * 64, 0, pol_w);  // box = EP rows
-          }
+    // TMA producer (warp-uniform loop, one elected lane issues)
+    const uint64_t pol_x = policy_evict_first();
+    const uint64_t pol_w = policy_evict_last();
+    int s = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      mbar_wait(&empty[s], ph ^ 1);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&full[s], a_stage + b_bytes);
+        tma_load_2d(&tmX, &full[s], sA + s * a_stage, kb * 64, tok0, pol_x);
+        if (kMN) {
+          for (int a = 0; a < n_atoms; ++a)
+            tma_load_2d(&tmW, &full[s], sB + s * b_bytes + a * 8192, a * 64, kb * 64, pol_w);
+        } else {
+          tma_load_2d(&tmW, &full[s], sB + s * b_bytes, kb * 64, 0, pol_w);  // box = EP rows
         }
-        __syncwarp();
-        if (++s == RTC_STAGES) { s = 0; ph ^= 1; }
       }
+      __syncwarp();
+      if (++s == RTC_STAGES) { s = 0; ph ^= 1; }
     }
   } else if (warp == 5) {
-    {  // MMA issuer (warp-uniform loop, one elected lane issues)
-      const uint32_t idesc = idesc_bf16_f32(128, EP, kMN);
-      int s = 0;
-      uint32_t ph = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&full[s], ph);
-        tc_fence_after();
-        const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + s * a_stage));
-        const uint64_t bd = kMN ? smem_desc_mn_sw128(smem_u32(sB + s * b_bytes), 8192)
-                                : smem_desc_k_sw128(smem_u32(sB + s * b_bytes));
-        const uint32_t bstep = kMN ? 128 : 2;   // K=16 step: 16 rows x 128 B (MN) or 32 B (K)
-        if (elect_one()) {
+    // MMA issuer (warp-uniform loop, one elected lane issues)
+    const uint32_t idesc = idesc_bf16_f32(128, EP, kMN);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + s * a_stage));
+      const uint64_t bd = kMN ? smem_desc_mn_sw128(smem_u32(sB + s * b_bytes), 8192)
+                              : smem_desc_k_sw128(smem_u32(sB + s * b_bytes));
+      const uint32_t bstep = kMN ? 128 : 2;   // K=16 step: 16 rows x 128 B (MN) or 32 B (K)
+      if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma_bf16_ss(tmem, ad + 2 * k, bd + bstep * k, idesc, (kb | k) != 0);
-          mma_commit(&empty[s]);
-        }
-        __syncwarp();
-        if (++s == RTC_STAGES) { s = 0; ph ^= 1; }
+        for (int k = 0; k < 4; ++k)
+          mma_bf16_ss(tmem, ad + 2 * k, bd + bstep * k, idesc, (kb | k) != 0);
+        mma_commit(&empty[s]);
       }
-      if (elect_one()) mma_commit(done);
       __syncwarp();
+      if (++s == RTC_STAGES) { s = 0; ph ^= 1; }
     }
-  } else if (warp < tok / 32) {
-    // epilogue: warps 0-3 (0-1 for 64-token CTAs), thread = token (TMEM lane 32*warp + lane)
+    if (elect_one()) mma_commit(done);
+    __syncwarp();
+  } else {
+    // epilogue: warps 0-3, thread = token (TMEM lane 32*warp + lane)
     const int t = tok0 + warp * 32 + lane;
     int sel = -1;
     bool bad = false;
@@ -476,12 +344,13 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_wait(done, 0);
     tc_fence_after();
-    const long long t_done = clock64();
     const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     // one pass over the logit row, 32 columns per TMEM load: columns >= E are
     // masked to -inf; chunk max by a tree, argmax = the smallest column attaining
     // it (lowest index on ties, R4) by a tree of index minima, then a running
-    // (max, sum exp(l - max)) pair rescaled when the max moves.
+    // (max, sum exp(l - max)) pair rescaled when the max moves. A later chunk
+    // replaces the running argmax only with a strictly larger max, so ties across
+    // chunks also resolve to the lowest index.
     constexpr float kLog2e = 1.4426950408889634f;
     float best = -INFINITY, lsel = 0.f, sum = 0.f;
     int best_e = 0;
@@ -536,37 +405,28 @@ __global__ void __launch_bounds__(256, 1)
       }
       sum += (p0 + p1) + (p2 + p3);
     }
-    const long long t_loop = clock64();
     if (t < n) {
       RouteRec rec;
       rec.expert = sel >= 0 ? sel : best_e;
       rec.gate = (sel >= 0 ? fast_exp2((lsel - best) * kLog2e) : 1.f) / sum;
       out[t] = rec;
       atomicAdd(&s_hist[rec.expert], 1);
-      if (bad) atomicExch(err_flag, 1);
+      if (bad) atomicOr(err_flag, 1);
     }
-    if (kGroup) s_tok_e[threadIdx.x] = t < n ? (sel >= 0 ? sel : best_e) : -1;
-    const long long t_store = clock64();
-    asm volatile("bar.sync 1, %0;" ::"r"(tok) : "memory");  // the epilogue warps
-    const long long t_bar = clock64();
-    for (int e = threadIdx.x; e < E; e += tok) hist_out[(size_t)blockIdx.x * E + e] = s_hist[e];
-    if (kT && !kGroup && (threadIdx.x == 0 || threadIdx.x == 127) && (blockIdx.x == 0 || blockIdx.x == 40))
-      printf("[router cta %d t%d] setup %lld mainloop %lld softmax %lld store %lld bar %lld hist %lld\n",
-             blockIdx.x, threadIdx.x, t_setup - t_start, t_done - t_setup, t_loop - t_done,
-             t_store - t_loop, t_bar - t_store, clock64() - t_bar);
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // the epilogue warps
+    for (int e = threadIdx.x; e < E; e += kTok) hist_out[(size_t)blockIdx.x * E + e] = s_hist[e];
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 0) tmem_dealloc(tmem, ncols);
-  if constexpr (kGroup) route_group<kT>(ga, hist_out, s_tok_e, n, E, g_entry, kT ? gtimer() : 0);
 }
 
 }  // namespace
 
-size_t router_tc_smem_bytes(int EP, bool mn, int tok) {
+size_t router_tc_smem_bytes(int EP, bool mn) {
   const int b = mn ? ((EP + 63) / 64) * 8192 : EP * 128;
-  const int a = tok * 128;
+  const int a = RTC_TOK * 128;
   const int st = std::min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (a + b));
   return 1024 + st * (a + b) + (2 * st + 1) * 8 + 16;
 }
@@ -574,10 +434,7 @@ size_t router_tc_smem_bytes(int EP, bool mn, int tok) {
 cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
                              const void* w_r, void* wt_r, int n, int h, int E, int EP,
                              const int32_t* forced, RouteRec* out, int32_t* hist_out,
-                             int32_t* err_flag, const void* pf, long long pf_bytes, int pf_ctas,
-                             int tok, cudaStream_t s) {
-  const auto* pfb = static_cast<const uint8_t*>(pf);
-  if (pf == nullptr || pf_bytes < 16384) pf_ctas = 0;
+                             int32_t* err_flag, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   static PerDeviceOnce attr;
   if (attr.need()) {
@@ -586,56 +443,20 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
                                          RTC_SMEM_BUDGET + 2048);  // >= router_tc_smem_bytes(any EP)
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(router_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               RTC_SMEM_BUDGET + 2048);  // >= router_tc_smem_bytes(any EP)
+                               RTC_SMEM_BUDGET + 2048);
     if (e != cudaSuccess) return e;
     attr.done();
   }
-  const RouteGroupArgs none{};
-  static const bool timing = getenv("MOESHARD_ROUTER_TIMING") != nullptr;
-  if (mn_major && timing) {
-    cudaFuncSetAttribute(router_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         RTC_SMEM_BUDGET + 2048);
-    router_tc_kernel<true, true><<<ceil_div(n, tok), 192, router_tc_smem_bytes(EP, true, tok), s>>>(
-        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, 0LL, none, tok);
-  } else if (mn_major) {
-    return launch_pdl(router_tc_kernel<true>, dim3(ceil_div(n, tok) + pf_ctas), dim3(192),
-                      router_tc_smem_bytes(EP, true, tok), s, tmX, tmW, n, h, E, EP, forced, out,
-                      hist_out, err_flag, pfb, pf_bytes, none, tok);
-  } else {
-    dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
-    router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,
-                                       static_cast<__nv_bfloat16*>(wt_r));
-    router_tc_kernel<false><<<ceil_div(n, tok) + pf_ctas, 192, router_tc_smem_bytes(EP, false, tok), s>>>(
-        tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, pfb, pf_bytes, none, tok);
-  }
+  const dim3 grid(ceil_div(n, RTC_TOK));
+  if (mn_major)
+    return launch_pdl(router_tc_kernel<true>, grid, dim3(192), router_tc_smem_bytes(EP, true), s,
+                      tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
+  dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
+  router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,
+                                     static_cast<__nv_bfloat16*>(wt_r));
+  router_tc_kernel<false><<<grid, 192, router_tc_smem_bytes(EP, false), s>>>(
+      tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
   return cudaGetLastError();
-}
-
-cudaError_t launch_route_group_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, int n, int h,
-                                  int E, int EP, const int32_t* forced, RouteRec* out,
-                                  int32_t* hist_out, int32_t* err_flag, const RouteGroupArgs& ga,
-                                  cudaStream_t s) {
-  const int tok = 128;
-  if (n <= 0) return cudaSuccess;
-  static PerDeviceOnce attr;
-  if (attr.need()) {
-    cudaError_t e = cudaFuncSetAttribute(router_tc_kernel<true, false, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         RTC_SMEM_BUDGET + 2048);
-    if (e != cudaSuccess) return e;
-    attr.done();
-  }
-  static const bool timing = getenv("MOESHARD_ROUTER_TIMING") != nullptr;
-  if (timing) {
-    cudaFuncSetAttribute(router_tc_kernel<true, true, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, RTC_SMEM_BUDGET + 2048);
-    return launch_pdl(router_tc_kernel<true, true, true>, dim3(ceil_div(n, 128)), dim3(256),
-                      router_tc_smem_bytes(EP, true, tok), s, tmX, tmW, n, h, E, EP, forced, out,
-                      hist_out, err_flag, static_cast<const uint8_t*>(nullptr), 0LL, ga, 128);
-  }
-  return launch_pdl(router_tc_kernel<true, false, true>, dim3(ceil_div(n, 128)), dim3(256),
-                    router_tc_smem_bytes(EP, true, tok), s, tmX, tmW, n, h, E, EP, forced, out,
-                    hist_out, err_flag, static_cast<const uint8_t*>(nullptr), 0LL, ga, 128);
 }
 
 }  // namespace moeshard

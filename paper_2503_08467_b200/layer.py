@@ -80,9 +80,9 @@ class MoEShardLayer:
         elif p2p:
             self.p2p_connect([self.p2p_region()])
 
-    @staticmethod
-    def _stream() -> int:
-        return torch.cuda.current_stream().cuda_stream
+    def _stream(self) -> int:
+        """The current stream of this layer's device (not of the current device)."""
+        return torch.cuda.current_stream(self.device).cuda_stream
 
     def load_expert_shards(self, layer: int, w_in_shard: torch.Tensor, w_out_shard: torch.Tensor):
         """w_in_shard [E, h, d_ff/world], w_out_shard [E, d_ff/world, h] (this rank's slices)."""
@@ -96,7 +96,7 @@ class MoEShardLayer:
         C.moeshard_load_expert_shards(self.ctx, layer, w_in_shard.data_ptr(),
                                       w_out_shard.data_ptr(), st.data_ptr(), self._wbytes,
                                       self._stream())
-        torch.cuda.current_stream().synchronize()  # inputs may be freed by the caller afterwards
+        torch.cuda.current_stream(self.device).synchronize()  # inputs may be freed afterwards
         self._storage[layer] = st
 
     # ---------------------------------------------------------- peer-memory exchange
@@ -130,6 +130,8 @@ class MoEShardLayer:
                 forced_expert: Optional[torch.Tensor] = None,
                 out: Optional[torch.Tensor] = None, stages: int = C.MOESHARD_STAGE_ALL) -> torch.Tensor:
         n = hidden.shape[0]
+        if hidden.device != torch.device("cuda", self.device):
+            raise C.MoEShardError(-1, f"hidden is on {hidden.device}, the layer on cuda:{self.device}")
         if hidden.dtype != self.dtype or router_w.dtype != self.dtype:
             raise C.MoEShardError(-1, f"hidden/router_w must be {self.dtype}")
         if hidden.dim() != 2 or hidden.shape[1] != self.h or tuple(router_w.shape) != (self.h, self.E):
@@ -226,12 +228,17 @@ class HostStreamer:
     buffers per direction suffice: a buffer is rewritten two steps after it was
     filled, one join after its reader ran.
 
-    host_out of batch k is complete after step(k+2) or join(); host_in, router_w
-    and forced_expert of batch k must stay unchanged until step(k+1) returns.
+    Host-buffer contract (the copies are asynchronous DMAs; nothing here blocks the
+    host): step() returns the batch index k. host_in of batch k may be refilled only
+    after input_done(k) (its H2D has completed; a CUDA event, wait with
+    .synchronize()). host_out of batch k holds the result only after output_done(k)
+    has completed; that event exists once the D2H was issued, by step(k+2) or join().
+    router_w and forced_expert of batch k must stay unchanged until output_done(k).
     join() drains the pipeline (issues the last forward and copies) and makes the
     caller's stream wait for them. Marshalling only: the forward is the library's."""
 
     NBUF = 2
+    KEEP = 8   # events kept per direction (batches older than k - KEEP are long complete)
 
     def __init__(self, layer: MoEShardLayer, n_local: int):
         self.layer = layer
@@ -242,37 +249,65 @@ class HostStreamer:
         self.din = [torch.empty(n_local, layer.h, dtype=layer.dtype, device=dev) for _ in range(nb)]
         self.dout = [torch.empty_like(self.din[0]) for _ in range(nb)]
         self.k = 0
-        self.to_forward = None   # (buffer, layer_idx, router_w, forced, host_out) of batch k-1
-        self.to_copy = None      # (buffer, host_out) of batch k-2
+        self.to_forward = None   # (buffer, batch, layer_idx, router_w, forced) of batch k-1
+        self.to_copy = None      # (buffer, batch) of batch k-2
+        self.host_out = {}       # batch -> pinned host output tensor
+        self.in_ev = {}          # batch -> event after its H2D
+        self.out_ev = {}         # batch -> event after its D2H
+
+    def _prune(self):
+        for d in (self.in_ev, self.out_ev, self.host_out):
+            for b in [b for b in d if b < self.k - self.KEEP]:
+                if d is not self.host_out or b in self.out_ev:
+                    del d[b]
 
     def _advance(self, new_in) -> None:
-        comp = torch.cuda.current_stream()
+        comp = torch.cuda.current_stream(self.layer.device)
         self.h2d.wait_stream(comp)
         self.d2h.wait_stream(comp)
         if new_in is not None:
-            b, host_in = new_in
+            b, batch, host_in = new_in
             with torch.cuda.stream(self.h2d):
                 self.din[b].copy_(host_in, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.h2d)
+                self.in_ev[batch] = ev
         if self.to_copy is not None:
-            b, host_out = self.to_copy
+            b, batch = self.to_copy
             with torch.cuda.stream(self.d2h):
-                host_out.copy_(self.dout[b], non_blocking=True)
+                self.host_out[batch].copy_(self.dout[b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.d2h)
+                self.out_ev[batch] = ev
         self.to_copy = None
         if self.to_forward is not None:
-            b, layer_idx, router_w, forced, host_out = self.to_forward
+            b, batch, layer_idx, router_w, forced = self.to_forward
             self.layer.forward(layer_idx, self.din[b], router_w, forced_expert=forced,
                                out=self.dout[b])
-            self.to_copy = (b, host_out)
+            self.to_copy = (b, batch)
         comp.wait_stream(self.h2d)
         comp.wait_stream(self.d2h)
 
     def step(self, layer_idx: int, host_in: torch.Tensor, router_w: torch.Tensor,
-             host_out: torch.Tensor, forced_expert: Optional[torch.Tensor] = None) -> torch.Tensor:
-        b = self.k % self.NBUF
-        self._advance((b, host_in))
-        self.to_forward = (b, layer_idx, router_w, forced_expert, host_out)
+             host_out: torch.Tensor, forced_expert: Optional[torch.Tensor] = None) -> int:
+        k = self.k
+        b = k % self.NBUF
+        self.host_out[k] = host_out
+        self._advance((b, k, host_in))
+        self.to_forward = (b, k, layer_idx, router_w, forced_expert)
         self.k += 1
-        return host_out
+        self._prune()
+        return k
+
+    def input_done(self, k: int) -> torch.cuda.Event:
+        """Event after the H2D copy of batch k (host_in of k may be refilled once it completes)."""
+        return self.in_ev[k]
+
+    def output_done(self, k: int) -> torch.cuda.Event:
+        """Event after the D2H copy of batch k (issued by step(k+2) or join())."""
+        if k not in self.out_ev:
+            raise RuntimeError(f"batch {k}: D2H not issued yet (call step() twice more or join())")
+        return self.out_ev[k]
 
     def join(self):
         while self.to_forward is not None or self.to_copy is not None:

@@ -13,9 +13,7 @@ import os
 from typing import Optional
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-# MOESHARD_LIB_PATH: another in-tree build of the same library (A/B experiments,
-# scripts/ab_lib.sh); the default is the package's own libmoeshard.so
-LIB_PATH = os.environ.get("MOESHARD_LIB_PATH") or os.path.join(PKG, "libmoeshard.so")
+LIB_PATH = os.path.join(PKG, "libmoeshard.so")
 
 MOESHARD_OK = 0
 MOESHARD_BF16 = 0
@@ -23,17 +21,11 @@ MOESHARD_FP32 = 1
 MOESHARD_FLAG_FORCE_COLLECTIVES = 0x1
 MOESHARD_FLAG_SIMT_GEMM = 0x2
 MOESHARD_FLAG_UNFUSED_GEMM = 0x4
-MOESHARD_FLAG_TMA_GATHER = 0x8
-MOESHARD_FLAG_H_TRANSPOSED = 0x10
-MOESHARD_FLAG_FUSED_ROUTE_GROUP = 0x20
-MOESHARD_FLAG_CPASYNC_GATHER = 0x40
 MOESHARD_FLAG_NO_L2_PERSIST = 0x80
-MOESHARD_FLAG_ROW_COPY_IN_FFN = 0x100
 MOESHARD_FLAG_P2P = 0x200
-MOESHARD_FLAG_FUSED_SCAN = 0x400
-MOESHARD_FLAG_ROUTER_TOK64 = 0x800
 MOESHARD_FLAG_DYNAMIC_SCHED = 0x1000
 MOESHARD_FLAG_UNEVEN_TOKENS = 0x2000
+MOESHARD_FLAG_SERIAL_AG = 0x4000
 MOESHARD_STAGE_ROUTE = 0x1
 MOESHARD_STAGE_COMPUTE = 0x2
 MOESHARD_STAGE_REDUCE = 0x4

@@ -25,7 +25,7 @@ x = W.make_tokens(seed, N, h, device="cuda")
 w_r = W.make_router_weight(seed, h, E, device="cuda")
 out = torch.empty_like(x)
 res = {"E": E, "h": h, "d_ff": d_ff, "N": N, "G": G, "F": F, "weight_sets": NW,
-       "flags": os.environ.get("MOESHARD_FLAGS", "0")}
+       }
 for routing in ("uniform", "zipf"):
     f = W.draw_experts(seed, N, E, routing, device="cuda")
     fwd = lambda k: L.forward(k % NW, x, w_r, forced_expert=f, out=out)

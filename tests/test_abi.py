@@ -63,6 +63,10 @@ def test_config_validation_errors():
     assert ei.value.code == -1
     with pytest.raises(C.MoEShardError):
         C.moeshard_workspace_size(_cfg(), 0)
+    for removed in (0x8, 0x10, 0x20, 0x40, 0x100, 0x400, 0x800, 1 << 20):   # unknown flag bits
+        with pytest.raises(C.MoEShardError) as ei:
+            C.moeshard_workspace_size(_cfg(flags=removed), 1)
+        assert ei.value.code == -1 and "unknown" in str(ei.value)
 
 
 def test_sizes():

@@ -159,24 +159,6 @@ def test_fused_and_unfused_gemm_agree_bitwise(N, h, d_ff, E):
     assert torch.equal(ys[0], ys[1])
 
 
-def test_tma_gather4_token_path_matches_oracle():
-    # experimental: the FFN gathers token rows by perm (TMA gather4) instead of X_perm
-    from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_TMA_GATHER
-    inp = W.make_layer_inputs(20, 1500, 256, 512, 16, dtype=torch.bfloat16, routing="zipf")
-    L, y, r = _run(inp, dtype=torch.bfloat16, flags=MOESHARD_FLAG_TMA_GATHER,
-                   forced=inp.forced.cuda().contiguous())
-    _check_layer(inp, y, r, tol=BF16_TOL)
-
-
-def test_transposed_h_path_matches_oracle():
-    # experimental: H kept as H^T, the down product reads an MN-major token tile
-    from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_H_TRANSPOSED
-    inp = W.make_layer_inputs(22, 1700, 256, 512, 16, dtype=torch.bfloat16, routing="zipf")
-    L, y, r = _run(inp, dtype=torch.bfloat16, flags=MOESHARD_FLAG_H_TRANSPOSED,
-                   forced=inp.forced.cuda().contiguous())
-    _check_layer(inp, y, r, tol=BF16_TOL)
-
-
 def test_forced_collectives_path_world1():
     # exercises AllGather / partial buffer / ReduceScatter through NCCL with one rank
     from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_FORCE_COLLECTIVES
@@ -281,136 +263,183 @@ def test_virtual_shards_sum_to_unsharded(G):
 
 
 # --------------------------------------------------------------------- full size, every config
-def _full_size_sampled(N, h, d_ff, E, seed, routing, **kw):
-    """A whole layer at BASELINE size through the C ABI; routing tables exact on
-    every token, outputs vs the oracle on a seeded sample covering every active
-    expert (first/last 2 tokens of each segment + 256 random tokens)."""
+def per_row_rel(y, y_ref) -> float:
+    """Row-local companion of R12: max over tokens t of max_j |y-y_ref|[t] / max_j |y_ref[t]|,
+    so an error confined to a few rows cannot hide under the global normalisation."""
+    y, y_ref = O._f64(y), O._f64(y_ref)
+    den = np.abs(y_ref).max(axis=1)
+    num = np.abs(y - y_ref).max(axis=1)
+    ok = den > 0
+    assert (num[~ok] == 0).all(), "rows with an all-zero reference must be exactly zero"
+    return float((num[ok] / den[ok]).max()) if ok.any() else 0.0
+
+
+def _full_size_all_tokens(N, h, d_ff, E, seed, routing, **kw):
+    """A whole layer at BASELINE size through the C ABI, checked against the oracle on
+    EVERY token: routing tables exact (forced ids; natural routing: R13 ambiguity rule),
+    gates, outputs by the global max-abs-rel (R12) and by the per-row bar. The oracle
+    materialises one expert's weights at a time (moe_layer_tokens)."""
     from paper_2503_08467_b200 import MoEShardLayer
     dev = "cuda"
     x = W.make_tokens(seed, N, h, device=dev)
     w_r = W.make_router_weight(seed, h, E, device=dev)
     w_i, w_o = W.make_expert_weights(seed, E, h, d_ff, device=dev)
-    forced = W.draw_experts(seed, N, E, routing, device=dev, **kw)
+    forced = None if routing == "natural" else W.draw_experts(seed, N, E, routing, device=dev, **kw)
     L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16)
     L.load_expert_shards(0, w_i, w_o)
     y = L.forward(0, x, w_r, forced_expert=forced)
     r = {k: v.cpu().numpy() for k, v in L.routing(N).items()}
     L.check()
-    fc = forced.cpu().numpy().astype(np.int64)
-    np.testing.assert_array_equal(r["expert"], fc)
-    counts, offsets, perm = O.group_per_expert(fc, E)
+    xc, wrc = x.cpu(), w_r.cpu()
+    experts = _check_routing(r, xc, wrc, forced)
+    counts, offsets, perm = O.group_per_expert(experts, E)
     np.testing.assert_array_equal(r["counts"], counts)
     np.testing.assert_array_equal(r["offsets"], offsets)
     np.testing.assert_array_equal(r["perm"], perm)
-    rng = np.random.default_rng(seed)
-    sample = set(rng.choice(N, 256, replace=False).tolist())
-    for e in range(E):
-        seg = perm[offsets[e]:offsets[e + 1]]
-        sample.update(seg[:2].tolist() + seg[-2:].tolist())
-    sample = np.array(sorted(sample))
-    y_s, rt = O.moe_layer_tokens(x[sample].cpu(), w_r.cpu(),
-                                 lambda e: (w_i[e].cpu(), w_o[e].cpu()), forced_rows=fc[sample])
-    np.testing.assert_allclose(r["gate"][sample], rt.gate, rtol=1e-5, atol=1e-6)
-    err = O.max_abs_rel(y[sample].float().cpu().numpy(), y_s)
-    assert err <= BF16_TOL, err
-    assert torch.isfinite(y).all() and (y.float().abs().sum(1) > 0).all()
+    wi_c, wo_c = w_i.cpu(), w_o.cpu()
+    del w_i, w_o
+    y_ref, rt = O.moe_layer_tokens(xc, wrc, lambda e: (wi_c[e], wo_c[e]), forced_rows=experts)
+    np.testing.assert_allclose(r["gate"], rt.gate, rtol=1e-5, atol=1e-6)
+    yc = y.float().cpu().numpy()
+    err = O.max_abs_rel(yc, y_ref)
+    row = per_row_rel(yc, y_ref)
     L.close()
-    return err
+    assert err <= BF16_TOL, f"max-abs-rel {err:.3e}"
+    assert row <= BF16_TOL, f"per-row max-abs-rel {row:.3e}"
+    return err, row
+
+
+@pytest.mark.parametrize("routing,kw", [("uniform", {}), ("zipf", {"s": 1.2})])
+def test_c2_full_size_all_tokens(routing, kw):
+    """BASELINE.json configs[1] at G=1 in bench.py's launch configuration (E=64, N=8192,
+    h=768, d_ff=3072, bf16): every one of the 8192 output rows vs the fp64 oracle."""
+    err, row = _full_size_all_tokens(8192, 768, 3072, 64, 2, routing, **kw)
+    print(f"C2 {routing}: max-abs-rel {err:.2e}, per-row {row:.2e}")
+
+
+@pytest.mark.parametrize("E", [64, 128, 256])
+def test_bf16_natural_routing_full_size(E):
+    """The bench / encoder router path: bf16 tcgen05 logits with the natural router at
+    E = 64 (C2), 128 (C3/C5) and 256 (C4) over 8192 tokens of h = 768 - several 32-column
+    TMEM chunks per token, so the cross-chunk max / argmax / rescale is exercised. Routing
+    exact wherever the fp64 top-2 gap exceeds the fp32 bound (R13), all outputs checked."""
+    err, row = _full_size_all_tokens(8192, 768, 3072, E, 100 + E, "natural")
+    print(f"natural E={E}: max-abs-rel {err:.2e}, per-row {row:.2e}")
+
+
+def test_router_cross_chunk_argmax_and_ties():
+    """Planted logits: the winning expert sits in the last 32-column chunk, in the first,
+    and in a middle one, and exact ties across chunks resolve to the lowest index (R4).
+    x = one-hot rows times a scale, W_r rows chosen so logits are exact in bf16/fp32."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    E, h, d_ff = 256, 128, 128
+    N = 6
+    w_r = torch.zeros(h, E, dtype=torch.float32)
+    x = torch.zeros(N, h, dtype=torch.float32)
+    # token t uses input feature t; logits of token t = w_r[t, :]
+    want = [255, 0, 77, 40, 200, 31]
+    w_r[0, 255] = 4.0; w_r[0, 254] = 3.0                     # winner in the last chunk
+    w_r[1, 0] = 2.0; w_r[1, 200] = 1.0                       # winner in the first chunk
+    w_r[2, 77] = 1.5; w_r[2, 3] = 1.25; w_r[2, 250] = 1.0    # middle chunk
+    w_r[3, 40] = 2.0; w_r[3, 140] = 2.0; w_r[3, 240] = 2.0   # tie across chunks -> 40
+    w_r[4, 200] = 1.0; w_r[4, 201] = 1.0                     # tie inside a chunk -> 200
+    w_r[5, 31] = 0.5; w_r[5, 32] = 0.5                       # tie across the chunk boundary -> 31
+    for t in range(N):
+        x[t, t] = 1.0
+    inp = W.LayerInputs(x.bfloat16(), w_r.bfloat16(),
+                        *W.make_expert_weights(7, E, h, d_ff), None)
+    L, y, r = _run(inp, dtype=torch.bfloat16)
+    np.testing.assert_array_equal(r["expert"], want)
+    rt = O.route(inp.x, inp.w_r)
+    np.testing.assert_array_equal(rt.expert, want)
+    np.testing.assert_allclose(r["gate"], rt.gate, rtol=1e-5, atol=1e-7)
+    y_ref = O.moe_layer(inp.x, inp.w_r, inp.w_i, inp.w_o, forced=np.array(want))
+    assert O.max_abs_rel(y.float().cpu().numpy(), y_ref) <= BF16_TOL
 
 
 @pytest.mark.parametrize("routing,kw", [("zipf", {"s": 1.2}), ("uniform", {})])
 def test_c3_switch_base_128_full_size(routing, kw):
     # BASELINE.json configs[2]: E=128, h=768, d_ff=3072, batch 32 x seq 512 = 16384 tokens
-    _full_size_sampled(16384, 768, 3072, 128, 3, routing, **kw)
+    _full_size_all_tokens(16384, 768, 3072, 128, 3, routing, **kw)
 
 
 @pytest.mark.parametrize("k", [1, 3])
 def test_c4_switch_base_256_pathological_full_size(k):
     # BASELINE.json configs[3]: E=256, all tokens to k experts (253-255 empty experts)
-    _full_size_sampled(16384, 768, 3072, 256, 4, "patho", k=k)
+    _full_size_all_tokens(16384, 768, 3072, 256, 4, "patho", k=k)
 
 
 def test_c5_switch_large_128_full_size():
     # BASELINE.json configs[4]: h=1024, d_ff=4096, E=128, batch 64 x seq 512 = 32768 tokens
-    _full_size_sampled(32768, 1024, 4096, 128, 5, "uniform")
+    _full_size_all_tokens(32768, 1024, 4096, 128, 5, "uniform")
 
 
-# --------------------------------------------------------------------- full size (bench config)
-@pytest.mark.parametrize("routing", ["uniform", "zipf"])
-def test_c2_full_size_sampled(routing):
-    """BASELINE.json configs[1] at G=1 in bench.py's launch configuration:
-    E=64, N=8192, h=768, d_ff=3072, bf16. Routing tables exact on all tokens;
-    outputs vs the oracle on a seeded sample of tokens covering every expert."""
+def test_wide_rows_h4096():
+    """d_model = 4096 (bf16 rows of 512 16-B vectors, wider than one column block of the
+    grouping kernel's row copy) - every output row vs the oracle."""
+    inp = W.make_layer_inputs(27, 700, 4096, 256, 8, dtype=torch.bfloat16, routing="zipf")
+    L, y, r = _run(inp, dtype=torch.bfloat16, forced=inp.forced.cuda().contiguous())
+    _check_layer(inp, y, r, tol=BF16_TOL)
+    y_ref = O.moe_layer(inp.x, inp.w_r, inp.w_i, inp.w_o, forced=inp.forced.numpy())
+    assert per_row_rel(y.float().cpu().numpy(), y_ref) <= BF16_TOL
+
+
+def test_fp32_wide_rows_h2048():
+    """fp32 validation mode with d_model = 2048 (rows of 512 16-B vectors)."""
+    inp = W.make_layer_inputs(28, 300, 2048, 256, 4, dtype=torch.float32, routing="uniform")
+    L, y, r = _run(inp, dtype=torch.float32, forced=inp.forced.cuda().contiguous())
+    _check_layer(inp, y, r, tol=FP32_TOL)
+
+
+# --------------------------------------------------------------------- encoder stack, per MoE layer
+def test_c3_encoder_teacher_forced_moe_layers():
+    """SURVEY.md §8(d) C3 check: run the Switch-Base-128 encoder (12 layers, 6 MoE, batch 32 x
+    seq 512) with the natural router and capture every MoE layer's actual GPU input; the fp64
+    oracle then gets that same input (teacher forcing) and each MoE layer's routing (R13
+    ambiguity rule), gates and all 16384 output rows must match."""
+    from harness.encoder import EncoderConfig, SwitchEncoder
     from paper_2503_08467_b200 import MoEShardLayer
-    N, h, d_ff, E, seed = 8192, 768, 3072, 64, 2
-    dev = "cuda"
-    x = W.make_tokens(seed, N, h, device=dev)
-    w_r = W.make_router_weight(seed, h, E, device=dev)
-    w_i, w_o = W.make_expert_weights(seed, E, h, d_ff, device=dev)
-    forced = W.draw_experts(seed, N, E, routing, device=dev, s=1.2)
-    L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16)
-    L.load_expert_shards(0, w_i, w_o)
-    y = L.forward(0, x, w_r, forced_expert=forced)
-    r = {k: v.cpu().numpy() for k, v in L.routing(N).items()}
-    L.check()
-    fc = forced.cpu().numpy().astype(np.int64)
-    np.testing.assert_array_equal(r["expert"], fc)
-    counts, offsets, perm = O.group_per_expert(fc, E)
-    np.testing.assert_array_equal(r["counts"], counts)
-    np.testing.assert_array_equal(r["perm"], perm)
-    # sample: 4 tokens of every non-empty expert + 256 random tokens
-    rng = np.random.default_rng(0)
-    sample = set(rng.choice(N, 256, replace=False).tolist())
-    for e in range(E):
-        seg = perm[offsets[e]:offsets[e + 1]]
-        sample.update(seg[:2].tolist() + seg[-2:].tolist())
-    sample = np.array(sorted(sample))
-    wi_c, wo_c = w_i.cpu(), w_o.cpu()
-    y_s, rt = O.moe_layer_tokens(x[sample].cpu(), w_r.cpu(), lambda e: (wi_c[e], wo_c[e]),
-                                 forced_rows=fc[sample])
-    np.testing.assert_allclose(r["gate"][sample], rt.gate, rtol=1e-5, atol=1e-6)
-    err = O.max_abs_rel(y[sample].float().cpu().numpy(), y_s)
-    assert err <= BF16_TOL, err
-    # every output row was written (droplessness): no NaN/garbage, no zero rows
-    assert torch.isfinite(y).all() and (y.float().abs().sum(1) > 0).all()
+    cfg = EncoderConfig(d_model=768, d_ff=3072, n_heads=12, n_layers=12, n_experts=128,
+                        seq=512, batch=32)
+    seed = 3
+    factory = lambda n_moe, n_local: MoEShardLayer(cfg.d_model, cfg.d_ff, cfg.n_experts,
+                                                   n_layers=n_moe, max_tokens_per_rank=n_local,
+                                                   dtype=torch.bfloat16)
+    enc = SwitchEncoder(cfg, seed=seed, device="cuda", moe_layer_factory=factory)
+    x = W.make_tokens(seed, cfg.batch * cfg.seq, cfg.d_model, device="cuda").view(
+        cfg.batch, cfg.seq, cfg.d_model)
+    cap = []
+    enc.forward(x, capture=cap)
+    torch.cuda.synchronize()
+    assert len(cap) == len(enc.moe_ids) == 6
+    N = cfg.batch * cfg.seq
+    for c in cap:
+        i = enc.moe_ids[c["slot"]]
+        s_l = seed * 1000 + i   # the encoder's per-layer seed (harness/encoder.py)
+        wi, wo = W.make_expert_weights(s_l, cfg.n_experts, cfg.d_model, cfg.d_ff, device="cuda")
+        wi_c, wo_c = wi.cpu(), wo.cpu()
+        del wi, wo
+        xin, w_r = c["input"].cpu(), enc.layers[i]["w_r"].cpu()
+        r = {k: v.cpu().numpy() for k, v in c["routing"].items()}
+        experts = _check_routing(r, xin, w_r, None)
+        counts, offsets, perm = O.group_per_expert(experts, cfg.n_experts)
+        np.testing.assert_array_equal(r["counts"], counts)
+        np.testing.assert_array_equal(r["perm"], perm)
+        y_ref, rt = O.moe_layer_tokens(xin, w_r, lambda e: (wi_c[e], wo_c[e]), forced_rows=experts)
+        np.testing.assert_allclose(r["gate"], rt.gate, rtol=1e-5, atol=1e-6)
+        yc = c["output"].float().cpu().numpy()
+        err, row = O.max_abs_rel(yc, y_ref), per_row_rel(yc, y_ref)
+        print(f"encoder MoE layer {i}: max-abs-rel {err:.2e} per-row {row:.2e} "
+              f"ambiguous {int((experts != O.route(xin, w_r).expert).sum())}")
+        assert err <= BF16_TOL and row <= BF16_TOL, (i, err, row)
+        assert yc.shape == (N, cfg.d_model)
+    enc.moe.close()
 
 
-# --------------------------------------------------------------------- fused route + group (world = 1)
-@pytest.mark.parametrize("N,h,d_ff,E,routing", [
-    (3000, 512, 1024, 64, "zipf"),       # 24 router CTAs, multi-chunk segments
-    (18944, 256, 256, 16, "uniform"),    # 148 hist-blocks = one CTA on every SM (largest fused grid)
-    (18945, 256, 256, 16, "uniform"),    # 149 blocks: falls back to the separate grouping launches
-    (700, 1024, 512, 256, "patho"),      # E = 256 (two expert scans per CTA), h = 1024
-])
-def test_route_group_fused_matches_separate_and_oracle(N, h, d_ff, E, routing):
-    """Step 2 inside the router launch (grid barriers) == the separate launches,
-    bit for bit, and == the oracle; repeated forwards reuse the barrier."""
-    from paper_2503_08467_b200 import MoEShardLayer
-    from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_FUSED_ROUTE_GROUP
-    inp = W.make_layer_inputs(23, N, h, d_ff, E, dtype=torch.bfloat16, routing=routing, k=2)
-    f = inp.forced.cuda().contiguous()
-    outs, routes = [], []
-    for flags in (MOESHARD_FLAG_FUSED_ROUTE_GROUP, 0):
-        L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16, flags=flags)
-        L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
-        for _ in range(3):
-            y = L.forward(0, inp.x.cuda(), inp.w_r.cuda(), forced_expert=f)
-        L.check()
-        torch.cuda.synchronize()
-        outs.append(y.clone())
-        routes.append({k: v.cpu().numpy() for k, v in L.routing(N).items()})
-        L.close()
-    assert torch.equal(outs[0], outs[1])
-    for k in routes[0]:
-        np.testing.assert_array_equal(routes[0][k], routes[1][k])
-    _check_layer(inp, outs[0], routes[0], tol=BF16_TOL)
-
-
-@pytest.mark.parametrize("flag", ["FUSED_ROUTE_GROUP", "CPASYNC_GATHER", "ROW_COPY_IN_FFN", "FUSED_SCAN",
-                                  "DYNAMIC_SCHED", "FORCE_COLLECTIVES", None])
+@pytest.mark.parametrize("flag", ["DYNAMIC_SCHED", "FORCE_COLLECTIVES", "UNFUSED_GEMM", None])
 def test_forward_under_cuda_graph_replay(flag):
     """A captured forward replays correctly with new token values and new routing
-    (the grid barrier of the fused route+group launch carries no launch arguments)."""
+    (no launch argument depends on the data: tables and counters live on the device)."""
     from paper_2503_08467_b200 import MoEShardLayer
     from paper_2503_08467_b200 import moeshard as C
     flags = getattr(C, f"MOESHARD_FLAG_{flag}") if flag else 0
@@ -449,9 +478,9 @@ def test_forward_under_cuda_graph_replay(flag):
 
 
 @pytest.mark.parametrize("uneven", [False, True])
-def test_token_allgather_overlap_matches_serial(uneven, monkeypatch):
+def test_token_allgather_overlap_matches_serial(uneven):
     """Step 3's token AllGather forked onto a side stream ahead of the router (default) gives
-    bit-identical routing and outputs to the all-on-one-stream order (MOESHARD_OVERLAP_AG=0),
+    bit-identical routing and outputs to the all-on-one-stream order (MOESHARD_FLAG_SERIAL_AG),
     through the NCCL exchange (one rank), eagerly and back to back on the same inputs."""
     from paper_2503_08467_b200 import MoEShardLayer
     from paper_2503_08467_b200 import moeshard as C
@@ -459,10 +488,9 @@ def test_token_allgather_overlap_matches_serial(uneven, monkeypatch):
     N, h, d_ff, E = 1500, 256, 512, 16
     inp = W.make_layer_inputs(26, N, h, d_ff, E, dtype=torch.bfloat16, routing="zipf")
     outs, routes = [], []
-    for ov in ("1", "0"):
-        monkeypatch.setenv("MOESHARD_OVERLAP_AG", ov)
+    for extra in (0, C.MOESHARD_FLAG_SERIAL_AG):
         L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N + 37 if uneven else N,
-                          dtype=torch.bfloat16, flags=flags)
+                          dtype=torch.bfloat16, flags=flags | extra)
         L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
         x, w_r, f = inp.x.cuda(), inp.w_r.cuda(), inp.forced.cuda()
         for _ in range(3):
@@ -485,19 +513,17 @@ def test_token_allgather_overlap_matches_serial(uneven, monkeypatch):
         _check_layer(inp, outs[0], routes[0], tol=BF16_TOL)
 
 
-# --------------------------------------------------------------------- alternative token paths
-@pytest.mark.parametrize("flag", ["DYNAMIC_SCHED", "ROUTER_TOK64", "FUSED_SCAN", "ROW_COPY_IN_FFN", "CPASYNC_GATHER",
-                                  "TMA_GATHER", "FUSED_ROUTE_GROUP"])
+# --------------------------------------------------------------------- alternative schedules
+@pytest.mark.parametrize("flag", ["DYNAMIC_SCHED", "UNFUSED_GEMM"])
 @pytest.mark.parametrize("N,h,d_ff,E,routing", [
     (3000, 512, 1024, 64, "zipf"),       # multi-chunk segments, ragged halves
     (777, 384, 640, 16, "patho"),        # odd tile counts (duplicated last pair), empty experts
     (8192, 768, 3072, 64, "zipf"),       # C2 shape
 ])
-def test_token_paths_bitwise_equal_and_match_oracle(flag, N, h, d_ff, E, routing):
-    """How the expert-ordered token rows reach the up-projection (copied by the grouping
-    launch - the default -, copied inside the FFN launch, gathered by cp.async or TMA
-    gather4, grouped inside the router launch) changes no arithmetic: outputs and
-    routing tables are identical bit for bit, and match the oracle."""
+def test_schedules_bitwise_equal_and_match_oracle(flag, N, h, d_ff, E, routing):
+    """How the fused FFN's work units reach the clusters (static round robin - the default -
+    or a global counter) and whether both products run in one launch or two changes no
+    arithmetic: outputs and routing tables are identical bit for bit, and match the oracle."""
     from paper_2503_08467_b200 import MoEShardLayer
     from paper_2503_08467_b200 import moeshard as C
     inp = W.make_layer_inputs(26, N, h, d_ff, E, dtype=torch.bfloat16, routing=routing, k=1)
@@ -516,8 +542,7 @@ def test_token_paths_bitwise_equal_and_match_oracle(flag, N, h, d_ff, E, routing
     assert torch.equal(ys[0], ys[1])
     for k in routes[0]:
         np.testing.assert_array_equal(routes[0][k], routes[1][k])
-    if N <= 3000:
-        _check_layer(inp, ys[0], routes[0], tol=BF16_TOL)
+    _check_layer(inp, ys[0], routes[0], tol=BF16_TOL)
 
 
 # --------------------------------------------------------------------- peer-memory exchange

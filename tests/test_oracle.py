@@ -84,6 +84,36 @@ def test_router_gate_is_softmax_probability_of_chosen_expert():
         assert rf.gate[t] == pytest.approx(z[forced[t]] / sum(z), rel=1e-12)
 
 
+def test_routing_margin_worked_cases(golden):
+    g = golden("routing_margin.json")
+    for c in g["cases"]:
+        want = [np.inf if v == "inf" else v for v in c["margin"]]
+        np.testing.assert_array_equal(O.routing_margin(np.array(c["logits"])), want)
+    # SPEC.md:130 example: two experts, gate g printed -> margin = log(g / (1 - g)) = 5
+    gate = g["spec_gate"]
+    rt = O.route(np.array([[5.0, 0.0]]), np.eye(2))
+    assert abs(O.routing_margin(rt.logits)[0] - np.log(gate / (1 - gate))) < 1e-12
+
+
+def test_routing_margin_brute_force_and_invariances():
+    """Against a pure-Python pairwise definition (max over e of l_e minus max over the
+    others), and invariant to permuting experts and to a common shift of the logits."""
+    rng = np.random.default_rng(3)
+    L = rng.normal(size=(50, 9))
+    top = L.max(axis=1)[::7] + 1.0
+    L[::7, 2] = top                             # exact ties for the maximum on some rows
+    L[::7, 4] = top
+    want = []
+    for row in L.tolist():
+        best = max(range(len(row)), key=lambda e: (row[e], -e))
+        want.append(row[best] - max(v for e, v in enumerate(row) if e != best))
+    np.testing.assert_array_equal(O.routing_margin(L), np.array(want))
+    perm = rng.permutation(9)
+    np.testing.assert_array_equal(O.routing_margin(L[:, perm]), O.routing_margin(L))
+    np.testing.assert_allclose(O.routing_margin(L + 3.5), O.routing_margin(L), atol=1e-12)
+    assert (O.routing_margin(L)[::7] == 0).all()
+
+
 def test_router_shape_and_bounds_errors():
     with pytest.raises(ValueError):
         O.route(np.zeros((3, 4)), np.zeros((5, 2)))
