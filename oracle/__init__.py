@@ -22,7 +22,9 @@ Readings of the paper (R1-R19) used here:
   R2  y = g_t * FFN(x_t), g_t = softmax(logits_t)[e_t];
   R3  no router bias / temperature / jitter, no expert biases;
   R4  argmax ties -> lowest expert index;
-  R12 error metric max|y - y_ref| / max|y_ref|.
+  R12 error metric max|y - y_ref| / max|y_ref|;
+  R20 expert-parallel baseline: capacity ceil(CF n / |E|), CF = min(|E|, 50),
+      first-come admission per GPU, dropped tokens give a zero MoE output.
 
 Parity status: every function below is pinned by a ``-m "not gpu"`` test in
 tests/test_oracle.py (worked examples under tests/golden/, closed forms,
@@ -40,6 +42,7 @@ __all__ = [
     "moe_layer_sharded", "brute_force_layer", "shard_plan", "extract_shard",
     "transfer_entries", "shard_storage_entries", "scatter_payload_bytes",
     "macs_per_rank", "max_abs_rel", "routing_margin", "Routing",
+    "ep_capacity", "ep_admit", "moe_layer_ep",
 ]
 
 
@@ -276,6 +279,72 @@ def moe_layer_sharded(x_per_gpu: Sequence, w_r, w_i, w_o, forced_per_gpu=None, s
         stats["macs_per_rank"] = macs
         stats["m_sizes"] = m_sizes_recv
         stats["tokens_per_rank"] = [sum(int(m_sizes_recv[g].sum()) for g in range(G))] * G
+    return outputs
+
+
+# ---------------------------------------------------------------------------
+# Expert-parallel baseline (the paper's comparison system)
+#   PAPER.md:153-161 (EP forward), 393-398 (DeepSpeed baseline, CF = min(|E|, 50))
+# ---------------------------------------------------------------------------
+def ep_capacity(n_tokens: int, E: int, capacity_factor=None) -> int:
+    """Tokens each expert admits from one GPU's minibatch: ceil(CF * n / |E|), with the
+    paper's CF = min(|E|, 50) by default (reading R20)."""
+    cf = min(E, 50) if capacity_factor is None else capacity_factor
+    return int(np.ceil(cf * n_tokens / E))
+
+
+def ep_admit(expert, E: int, capacity: int) -> np.ndarray:
+    """First-come admission inside one GPU's minibatch: token t is kept iff fewer than
+    `capacity` earlier tokens (in token order) chose the same expert (R20)."""
+    expert = np.asarray(expert, dtype=np.int64).reshape(-1)
+    seen = np.zeros(E, dtype=np.int64)
+    keep = np.zeros(expert.shape[0], dtype=bool)
+    for t, e in enumerate(expert.tolist()):
+        keep[t] = seen[e] < capacity
+        seen[e] += 1
+    return keep
+
+
+def moe_layer_ep(x_per_gpu: Sequence, w_r, w_i, w_o, capacity_factor=None, forced_per_gpu=None,
+                 stats=None):
+    """Expert parallelism, step by step: the router is replicated and each
+    GPU routes its own minibatch; GPU o hosts the |E|/|G| whole experts
+    [o*|E|/|G|, (o+1)*|E|/|G|); an all-to-all scatter sends every admitted token to the GPU
+    hosting its expert, which computes it with the full expert; an all-to-all gather returns
+    the results, scaled by the gate. A token beyond its expert's capacity (first-come per
+    GPU, ep_admit) is dropped: its MoE output is zero (the residual carries it, R20).
+
+    Returns the per-GPU outputs; ``stats`` receives per-GPU received-token counts, MACs and
+    the dropped-token count."""
+    G = len(x_per_gpu)
+    xs = [_f64(x) for x in x_per_gpu]
+    w_i, w_o = _f64(w_i), _f64(w_o)
+    E = w_i.shape[0]
+    if E % G:
+        raise ValueError(f"moe_layer_ep: |E|={E} not divisible by |G|={G}")
+    E_loc = E // G
+    routings = [route(xs[g], w_r, None if forced_per_gpu is None else forced_per_gpu[g])
+                for g in range(G)]
+    keeps = [ep_admit(routings[g].expert, E, ep_capacity(xs[g].shape[0], E, capacity_factor))
+             for g in range(G)]
+    # all-to-all scatter: inbox[o] = (source GPU, token index) pairs of o's experts
+    inbox = [[] for _ in range(G)]
+    for g in range(G):
+        for t in np.nonzero(keeps[g])[0].tolist():
+            inbox[int(routings[g].expert[t]) // E_loc].append((g, t))
+    outputs = [np.zeros_like(xs[g]) for g in range(G)]
+    macs = [0] * G
+    for o in range(G):                     # expert computation on the hosting GPU
+        for g, t in inbox[o]:
+            e = int(routings[g].expert[t])
+            y = expert_ffn(xs[g][t:t + 1], w_i[e], w_o[e])[0]
+            outputs[g][t] = routings[g].gate[t] * y   # all-to-all gather back to GPU g
+            macs[o] += 2 * w_i.shape[1] * w_i.shape[2]
+    if stats is not None:
+        stats["tokens_per_rank"] = [len(inbox[o]) for o in range(G)]
+        stats["macs_per_rank"] = macs
+        stats["dropped"] = int(sum((~k).sum() for k in keeps))
+        stats["keep"] = keeps
     return outputs
 
 

@@ -301,3 +301,89 @@ def test_max_abs_rel_definition():
     ref = np.array([[1.0, -4.0], [2.0, 0.0]])
     y = ref + np.array([[0.1, 0.0], [0.0, -0.2]])
     assert O.max_abs_rel(y, ref) == pytest.approx(0.2 / 4.0)
+
+
+# ---------------------------------------------------------------------------
+# expert-parallel baseline
+# ---------------------------------------------------------------------------
+def test_ep_admission_worked_cases(golden):
+    for c in golden("ep_admission.json")["cases"]:
+        cap = O.ep_capacity(c["n"], c["E"], c["cf"])
+        assert cap == c["capacity"]
+        np.testing.assert_array_equal(O.ep_admit(c["expert"], c["E"], cap), c["keep"])
+
+
+def test_ep_paper_cf_never_drops_up_to_50_experts():
+    """CF = min(|E|, 50): capacity = n for |E| <= 50, so no routing drops a
+    token; above 50 experts the pathological routing drops n - ceil(50 n / |E|)."""
+    rng = np.random.default_rng(0)
+    for E in (1, 8, 50):
+        n = 37
+        for expert in (np.zeros(n, int), rng.integers(0, E, n)):
+            assert O.ep_admit(expert, E, O.ep_capacity(n, E)).all()
+    for E in (64, 128, 256):
+        n = 1000
+        keep = O.ep_admit(np.zeros(n, int), E, O.ep_capacity(n, E))
+        assert (~keep).sum() == n - math.ceil(50 * n / E)
+
+
+@pytest.mark.parametrize("G,E,routing", [(1, 8, "uniform"), (2, 8, "skew"), (4, 16, "zipf")])
+def test_ep_without_drops_equals_unsharded_layer(G, E, routing):
+    """With capacity >= n nothing is dropped and EP computes exactly the Switch layer:
+    the concatenated per-GPU outputs equal moe_layer (fp64, rounding order only)."""
+    import torch
+    import workload as W
+    n, h, d_ff = 40, 16, 24
+    inp = W.make_layer_inputs(5, G * n, h, d_ff, E, dtype=torch.float64, routing=routing, k_r=2)
+    xs = [inp.x[g * n:(g + 1) * n] for g in range(G)]
+    fs = [inp.forced[g * n:(g + 1) * n].numpy() for g in range(G)]
+    st = {}
+    ys = O.moe_layer_ep(xs, inp.w_r, inp.w_i, inp.w_o, capacity_factor=E, forced_per_gpu=fs, stats=st)
+    y_ref = O.moe_layer(inp.x, inp.w_r, inp.w_i, inp.w_o, forced=inp.forced.numpy())
+    np.testing.assert_allclose(np.concatenate(ys), y_ref, rtol=1e-12, atol=1e-12)
+    assert st["dropped"] == 0 and sum(st["tokens_per_rank"]) == G * n
+
+
+def test_ep_matches_brute_force_with_drops():
+    """Tiny inputs with a capacity that bites: kept tokens equal the dense per-token brute
+    force, dropped tokens are exactly zero, and the kept set is first-come per GPU."""
+    import torch
+    import workload as W
+    G, n, h, d_ff, E = 2, 12, 8, 16, 4
+    inp = W.make_layer_inputs(9, G * n, h, d_ff, E, dtype=torch.float64, routing="patho", k=2)
+    xs = [inp.x[g * n:(g + 1) * n] for g in range(G)]
+    fs = [inp.forced[g * n:(g + 1) * n].numpy() for g in range(G)]
+    st = {}
+    ys = O.moe_layer_ep(xs, inp.w_r, inp.w_i, inp.w_o, capacity_factor=1.0, forced_per_gpu=fs, stats=st)
+    dense = O.brute_force_layer(inp.x, inp.w_r, inp.w_i, inp.w_o, forced=inp.forced.numpy())
+    cap = math.ceil(n / E)
+    for g in range(G):
+        seen = {}
+        for t in range(n):
+            e = int(fs[g][t])
+            kept = seen.get(e, 0) < cap
+            seen[e] = seen.get(e, 0) + 1
+            assert st["keep"][g][t] == kept
+            if kept:
+                np.testing.assert_allclose(ys[g][t], dense[g * n + t], rtol=1e-12, atol=1e-12)
+            else:
+                assert (ys[g][t] == 0).all()
+    assert st["dropped"] > 0
+
+
+def test_ep_per_rank_load_under_pathological_routing():
+    """SPEC.md:474-482 contrast: under EP all tokens routed to one expert land on one GPU
+    (max/mean load = G), while MoEShard's per-GPU MACs are identical whatever the routing."""
+    import torch
+    import workload as W
+    G, n, h, d_ff, E = 4, 30, 8, 16, 8
+    inp = W.make_layer_inputs(11, G * n, h, d_ff, E, dtype=torch.float64, routing="patho", k=1)
+    xs = [inp.x[g * n:(g + 1) * n] for g in range(G)]
+    fs = [inp.forced[g * n:(g + 1) * n].numpy() for g in range(G)]
+    st = {}
+    O.moe_layer_ep(xs, inp.w_r, inp.w_i, inp.w_o, capacity_factor=E, forced_per_gpu=fs, stats=st)
+    load = np.array(st["tokens_per_rank"])
+    assert load.max() == G * n and load.sum() == G * n and load.max() / load.mean() == G
+    st2 = {}
+    O.moe_layer_sharded(xs, inp.w_r, inp.w_i, inp.w_o, forced_per_gpu=fs, stats=st2)
+    assert len(set(st2["macs_per_rank"])) == 1
