@@ -80,6 +80,16 @@ typedef enum {
 #define MOESHARD_FLAG_UNEVEN_TOKENS 0x2000u  /* world > 1: ranks may pass different n_local each forward; token slots of max_tokens_per_rank rows per rank, routing tables [world * max_tokens_per_rank] with expert -1 in unused slots */
 #define MOESHARD_FLAG_P2P 0x200u             /* bf16: Steps 3 and 5 by device-initiated stores into peer GPU memory instead of NCCL (see moeshard_p2p_*) */
 #define MOESHARD_FLAG_SERIAL_AG 0x4000u      /* NCCL transport: token AllGather on the caller's stream after the router (default: a side stream, overlapping the router) */
+/* The paper's comparison system instead of MoEShard: expert parallelism with
+ * the DeepSpeed capacity of PAPER.md:393-398. Rank r hosts the E/world whole experts
+ * [r*E/world, (r+1)*E/world) - moeshard_load_expert_shards then takes w_in [E/world][h][d_ff]
+ * and w_out [E/world][d_ff][h] - and every admitted token is computed only by its expert's host:
+ * all-to-all scatter and gather over peer memory (requires MOESHARD_FLAG_P2P and E % world == 0;
+ * token slots of max_tokens_per_rank rows as with MOESHARD_FLAG_UNEVEN_TOKENS). Each expert
+ * admits at most cap = ceil(CF * n_local / E) tokens of a rank's minibatch, first come (token
+ * order); a dropped token's output row is zero. CF = config.ep_capacity_factor, or min(E, 50)
+ * when <= 0. Baseline for measurement; MoEShard itself never drops a token. */
+#define MOESHARD_FLAG_EXPERT_PARALLEL 0x8000u
 
 /* moeshard_forward_stages masks: ROUTE = Step 1 + the token exchange (Step 3 push),
  * COMPUTE = Steps 2 and 4 (+ the Step 5 send in P2P mode), REDUCE = the Step 5 aggregate. */
@@ -97,6 +107,7 @@ typedef struct {
   int32_t max_tokens_per_rank; /* upper bound on n_local */
   int32_t dtype;               /* moeshard_dtype */
   uint32_t flags;              /* MOESHARD_FLAG_* */
+  float ep_capacity_factor;    /* MOESHARD_FLAG_EXPERT_PARALLEL only: CF (<= 0: min(E, 50)) */
 } moeshard_config;
 
 typedef struct moeshard_ctx moeshard_ctx;
@@ -112,7 +123,8 @@ int moeshard_get_unique_id(uint8_t out[128]);
 int moeshard_workspace_size(const moeshard_config* cfg, int world, size_t* bytes);
 
 /* Bytes of device weight storage per layer: 2 * E * h * (d_ff/world) elements
- * of the config dtype. bytes_per_layer: [host] out. */
+ * of the config dtype (the same count, 2 * (E/world) * h * d_ff, for the
+ * MOESHARD_FLAG_EXPERT_PARALLEL baseline). bytes_per_layer: [host] out. */
 int moeshard_weight_storage_size(const moeshard_config* cfg, int world, size_t* bytes_per_layer);
 
 /* Create a context for `rank` of `world` on CUDA `device`.
@@ -210,6 +222,20 @@ int moeshard_p2p_connect(moeshard_ctx* ctx, void* const* regions);
 
 int moeshard_get_routing(moeshard_ctx* ctx, int32_t* expert_all, float* gate_all, int32_t* counts,
                          int32_t* offsets, int32_t* perm, void* stream);
+
+/* MOESHARD_FLAG_EXPERT_PARALLEL: the admission of the most recent forward, copied on `stream`
+ * into caller device buffers (any may be NULL):
+ *   owner    [dev] int32 [n_local]  rank hosting the expert of local token i, -1 if the
+ *                                   expert's capacity dropped it (its output row is zero)
+ *   expert   [dev] int32 [n_local]  e_i (global expert id) of local token i
+ *   gate     [dev] fp32  [n_local]  g_i
+ *   received [dev] int32 [E/world]  tokens (of all ranks) this rank's experts computed
+ * (moeshard_get_routing on an EP context describes the host side: expert_all / gate_all /
+ * perm over the world * max_tokens_per_rank received slots with LOCAL expert ids, -1 where
+ * not received; counts / offsets over the E/world local experts.)
+ * Errors: CONFIG (not an EP context), INVALID_ARG. */
+int moeshard_get_ep_admission(moeshard_ctx* ctx, int32_t* owner, int32_t* expert, float* gate,
+                              int32_t* received, void* stream);
 
 /* Per-forward work counters of the most recent forward ([host] out, syncs
  * the stream): tokens seen, grouped-GEMM tiles executed by the up and down

@@ -27,6 +27,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <algorithm>
@@ -124,14 +125,14 @@ constexpr int kL2PersistMB = 64;   // measured best of 0/32/48/64/79 MB on c2 (D
 constexpr uint32_t kKnownFlags =
     MOESHARD_FLAG_FORCE_COLLECTIVES | MOESHARD_FLAG_SIMT_GEMM | MOESHARD_FLAG_UNFUSED_GEMM |
     MOESHARD_FLAG_NO_L2_PERSIST | MOESHARD_FLAG_DYNAMIC_SCHED | MOESHARD_FLAG_UNEVEN_TOKENS |
-    MOESHARD_FLAG_P2P | MOESHARD_FLAG_SERIAL_AG;
+    MOESHARD_FLAG_P2P | MOESHARD_FLAG_SERIAL_AG | MOESHARD_FLAG_EXPERT_PARALLEL;
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 // Workspace carve-up, shared by moeshard_workspace_size and moeshard_init.
 struct Layout {
   size_t wt_r, route, block_hist, block_base, ints, done, perm, perm_pad, x_all, x_perm, H, partial,
-      total;
+      ep_route, ep_hist, ep_owner, total;
   int n_ints;
   size_t npad;   // rows of the internal expert-ordered layout: N_max + 32 per expert, rounded to 64
 };
@@ -143,7 +144,8 @@ Layout make_layout(const moeshard_config& c, int world) {
   const size_t Nmax = static_cast<size_t>(world) * c.max_tokens_per_rank;
   // hist-blocks: >= 64 tokens each (128 for the tcgen05 router), per rank
   const size_t nb = std::max<size_t>(1, world * ((c.max_tokens_per_rank + 63) / 64));
-  const size_t E = c.n_experts, h = c.d_model, F = c.d_ff / world;
+  const bool ep = (c.flags & MOESHARD_FLAG_EXPERT_PARALLEL) != 0;
+  const size_t E = c.n_experts, h = c.d_model, F = ep ? c.d_ff : c.d_ff / world;
   Layout L{};
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -167,6 +169,11 @@ Layout make_layout(const moeshard_config& c, int world) {
   L.x_perm = take(L.npad * h * elt);
   L.H = take(L.npad * F * elt);
   L.partial = coll ? take(Nmax * h * elt) : 0;
+  // EP baseline: this rank's own routing (the regions carry the hosts' copies)
+  const size_t nmax = static_cast<size_t>(c.max_tokens_per_rank);
+  L.ep_route = ep ? take(nmax * sizeof(RouteRec)) : 0;
+  L.ep_hist = ep ? take(((nmax + 127) / 128 + 1) * E * 4) : 0;
+  L.ep_owner = ep ? take(nmax * 4) : 0;
   L.total = off;
   return L;
 }
@@ -184,6 +191,13 @@ struct moeshard_ctx {
   moeshard_config cfg{};
   int rank = 0, world = 1, device = 0, num_sms = 148;
   int h = 0, F = 0, E = 0, elt = 2;
+  // EP baseline (MOESHARD_FLAG_EXPERT_PARALLEL): Et = experts hosted here (E / world), F = d_ff;
+  // MoEShard: Et = E, F = d_ff / world. The router always sees all E experts.
+  bool ep = false;
+  int Et = 0;
+  float ep_cf = 0.f;
+  RouteRec* ep_route = nullptr;
+  int32_t *ep_hist = nullptr, *ep_owner = nullptr;
   bool coll = false, use_tc = true;
   Layout L{};
   char* ws = nullptr;
@@ -290,9 +304,14 @@ int validate(const moeshard_config* c, int world) {
   if (c->d_ff < 1 || c->d_ff % world)
     return fail(nullptr, MOESHARD_ERR_DIVISIBILITY,
                 "d_ff=%d is not divisible by world=%d (PAPER.md:169, 329-330)", c->d_ff, world);
-  if ((c->d_ff / world) % 128)
+  const bool ep = (c->flags & MOESHARD_FLAG_EXPERT_PARALLEL) != 0;
+  if (!ep && (c->d_ff / world) % 128)
     return fail(nullptr, MOESHARD_ERR_CONFIG, "d_ff/world=%d must be a multiple of 128",
                 c->d_ff / world);
+  if (ep && (!(c->flags & MOESHARD_FLAG_P2P) || c->n_experts % world || c->d_ff % 128))
+    return fail(nullptr, MOESHARD_ERR_CONFIG,
+                "MOESHARD_FLAG_EXPERT_PARALLEL needs MOESHARD_FLAG_P2P, E %% world == 0 and d_ff %% 128 "
+                "== 0 (E=%d, world=%d, d_ff=%d)", c->n_experts, world, c->d_ff);
   if (c->n_layers < 1) return fail(nullptr, MOESHARD_ERR_CONFIG, "n_layers=%d < 1", c->n_layers);
   if (c->flags & ~kKnownFlags)
     return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "flags=0x%x has unknown bits (0x%x)", c->flags,
@@ -396,8 +415,12 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
   c->h = cfg->d_model;
-  c->F = cfg->d_ff / world;
+  c->ep = (cfg->flags & MOESHARD_FLAG_EXPERT_PARALLEL) != 0;
+  c->F = c->ep ? cfg->d_ff : cfg->d_ff / world;
   c->E = cfg->n_experts;
+  c->Et = c->ep ? cfg->n_experts / world : cfg->n_experts;
+  c->ep_cf = cfg->ep_capacity_factor > 0.f ? cfg->ep_capacity_factor
+                                          : static_cast<float>(std::min(cfg->n_experts, 50));
   c->elt = cfg->dtype == MOESHARD_BF16 ? 2 : 4;
   c->p2p = (c->cfg.flags & MOESHARD_FLAG_P2P) != 0;
   // coll: tokens of all ranks are exchanged (rank-major x_all / route / hist buffers)
@@ -438,6 +461,11 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->x_perm = c->ws + L.x_perm;
   c->H = c->ws + L.H;
   c->partial = c->coll && !c->p2p ? c->ws + L.partial : nullptr;
+  if (c->ep) {
+    c->ep_route = reinterpret_cast<RouteRec*>(c->ws + L.ep_route);
+    c->ep_hist = reinterpret_cast<int32_t*>(c->ws + L.ep_hist);
+    c->ep_owner = reinterpret_cast<int32_t*>(c->ws + L.ep_owner);
+  }
   c->layers.resize(cfg->n_layers);
   cudaError_t e = cudaMemset(ints, 0, L.n_ints * 4);
   if (e == cudaSuccess) e = cudaMemset(c->tb.done, 0, L.perm - L.done);
@@ -522,7 +550,7 @@ int moeshard_load_expert_shards(moeshard_ctx* c, int layer, const void* w_in_sha
     return fail(c, MOESHARD_ERR_INVALID_ARG, "NULL shard or storage pointer");
   if (reinterpret_cast<uintptr_t>(storage) & 255)
     return fail(c, MOESHARD_ERR_INVALID_ARG, "weight storage must be 256-B aligned");
-  const size_t per = static_cast<size_t>(c->E) * c->h * c->F * c->elt;
+  const size_t per = static_cast<size_t>(c->Et) * c->h * c->F * c->elt;   // Et experts' slices
   if (bytes < 2 * per)
     return fail(c, MOESHARD_ERR_SHAPE, "weight storage has %zu bytes, needs %zu", bytes, 2 * per);
   CUDA_TRY(c, cudaSetDevice(c->device));
@@ -532,16 +560,16 @@ int moeshard_load_expert_shards(moeshard_ctx* c, int layer, const void* w_in_sha
   lw.wt_out = static_cast<char*>(storage) + per;
   if (c->use_tc) {
     // swizzled contiguous 128 x 64 tiles of W_i^T [E][F][h] and W_o^T [E][h][F]
-    launch_pack_a_tiles(w_in_shard, lw.wt_in, c->E, c->h, c->F, s);
-    launch_pack_a_tiles(w_out_shard, lw.wt_out, c->E, c->F, c->h, s);
-    const uint64_t rows = static_cast<uint64_t>(c->E) * c->F * c->h / 64;
+    launch_pack_a_tiles(w_in_shard, lw.wt_in, c->Et, c->h, c->F, s);
+    launch_pack_a_tiles(w_out_shard, lw.wt_out, c->Et, c->F, c->h, s);
+    const uint64_t rows = static_cast<uint64_t>(c->Et) * c->F * c->h / 64;
     if (!make_tmap(&lw.tm_in, lw.wt_in, 64, rows, 128, false) ||
         !make_tmap(&lw.tm_out, lw.wt_out, 64, rows, 128, false))
       return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for weight tiles");
   } else {
     // W_i^r [E][h][F] -> [E][F][h];  W_o^r [E][F][h] -> [E][h][F]
-    launch_transpose(c->cfg.dtype, w_in_shard, lw.wt_in, c->E, c->h, c->F, s);
-    launch_transpose(c->cfg.dtype, w_out_shard, lw.wt_out, c->E, c->F, c->h, s);
+    launch_transpose(c->cfg.dtype, w_in_shard, lw.wt_in, c->Et, c->h, c->F, s);
+    launch_transpose(c->cfg.dtype, w_out_shard, lw.wt_out, c->Et, c->F, c->h, s);
   }
   CUDA_TRY(c, cudaGetLastError());
   lw.loaded = true;
@@ -575,7 +603,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   CUDA_TRY(c, cudaSetDevice(c->device));   // kernel attributes and launches target this device
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const LayerW& lw = c->layers[layer];
-  const int h = c->h, F = c->F, E = c->E;
+  const int h = c->h, F = c->F, E = c->E, Et = c->Et;   // Et: experts computed here
   if (!(stages & MOESHARD_STAGE_ROUTE) && n != c->last_n)
     return fail(c, MOESHARD_ERR_PROTOCOL, "n_local=%d differs from the ROUTE stage's %d", n,
                 c->last_n);
@@ -584,7 +612,8 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   // exchanges the per-GPU sizes): every rank's tokens occupy a slot of
   // ns = max_tokens_per_rank rows, the unused tail of a slot is marked invalid (expert -1)
   // and routes nowhere. Without the flag every rank passes the same n and ns = n.
-  const bool uneven = c->coll && (c->cfg.flags & MOESHARD_FLAG_UNEVEN_TOKENS);
+  // The EP baseline always uses slots (a host receives rows of every rank's slot).
+  const bool uneven = c->coll && (c->cfg.flags & (MOESHARD_FLAG_UNEVEN_TOKENS | MOESHARD_FLAG_EXPERT_PARALLEL));
   if (n == 0 && !uneven) return MOESHARD_OK;
   const int ns = uneven ? c->cfg.max_tokens_per_rank : n;   // rows per rank slot
   const bool st_route = stages & MOESHARD_STAGE_ROUTE, st_compute = stages & MOESHARD_STAGE_COMPUTE,
@@ -602,13 +631,15 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     CUDA_TRY(c, cudaEventRecord(c->ev_join, c->s_x));
   }
   // Step 1: route local tokens
-  RouteRec* my_route = c->route + (c->coll ? static_cast<size_t>(c->rank) * ns : 0);
+  // (EP: the router's output stays in the workspace; the dispatch writes the hosts' copies)
+  RouteRec* my_route = c->ep ? c->ep_route : c->route + (c->coll ? static_cast<size_t>(c->rank) * ns : 0);
   // tokens per hist-block = tokens per router CTA (128 for the tcgen05 router, 64 for SIMT)
   const int HB = c->use_tc ? kRouterTok : 64;
   const int nbr_own = (n + HB - 1) / HB;                // hist-blocks this rank's router fills
   const int nbr = (ns + HB - 1) / HB;                   // hist-blocks per rank slot
   const int NB = (c->coll ? c->world : 1) * nbr;
-  int32_t* my_hist = c->block_hist + (c->coll ? static_cast<size_t>(c->rank) * nbr * E : 0);
+  int32_t* my_hist = c->ep ? c->ep_hist
+                           : c->block_hist + (c->coll ? static_cast<size_t>(c->rank) * nbr * E : 0);
   const bool fused = c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_UNFUSED_GEMM) &&
                      F % kTcFeatTile == 0 && h % kTcFeatTile == 0;   // odd tile counts: see FFN kernel
   if (!st_route || n == 0) {
@@ -626,7 +657,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, my_hist, err_flag, s);
     c->launches += 1;
   }
-  if (st_route && uneven) {
+  if (st_route && uneven && !c->ep) {
     // the rest of this rank's slot: no token (expert -1), empty hist-blocks
     if (ns > n)
       CUDA_TRY(c, cudaMemsetAsync(my_route + n, 0xFF, static_cast<size_t>(ns - n) * sizeof(RouteRec), s));
@@ -637,7 +668,13 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   c->mark(1, s);
   // Steps 2+3: metadata + token scatter (replicate all tokens on all GPUs)
   const void* x_all = c->coll ? c->x_all : hidden;
-  if (st_route && c->p2p) {
+  if (st_route && c->ep) {
+    // EP all-to-all scatter: admitted rows only to their expert's host (capacity, first come)
+    const int cap = static_cast<int>(std::ceil(static_cast<double>(c->ep_cf) * n / E));
+    CUDA_TRY(c, launch_ep_dispatch(c->pa, hidden, n, h * c->elt / 16, c->ep_route, c->ep_hist, E, Et,
+                                   cap, c->ep_owner, s));
+    c->launches += 1;
+  } else if (st_route && c->p2p) {
     // Step 3 over peer memory: push this rank's tokens / records / histograms to every rank
     CUDA_TRY(c, launch_p2p_push(c->pa, hidden, n, ns, h * c->elt / 16, nbr, E, c->num_sms, s));
     c->launches += 1;
@@ -658,7 +695,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
       c->launches += 1;
     }
     // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs
-    launch_group_blocks(c->block_hist, NB, E, c->block_base, c->block_tot, c->tb,
+    launch_group_blocks(c->block_hist, NB, Et, c->block_base, c->block_tot, c->tb,
                         F / kTcFeatTile, h / kTcFeatTile, c->route, x_all, ns, nbr, HB,
                         h * c->elt, c->perm, c->x_perm, s);
     c->launches += 2;
@@ -666,9 +703,9 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     // Step 4: expert computation, one grouped product per projection
     void* P = c->coll && !c->p2p ? c->partial : hidden_out;
     if (fused) {
-      TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
+      TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), Et, c->tb,
                   static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
-      TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
+      TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), Et, c->tb,
                   static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
       if (c->p2p) {   // Step 5 send: partial rows go straight to their owner's receive slot
         dn.p2p_n = ns;
@@ -679,7 +716,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
       }
       CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, c->tm_xperm16, lw.tm_out, c->tm_H16, up, dn,
                                     c->tb.done, (c->cfg.flags & MOESHARD_FLAG_DYNAMIC_SCHED) != 0,
-                                    /*early_tables=*/n > 0, c->num_sms, s));
+                                    /*early_tables=*/n > 0 && !c->ep, c->num_sms, s));
       c->mark(4, s);
       c->launches += 1;
       if (c->p2p) {
@@ -687,18 +724,18 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
         c->launches += 1;
       }
     } else if (c->use_tc) {
-      TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), E, c->tb,
+      TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), Et, c->tb,
                   static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
       CUDA_TRY(c, launch_tc_gemm(false, lw.tm_in, c->tm_xperm, c->tm_xperm16, up, c->num_sms, s));
       c->mark(4, s);
-      TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), E, c->tb,
+      TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), Et, c->tb,
                   static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
       CUDA_TRY(c, launch_tc_gemm(true, lw.tm_out, c->tm_H, c->tm_H16, dn, c->num_sms, s));
       c->launches += 2;
     } else {
-      launch_simt_up(c->cfg.dtype, c->x_perm, lw.wt_in, h, F, E, c->tb, c->H, c->num_sms, s);
+      launch_simt_up(c->cfg.dtype, c->x_perm, lw.wt_in, h, F, Et, c->tb, c->H, c->num_sms, s);
       c->mark(4, s);
-      launch_simt_down(c->cfg.dtype, c->H, lw.wt_out, F, h, E, c->tb, c->tb.perm_pad, c->route, P,
+      launch_simt_down(c->cfg.dtype, c->H, lw.wt_out, F, h, Et, c->tb, c->tb.perm_pad, c->route, P,
                        c->num_sms, s);
       c->launches += 2;
     }
@@ -706,7 +743,11 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   }
   c->mark(5, s);
   // Step 5: gather partial outputs to their owner and sum (aggregateTokens)
-  if (st_reduce && c->p2p) {
+  if (st_reduce && c->ep) {   // EP all-to-all gather: each token's row from its host
+    CUDA_TRY(c, launch_ep_combine(c->pa, n, h * c->elt / 16, c->ep_owner, hidden_out, err_flag,
+                                  c->num_sms, s));
+    c->launches += 1;
+  } else if (st_reduce && c->p2p) {
     CUDA_TRY(c, launch_p2p_reduce(c->pa, n, h * c->elt / 16, hidden_out, err_flag, c->num_sms, s));
     c->launches += 1;
   } else if (st_reduce && c->coll && !uneven) {
@@ -776,7 +817,7 @@ int moeshard_get_routing(moeshard_ctx* c, int32_t* expert_all, float* gate_all, 
                          int32_t* offsets, int32_t* perm, void* stream) {
   if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "ctx is NULL");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const bool uneven = c->coll && (c->cfg.flags & MOESHARD_FLAG_UNEVEN_TOKENS);
+  const bool uneven = c->coll && (c->cfg.flags & (MOESHARD_FLAG_UNEVEN_TOKENS | MOESHARD_FLAG_EXPERT_PARALLEL));
   const size_t N = static_cast<size_t>(c->coll ? c->world : 1) *
                    (uneven ? c->cfg.max_tokens_per_rank : c->last_n);
   if (N > 0) {
@@ -789,10 +830,30 @@ int moeshard_get_routing(moeshard_ctx* c, int32_t* expert_all, float* gate_all, 
     if (perm) CUDA_TRY(c, cudaMemcpyAsync(perm, c->perm, N * 4, cudaMemcpyDeviceToDevice, s));
   }
   if (counts)
-    CUDA_TRY(c, cudaMemcpyAsync(counts, c->tb.counts, c->E * 4, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(counts, c->tb.counts, c->Et * 4, cudaMemcpyDeviceToDevice, s));
   if (offsets)
-    CUDA_TRY(c, cudaMemcpyAsync(offsets, c->tb.offsets, (c->E + 1) * 4, cudaMemcpyDeviceToDevice,
+    CUDA_TRY(c, cudaMemcpyAsync(offsets, c->tb.offsets, (c->Et + 1) * 4, cudaMemcpyDeviceToDevice,
                                 s));
+  return MOESHARD_OK;
+}
+
+int moeshard_get_ep_admission(moeshard_ctx* c, int32_t* owner, int32_t* expert, float* gate,
+                              int32_t* received, void* stream) {
+  if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "ctx is NULL");
+  if (!c->ep) return fail(c, MOESHARD_ERR_CONFIG, "context was not created with MOESHARD_FLAG_EXPERT_PARALLEL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t n = static_cast<size_t>(c->last_n);
+  if (n > 0) {
+    if (owner) CUDA_TRY(c, cudaMemcpyAsync(owner, c->ep_owner, n * 4, cudaMemcpyDeviceToDevice, s));
+    if (expert)
+      CUDA_TRY(c, cudaMemcpy2DAsync(expert, 4, &c->ep_route[0].expert, sizeof(RouteRec), 4, n,
+                                    cudaMemcpyDeviceToDevice, s));
+    if (gate)
+      CUDA_TRY(c, cudaMemcpy2DAsync(gate, 4, &c->ep_route[0].gate, sizeof(RouteRec), 4, n,
+                                    cudaMemcpyDeviceToDevice, s));
+  }
+  if (received)
+    CUDA_TRY(c, cudaMemcpyAsync(received, c->tb.counts, c->Et * 4, cudaMemcpyDeviceToDevice, s));
   return MOESHARD_OK;
 }
 

@@ -21,6 +21,7 @@
 // Waits are bounded: a peer that never arrives sets error bit 4 (reported by
 // moeshard_check) instead of hanging the GPU.
 #include "common.cuh"
+#include "group.cuh"
 #include "p2p.cuh"
 #include "ptx.cuh"
 
@@ -186,6 +187,153 @@ __global__ void wait_tokens(P2PArgs a, int32_t* err) {
     wait_flags(reinterpret_cast<const int32_t*>(a.self) + 32, a.world, epoch + 1, err);
 }
 
+// ===========================================================================
+// Expert-parallel baseline (MOESHARD_FLAG_EXPERT_PARALLEL, the
+// comparison system of Sec. 4, with the DeepSpeed capacity of PAPER.md:393-398).
+// Rank o hosts whole experts [o*E_loc, (o+1)*E_loc). The all-to-all scatter is a
+// routed push: each admitted token row goes only to its expert's host, into the
+// same rank-major x_all slot MoEShard uses (row r*n_max + i), with a route record
+// carrying the LOCAL expert id (-1 in every other host's copy) and per-block
+// histograms over the host's experts - so the host runs the unchanged Step-2
+// grouping and fused FFN (F = d_ff) on what it received, and its down epilogue
+// stores each result row into the source rank's receive slot (the all-to-all
+// gather). Admission is first-come inside the source rank's minibatch: token i of
+// expert e is kept iff fewer than `cap` earlier tokens of this rank chose e.
+// ===========================================================================
+
+// One group of kSplit CTAs per 128-token block of this rank's slot (n_max rows).
+template <int kSplit>
+__global__ void __launch_bounds__(256) ep_dispatch(P2PArgs a, const uint4* __restrict__ x, int n,
+                                                   int row_vecs, const RouteRec* __restrict__ rec,
+                                                   const int32_t* __restrict__ hist, int E,
+                                                   int E_loc, int cap, int32_t* __restrict__ owner) {
+  constexpr int kThreads = 256, kRows = 128 / kSplit;
+  __shared__ int32_t s_pre[kMaxExperts];      // this rank's tokens of e in earlier blocks
+  __shared__ int32_t s_kept[kMaxExperts];     // admitted tokens of e in this block
+  __shared__ int32_t whist[4][kMaxExperts];
+  __shared__ int32_t s_own[128];              // host rank of each token of the block, -1 dropped
+  __shared__ int32_t s_el[128];               // local expert id at the host
+  ptx::griddep_wait();   // route records / histograms come from the router
+  const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
+  const int b = blockIdx.x / kSplit, part = blockIdx.x % kSplit;
+  const int nbr = (a.n_max + 127) / 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb_own = (n + 127) / 128;   // blocks holding tokens (the router's histograms)
+  for (int e = threadIdx.x; e < E; e += kThreads) {
+    int sum = 0;
+    for (int bb = 0; bb < min(b, nb_own); ++bb) sum += __ldg(hist + static_cast<size_t>(bb) * E + e);
+    s_pre[e] = sum;
+    s_kept[e] = 0;
+  }
+  for (int k = threadIdx.x; k < 4 * E; k += kThreads) whist[k / E][k % E] = 0;
+  __syncthreads();
+  int e = -1, rank_w = 0;
+  const int t = b * 128 + threadIdx.x;
+  float gate = 0.f;
+  if (warp < 4) {
+    if (t < n) {
+      const RouteRec r = rec[t];
+      e = r.expert;
+      gate = r.gate;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    rank_w = __popc(peers & lanemask_lt());
+    if (e >= 0 && rank_w == 0) whist[warp][e] = __popc(peers);
+  }
+  __syncthreads();
+  if (warp < 4) {
+    int own = -1, el = -1;
+    if (e >= 0) {
+      int before = 0;
+      for (int w = 0; w < warp; ++w) before += whist[w][e];
+      if (s_pre[e] + before + rank_w < cap) {   // first-come admission (R20)
+        own = e / E_loc;
+        el = e - own * E_loc;
+        atomicAdd(&s_kept[e], 1);
+      }
+    }
+    s_own[threadIdx.x] = own;
+    s_el[threadIdx.x] = el;
+    if (part == 0 && t < a.n_max) {
+      if (t < n) owner[t] = own;
+      for (int g = 0; g < a.world; ++g) {   // every host's copy of this rank's slot
+        RouteRec r;
+        r.expert = g == own ? el : -1;
+        r.gate = g == own ? gate : 0.f;
+        reinterpret_cast<RouteRec*>(a.peers[g] + a.off_route)[static_cast<size_t>(a.rank) * a.n_max + t] = r;
+      }
+    }
+  }
+  __syncthreads();
+  if (part == 0 && b < nbr) {   // admitted-token histograms over each host's experts
+    for (int k = threadIdx.x; k < a.world * E_loc; k += kThreads) {
+      const int g = k / E_loc, el = k - g * E_loc;
+      int32_t* dh = reinterpret_cast<int32_t*>(a.peers[g] + a.off_hist);
+      dh[(static_cast<size_t>(a.rank) * nbr + b) * E_loc + el] = s_kept[g * E_loc + el];
+    }
+  }
+  // admitted rows to their host's x_all slot (8 warps x kRows / 8 rows, 16-B vectors)
+  for (int rr = warp; rr < kRows; rr += kThreads / 32) {
+    const int j = part * kRows + rr;
+    const int own = s_own[j];
+    const int tt = b * 128 + j;
+    if (own < 0) continue;
+    const uint4* src = x + static_cast<size_t>(tt) * row_vecs;
+    uint4* dst = reinterpret_cast<uint4*>(a.peers[own] + a.off_x) +
+                 (static_cast<size_t>(a.rank) * a.n_max + tt) * row_vecs;
+    for (int c = lane; c < row_vecs; c += 32) dst[c] = __ldg(src + c);
+  }
+  // publish: every CTA's stores fenced at system scope, then the last CTA raises
+  // flags_ag[rank] on every host (as push_tokens)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    int32_t* ctr = reinterpret_cast<int32_t*>(a.self) + 1;
+    if (atomicAdd(ctr, 1) == static_cast<int>(gridDim.x) - 1) {
+      *ctr = 0;
+      __threadfence_system();
+      for (int g = 0; g < a.world; ++g)
+        st_release_sys(reinterpret_cast<int32_t*>(a.peers[g]) + 32 * (1 + a.rank), epoch + 1);
+    }
+  }
+}
+
+// EP all-to-all gather: out[i] = recv[owner[i]][i] (the host's gate-scaled row), 0 for a
+// dropped token; waits for every host's signal, then advances the epoch.
+__global__ void __launch_bounds__(256) ep_combine(P2PArgs a, int n, int row_vecs,
+                                                  const int32_t* __restrict__ owner,
+                                                  uint4* __restrict__ out, int32_t* err) {
+  const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
+  if (threadIdx.x == 0)
+    wait_flags(reinterpret_cast<const int32_t*>(a.self) + 32 * (1 + a.world), a.world, epoch + 1,
+               err);
+  __syncthreads();
+  const uint4* recv = reinterpret_cast<const uint4*>(a.self + a.off_recv);
+  const size_t slot = static_cast<size_t>(a.n_max) * row_vecs;
+  const int warps = gridDim.x * (blockDim.x / 32);
+  const int lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n; i += warps) {
+    const int o = __ldg(owner + i);
+    uint4* dst = out + static_cast<size_t>(i) * row_vecs;
+    if (o < 0) {
+      for (int c = lane; c < row_vecs; c += 32) dst[c] = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+      const uint4* src = recv + o * slot + static_cast<size_t>(i) * row_vecs;
+      for (int c = lane; c < row_vecs; c += 32) dst[c] = __ldcg(src + c);   // peers' writes: L2
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t* ctr = reinterpret_cast<int32_t*>(a.self) + 2;
+    __threadfence();
+    if (atomicAdd(ctr, 1) == static_cast<int>(gridDim.x) - 1) {
+      *ctr = 0;
+      *reinterpret_cast<volatile int32_t*>(a.self) = epoch + 1;
+      __threadfence();
+    }
+  }
+}
+
 }  // namespace
 
 P2PLayout p2p_layout(int world, int n_max, int h, int E, int nbr_max) {
@@ -211,6 +359,21 @@ cudaError_t launch_p2p_push(const P2PArgs& a, const void* x, int n, int ns, int 
   const int grid = static_cast<int>(std::min<size_t>(4 * num_sms, (work + 1023) / 1024));
   return launch_pdl(push_tokens, dim3(std::max(grid, 1)), dim3(256), 0, s, a,
                     static_cast<const uint4*>(x), n, ns, row_vecs, nbr, E);
+}
+
+cudaError_t launch_ep_dispatch(const P2PArgs& a, const void* x, int n, int row_vecs,
+                               const RouteRec* rec, const int32_t* hist, int E, int E_loc, int cap,
+                               int32_t* owner, cudaStream_t s) {
+  const int nbr = (a.n_max + 127) / 128;
+  return launch_pdl(ep_dispatch<4>, dim3(nbr * 4), dim3(256), 0, s, a, static_cast<const uint4*>(x),
+                    n, row_vecs, rec, hist, E, E_loc, cap, owner);
+}
+
+cudaError_t launch_ep_combine(const P2PArgs& a, int n, int row_vecs, const int32_t* owner, void* out,
+                              int32_t* err, int num_sms, cudaStream_t s) {
+  const int grid = std::max(1, std::min(4 * num_sms, (n + 7) / 8));
+  ep_combine<<<grid, 256, 0, s>>>(a, n, row_vecs, owner, static_cast<uint4*>(out), err);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_p2p_wait_tokens(const P2PArgs& a, int32_t* err, cudaStream_t s) {

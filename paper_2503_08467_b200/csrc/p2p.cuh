@@ -33,4 +33,15 @@ cudaError_t launch_p2p_signal_partials(const P2PArgs& a, cudaStream_t s);
 cudaError_t launch_p2p_reduce(const P2PArgs& a, int n, int row_vecs, void* out, int32_t* err,
                               int num_sms, cudaStream_t s);
 
+// Expert-parallel baseline (MOESHARD_FLAG_EXPERT_PARALLEL): routed push of this rank's
+// admitted tokens (rec / hist: its router's output for n tokens over E experts) to the
+// hosts of their experts (E_loc per rank), capacity `cap` per expert (first-come);
+// owner[i] = host of token i or -1 (dropped). Publishes flags_ag like launch_p2p_push.
+cudaError_t launch_ep_dispatch(const P2PArgs& a, const void* x, int n, int row_vecs,
+                               const RouteRec* rec, const int32_t* hist, int E, int E_loc, int cap,
+                               int32_t* owner, cudaStream_t s);
+// EP gather: out[i] = the host's result row for token i (recv[owner[i]][i]), 0 if dropped.
+cudaError_t launch_ep_combine(const P2PArgs& a, int n, int row_vecs, const int32_t* owner, void* out,
+                              int32_t* err, int num_sms, cudaStream_t s);
+
 }  // namespace moeshard

@@ -52,15 +52,22 @@ class MoEShardLayer:
 
     def __init__(self, d_model: int, d_ff: int, n_experts: int, *, n_layers: int = 1,
                  max_tokens_per_rank: int, dtype=torch.bfloat16, rank: int = 0, world: int = 1,
-                 device: Optional[int] = None, flags: int = 0, group=None):
+                 device: Optional[int] = None, flags: int = 0, group=None,
+                 ep_capacity_factor: float = 0.0):
+        """flags & MOESHARD_FLAG_EXPERT_PARALLEL builds the paper's expert-parallel baseline
+        instead (needs MOESHARD_FLAG_P2P): this rank then hosts experts
+        [rank*E/world, (rank+1)*E/world) whole, and load_expert_shards takes
+        [E/world, h, d_ff] / [E/world, d_ff, h]; ep_capacity_factor <= 0 means min(E, 50)."""
         if dtype not in _DTYPES:
             raise ValueError(f"dtype must be bf16 or fp32, got {dtype}")
         self.device = torch.cuda.current_device() if device is None else device
         self.dtype, self.rank, self.world = dtype, rank, world
         self.h, self.d_ff, self.E = d_model, d_ff, n_experts
-        self.F = d_ff // world
+        self.ep = bool(flags & C.MOESHARD_FLAG_EXPERT_PARALLEL)
+        self.F = d_ff if self.ep else d_ff // world
+        self.E_host = n_experts // world if self.ep else n_experts   # experts computed here
         self.cfg = C.moeshard_config(d_model, d_ff, n_experts, n_layers, max_tokens_per_rank,
-                                     _DTYPES[dtype], flags)
+                                     _DTYPES[dtype], flags, ep_capacity_factor)
         ws = C.moeshard_workspace_size(self.cfg, world)
         self.workspace = torch.empty(ws, dtype=torch.uint8, device=f"cuda:{self.device}")
         self._wbytes = C.moeshard_weight_storage_size(self.cfg, world)
@@ -85,8 +92,9 @@ class MoEShardLayer:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     def load_expert_shards(self, layer: int, w_in_shard: torch.Tensor, w_out_shard: torch.Tensor):
-        """w_in_shard [E, h, d_ff/world], w_out_shard [E, d_ff/world, h] (this rank's slices)."""
-        exp_in, exp_out = (self.E, self.h, self.F), (self.E, self.F, self.h)
+        """w_in_shard [E, h, d_ff/world], w_out_shard [E, d_ff/world, h] (this rank's slices);
+        expert-parallel baseline: [E/world, h, d_ff] / [E/world, d_ff, h] (this rank's experts)."""
+        exp_in, exp_out = (self.E_host, self.h, self.F), (self.E_host, self.F, self.h)
         if tuple(w_in_shard.shape) != exp_in or tuple(w_out_shard.shape) != exp_out:
             raise C.MoEShardError(-2, f"shards {tuple(w_in_shard.shape)}/{tuple(w_out_shard.shape)}"
                                       f" vs expected {exp_in}/{exp_out}")
@@ -157,20 +165,33 @@ class MoEShardLayer:
     def routing(self, n_local: int) -> dict:
         """Routing tables of the last forward. With MOESHARD_FLAG_UNEVEN_TOKENS the token
         index space is world slots of max_tokens_per_rank (unused slot entries: expert -1)."""
-        if self._collective() and (self.cfg.flags & C.MOESHARD_FLAG_UNEVEN_TOKENS):
+        if self._collective() and (self.cfg.flags & (C.MOESHARD_FLAG_UNEVEN_TOKENS |
+                                                     C.MOESHARD_FLAG_EXPERT_PARALLEL)):
             n_local = self.cfg.max_tokens_per_rank
         N = n_local * (self.world if self._collective() else 1)
         dev = f"cuda:{self.device}"
         r = {
             "expert": torch.empty(N, dtype=torch.int32, device=dev),
             "gate": torch.empty(N, dtype=torch.float32, device=dev),
-            "counts": torch.empty(self.E, dtype=torch.int32, device=dev),
-            "offsets": torch.empty(self.E + 1, dtype=torch.int32, device=dev),
+            "counts": torch.empty(self.E_host, dtype=torch.int32, device=dev),
+            "offsets": torch.empty(self.E_host + 1, dtype=torch.int32, device=dev),
             "perm": torch.empty(N, dtype=torch.int32, device=dev),
         }
         C.moeshard_get_routing(self.ctx, r["expert"].data_ptr(), r["gate"].data_ptr(),
                                r["counts"].data_ptr(), r["offsets"].data_ptr(),
                                r["perm"].data_ptr(), self._stream())
+        return r
+
+    def ep_admission(self, n_local: int) -> dict:
+        """Expert-parallel baseline: this rank's admission of its last forward - owner (host
+        rank, -1 = dropped), expert, gate per local token, and the tokens its experts received."""
+        dev = f"cuda:{self.device}"
+        r = {"owner": torch.empty(n_local, dtype=torch.int32, device=dev),
+             "expert": torch.empty(n_local, dtype=torch.int32, device=dev),
+             "gate": torch.empty(n_local, dtype=torch.float32, device=dev),
+             "received": torch.empty(self.E_host, dtype=torch.int32, device=dev)}
+        C.moeshard_get_ep_admission(self.ctx, r["owner"].data_ptr(), r["expert"].data_ptr(),
+                                    r["gate"].data_ptr(), r["received"].data_ptr(), self._stream())
         return r
 
     def _collective(self) -> bool:

@@ -26,6 +26,7 @@ MOESHARD_FLAG_P2P = 0x200
 MOESHARD_FLAG_DYNAMIC_SCHED = 0x1000
 MOESHARD_FLAG_UNEVEN_TOKENS = 0x2000
 MOESHARD_FLAG_SERIAL_AG = 0x4000
+MOESHARD_FLAG_EXPERT_PARALLEL = 0x8000
 MOESHARD_STAGE_ROUTE = 0x1
 MOESHARD_STAGE_COMPUTE = 0x2
 MOESHARD_STAGE_REDUCE = 0x4
@@ -46,7 +47,7 @@ EXPORTS = [
     "moeshard_get_stats", "moeshard_check", "moeshard_last_error", "moeshard_status_string",
     "moeshard_destroy", "moeshard_version", "moeshard_profile", "moeshard_get_phase_ms",
     "moeshard_forward_stages", "moeshard_p2p_region", "moeshard_p2p_export", "moeshard_p2p_open",
-    "moeshard_p2p_connect",
+    "moeshard_p2p_connect", "moeshard_get_ep_admission",
 ]
 PHASES = ["router", "allgather", "grouping", "gemm_up", "gemm_down", "reduce_scatter"]
 
@@ -62,6 +63,7 @@ class moeshard_config(ctypes.Structure):
         ("d_model", ctypes.c_int32), ("d_ff", ctypes.c_int32), ("n_experts", ctypes.c_int32),
         ("n_layers", ctypes.c_int32), ("max_tokens_per_rank", ctypes.c_int32),
         ("dtype", ctypes.c_int32), ("flags", ctypes.c_uint32),
+        ("ep_capacity_factor", ctypes.c_float),
     ]
 
 
@@ -114,6 +116,7 @@ def load_library() -> ctypes.CDLL:
         "moeshard_p2p_export": ([vp, ctypes.c_char_p], i32),
         "moeshard_p2p_open": ([vp, ctypes.c_char_p, ctypes.POINTER(vp)], i32),
         "moeshard_p2p_connect": ([vp, ctypes.POINTER(vp)], i32),
+        "moeshard_get_ep_admission": ([vp, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -204,6 +207,11 @@ def moeshard_p2p_connect(ctx, regions):
 def moeshard_get_routing(ctx, expert_ptr, gate_ptr, counts_ptr, offsets_ptr, perm_ptr, stream):
     _check(_lib.moeshard_get_routing(ctx, expert_ptr, gate_ptr, counts_ptr, offsets_ptr, perm_ptr,
                                      stream), ctx)
+
+
+def moeshard_get_ep_admission(ctx, owner_ptr, expert_ptr, gate_ptr, received_ptr, stream):
+    _check(_lib.moeshard_get_ep_admission(ctx, owner_ptr, expert_ptr, gate_ptr, received_ptr,
+                                          stream), ctx)
 
 
 def moeshard_get_stats(ctx, stream) -> dict:

@@ -791,3 +791,67 @@ def test_staged_forward_protocol_errors():
     L.forward(0, x, w_r, stages=C.MOESHARD_STAGE_COMPUTE | C.MOESHARD_STAGE_REDUCE)
     L.check()
     L.close()
+
+
+# --------------------------------------------------------------------- expert-parallel baseline
+@pytest.mark.parametrize("G,E,routing,cf", [
+    (2, 16, "skew", 0.0),      # CF = min(E, 50) = E: nothing dropped
+    (4, 64, "zipf", 1.0),      # CF = 1: hot experts overflow, first-come drops
+    (4, 128, "patho", 0.0),    # E > 50: CF = 50 -> capacity 50 n / E; 3 experts
+    (2, 8, "uniform", 0.0),
+])
+def test_expert_parallel_baseline_matches_oracle(G, E, routing, cf):
+    """MOESHARD_FLAG_EXPERT_PARALLEL (the paper's comparison system, PAPER.md:153-161 with the
+    CF of PAPER.md:393-398): G ranks share this GPU in lock-step stages, rank o hosting experts
+    [o E/G, (o+1) E/G) whole; tokens go to their expert's host (routed push), are computed there
+    with the full d_ff, and come back. Against oracle.moe_layer_ep: admission (host rank or
+    dropped) exact per token, tokens received per host expert exact, every output row within
+    2e-2 and dropped rows exactly zero - over two forwards with different tokens."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200 import moeshard as C
+    n, h, d_ff = 700, 256, 384
+    N, El = G * n, E // G
+    flags = C.MOESHARD_FLAG_P2P | C.MOESHARD_FLAG_EXPERT_PARALLEL
+    layers = [MoEShardLayer(h, d_ff, E, max_tokens_per_rank=n + 60, dtype=torch.bfloat16, rank=r,
+                            world=G, flags=flags, ep_capacity_factor=cf) for r in range(G)]
+    MoEShardLayer.p2p_connect_local(layers)
+    base = W.make_layer_inputs(81, N, h, d_ff, E, dtype=torch.bfloat16, routing=routing, k=3,
+                               k_r=max(1, E // 10))
+    for r, L in enumerate(layers):
+        L.load_expert_shards(0, base.w_i[r * El:(r + 1) * El].cuda(), base.w_o[r * El:(r + 1) * El].cuda())
+    w_r = base.w_r.cuda()
+    for seed in (81, 82):
+        x = W.make_tokens(seed, N, h)
+        f = W.draw_experts(seed, N, E, routing, k=3, k_r=max(1, E // 10))
+        xs = [x[r * n:(r + 1) * n].cuda().contiguous() for r in range(G)]
+        fs = [f[r * n:(r + 1) * n].cuda().contiguous() for r in range(G)]
+        ys = [torch.empty_like(v) for v in xs]
+        for stage in (C.MOESHARD_STAGE_ROUTE, C.MOESHARD_STAGE_COMPUTE, C.MOESHARD_STAGE_REDUCE):
+            for r, L in enumerate(layers):
+                L.forward(0, xs[r], w_r, forced_expert=fs[r], out=ys[r], stages=stage)
+        for L in layers:
+            L.check()
+        torch.cuda.synchronize()
+        st = {}
+        y_ref = O.moe_layer_ep([x[r * n:(r + 1) * n] for r in range(G)], base.w_r, base.w_i, base.w_o,
+                               capacity_factor=None if cf <= 0 else cf,
+                               forced_per_gpu=[f[r * n:(r + 1) * n].numpy() for r in range(G)],
+                               stats=st)
+        recv_ref = np.zeros(E, dtype=np.int64)
+        for r in range(G):
+            a = {k: v.cpu().numpy() for k, v in layers[r].ep_admission(n).items()}
+            fr = f[r * n:(r + 1) * n].numpy().astype(np.int64)
+            np.testing.assert_array_equal(a["expert"], fr)
+            np.testing.assert_array_equal(a["owner"], np.where(st["keep"][r], fr // El, -1))
+            np.add.at(recv_ref, fr[st["keep"][r]], 1)
+            yr = ys[r].float().cpu().numpy()
+            assert (yr[~st["keep"][r]] == 0).all(), "dropped tokens must give a zero row"
+            err = O.max_abs_rel(yr, y_ref[r])
+            assert err <= BF16_TOL, f"rank {r} seed {seed}: max-abs-rel {err:.3e}"
+        for r in range(G):
+            got = layers[r].ep_admission(n)["received"].cpu().numpy()
+            np.testing.assert_array_equal(got, recv_ref[r * El:(r + 1) * El])
+        if cf == 1.0:
+            assert st["dropped"] > 0
+    for L in layers:
+        L.close()
