@@ -90,6 +90,12 @@ typedef enum {
  * order); a dropped token's output row is zero. CF = config.ep_capacity_factor, or min(E, 50)
  * when <= 0. Baseline for measurement; MoEShard itself never drops a token. */
 #define MOESHARD_FLAG_EXPERT_PARALLEL 0x8000u
+/* Sec. 3.3 ablation (the paper's "without MegaBlocks" mode): instead of one
+ * fused grouped launch, one up + one down tcgen05 launch per expert (2E launches; the paper's
+ * first optimisation alone) ... */
+#define MOESHARD_FLAG_LAUNCH_PER_EXPERT 0x10000u
+/* ... or per (source rank, expert) (2 E world launches; neither optimisation). bf16 only. */
+#define MOESHARD_FLAG_LAUNCH_PER_SOURCE 0x20000u
 
 /* moeshard_forward_stages masks: ROUTE = Step 1 + the token exchange (Step 3 push),
  * COMPUTE = Steps 2 and 4 (+ the Step 5 send in P2P mode), REDUCE = the Step 5 aggregate. */

@@ -75,6 +75,52 @@ __device__ __forceinline__ Unit decode(int u, int n_mt, int E, const int32_t* pr
   return w;
 }
 
+// Unit list of one launch: every (expert, tile, chunk) of the forward, or - launch-mode
+// ablation - only expert p.only_e (optionally restricted to source rank p.only_g's rows),
+// chunked on its own.
+struct UnitList {
+  int total;        // units in this launch
+  int e, lo, hi, nc, cs;   // restricted mode: expert, row range, chunks, chunk rows
+};
+__device__ __forceinline__ UnitList unit_list(const TcParams& p, int n_units_per_chunk,
+                                              const int32_t* pref, const int32_t* pos,
+                                              const int32_t* end) {
+  UnitList L{};
+  if (p.only_e < 0) {
+    L.total = pref[p.E] * n_units_per_chunk;
+    L.e = -1;
+    return L;
+  }
+  L.e = p.only_e;
+  L.lo = pos[L.e];
+  L.hi = end[L.e];
+  if (p.only_g >= 0) {
+    const int32_t* b = p.block_base;
+    const int g = p.only_g;
+    const int lo_rel = b[static_cast<size_t>(g) * p.nbr * p.E + L.e];
+    const int hi_rel = g + 1 < p.n_src ? b[static_cast<size_t>(g + 1) * p.nbr * p.E + L.e]
+                                       : end[L.e] - pos[L.e];
+    L.hi = L.lo + hi_rel;
+    L.lo += lo_rel;
+  }
+  tc_chunking(L.hi - L.lo, &L.nc, &L.cs);
+  L.total = L.nc * n_units_per_chunk;
+  return L;
+}
+__device__ __forceinline__ Unit unit_at(const UnitList& L, int u, int n_mt, int E,
+                                        const int32_t* pref, const int32_t* pos,
+                                        const int32_t* end, const int32_t* csz) {
+  if (L.e < 0) return decode(u, n_mt, E, pref, pos, end, csz);
+  Unit w;
+  w.e = L.e;
+  w.mt = u / L.nc;
+  const int c = u - w.mt * L.nc;
+  w.chunk = c;
+  w.tok0 = L.lo + c * L.cs;
+  w.ntok = min(L.cs, L.hi - w.tok0);
+  return w;
+}
+
 // Epilogue of one tile: TMEM accumulator (lane = output feature of this
 // warp's 32-feature slice, column = token) -> fused ReLU (up) or gate x (down)
 // -> bf16 -> a per-warp 1 KB shared staging buffer [16 tokens][32 features]
@@ -215,7 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int n_mt = p.n_mt;
-  const int total = s_pref[p.E] * n_mt;
+  const UnitList UL = unit_list(p, n_mt, s_pref, s_off, s_end);
+  const int total = UL.total;
   const int nkb = p.K / BK;
 
   if (warp == 0) {
@@ -224,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
-      const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
+      const Unit w = unit_at(UL, u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
       const __nv_bfloat16* tiles =
           p.a_tiles + (static_cast<size_t>(w.e) * n_mt + w.mt) * nkb * (BM * BK);
       for (int kb = 0; kb < nkb; ++kb) {
@@ -247,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
-      const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
+      const Unit w = unit_at(UL, u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
       const int nb = (w.ntok + B_BOX - 1) / B_BOX;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&emptyB[stage], phase ^ 1);
@@ -271,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int as = 0;
     uint32_t aphase = 0;
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
-      const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
+      const Unit w = unit_at(UL, u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
       const int nmma = (w.ntok + 15) & ~15;
       const uint32_t idesc = idesc_bf16_f32(BM, nmma);
       mbar_wait(&tempty[as], aphase ^ 1);
@@ -314,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int as = 0;
     uint32_t aphase = 0;
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
-      const Unit w = decode(u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
+      const Unit w = unit_at(UL, u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * BN_MAX;
@@ -326,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       as ^= 1;
       if (as == 0) aphase ^= 1;
     }
+    if (kDown && p.p2p_n > 0) __threadfence_system();   // remote rows before the signal kernel
   }
 
   tc_fence_before();
@@ -408,7 +456,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int n_mt = p.n_mt, n_mp = n_mt / 2;
-  const int total = s_pref[p.E] * n_mp;
+  const UnitList UL = unit_list(p, n_mp, s_pref, s_off, s_end);
+  const int total = UL.total;
   const int nkb = p.K / BK;
   const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
 
@@ -419,7 +468,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = cid; u < total; u += ncl) {
-      const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
+      const Unit w = unit_at(UL, u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
       const int mt = 2 * w.mt + static_cast<int>(rank);
       const int row0 = ((w.e * n_mt + mt) * nkb) * BM;
       for (int kb = 0; kb < nkb; ++kb) {
@@ -441,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = cid; u < total; u += ncl) {
-      const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
+      const Unit w = unit_at(UL, u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
       const int half = ((w.ntok + 31) & ~31) / 2;     // rows per CTA
       const int nb = half / B2_BOX;
       const int r0 = w.tok0 + static_cast<int>(rank) * half;
@@ -467,7 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int as = 0;
       uint32_t aphase = 0;
       for (int u = cid; u < total; u += ncl) {
-        const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
+        const Unit w = unit_at(UL, u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
         const int nmma = (w.ntok + 31) & ~31;
         const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
         mbar_wait(&tempty[as], aphase ^ 1);
@@ -506,7 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int as = 0;
     uint32_t aphase = 0;
     for (int u = cid; u < total; u += ncl) {
-      const Unit w = decode(u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
+      const Unit w = unit_at(UL, u, n_mp, p.E, s_pref, s_off, s_end, s_cs);
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const int mt = 2 * w.mt + static_cast<int>(rank);
@@ -519,6 +568,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       as ^= 1;
       if (as == 0) aphase ^= 1;
     }
+    if (kDown && p.p2p_n > 0) __threadfence_system();   // remote rows before the signal kernel
   }
 
   tc_fence_before();

@@ -28,6 +28,13 @@ struct TcParams {
   int ld_out;         // F (up) or h (down)
   const int32_t* perm;     // down: perm[j] = global token id of expert-ordered row j
   const RouteRec* route;   // down: gate per global token
+  // launch-mode ablation (Sec. 3.3, MOESHARD_FLAG_LAUNCH_PER_EXPERT / _PER_SOURCE): this
+  // launch covers only expert only_e (>= 0) and, if only_g >= 0, only the tokens of source
+  // rank only_g: rows [pos[e] + base[g*nbr][e], pos[e] + base[(g+1)*nbr][e]) of its segment
+  // (base = Step 2's per-block prefix [n_src*nbr][E], the last rank ends at counts[e])
+  int only_e = -1, only_g = -1;
+  const int32_t* block_base = nullptr;
+  int nbr = 0, n_src = 1;
   // down, peer-memory exchange (MOESHARD_FLAG_P2P): p2p_n > 0 sends the partial row of
   // global token t to its owner o = t / p2p_n, row t - o * p2p_n of p2p_out[o]
   int p2p_n = 0;

@@ -125,7 +125,8 @@ constexpr int kL2PersistMB = 64;   // measured best of 0/32/48/64/79 MB on c2 (D
 constexpr uint32_t kKnownFlags =
     MOESHARD_FLAG_FORCE_COLLECTIVES | MOESHARD_FLAG_SIMT_GEMM | MOESHARD_FLAG_UNFUSED_GEMM |
     MOESHARD_FLAG_NO_L2_PERSIST | MOESHARD_FLAG_DYNAMIC_SCHED | MOESHARD_FLAG_UNEVEN_TOKENS |
-    MOESHARD_FLAG_P2P | MOESHARD_FLAG_SERIAL_AG | MOESHARD_FLAG_EXPERT_PARALLEL;
+    MOESHARD_FLAG_P2P | MOESHARD_FLAG_SERIAL_AG | MOESHARD_FLAG_EXPERT_PARALLEL |
+    MOESHARD_FLAG_LAUNCH_PER_EXPERT | MOESHARD_FLAG_LAUNCH_PER_SOURCE;
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -290,6 +291,15 @@ int allgather_tokens(moeshard_ctx* c, const void* hidden, int n, int ns, bool un
 }
 
 }  // namespace
+
+// Step 5 send (peer memory): the down epilogue stores the partial row of global token t into
+// its owner's receive slot for this rank
+void set_p2p_out(const moeshard_ctx* c, TcParams& dn, int ns) {
+  dn.p2p_n = ns;
+  for (int g = 0; g < c->world; ++g)
+    dn.p2p_out[g] = reinterpret_cast<__nv_bfloat16*>(
+        c->pa.peers[g] + c->PL.off_recv + static_cast<size_t>(c->rank) * c->pa.n_max * c->h * 2);
+}
 
 int validate(const moeshard_config* c, int world) {
   if (!c) return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "config is NULL");
@@ -640,7 +650,8 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   const int NB = (c->coll ? c->world : 1) * nbr;
   int32_t* my_hist = c->ep ? c->ep_hist
                            : c->block_hist + (c->coll ? static_cast<size_t>(c->rank) * nbr * E : 0);
-  const bool fused = c->use_tc && !(c->cfg.flags & MOESHARD_FLAG_UNFUSED_GEMM) &&
+  const uint32_t kLaunchModes = MOESHARD_FLAG_LAUNCH_PER_EXPERT | MOESHARD_FLAG_LAUNCH_PER_SOURCE;
+  const bool fused = c->use_tc && !(c->cfg.flags & (MOESHARD_FLAG_UNFUSED_GEMM | kLaunchModes)) &&
                      F % kTcFeatTile == 0 && h % kTcFeatTile == 0;   // odd tile counts: see FFN kernel
   if (!st_route || n == 0) {
     // (routing ran in an earlier call, or this rank has no tokens this time)
@@ -707,18 +718,43 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
                   static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
       TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), Et, c->tb,
                   static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
-      if (c->p2p) {   // Step 5 send: partial rows go straight to their owner's receive slot
-        dn.p2p_n = ns;
-        for (int g = 0; g < c->world; ++g)
-          dn.p2p_out[g] = reinterpret_cast<__nv_bfloat16*>(
-              c->pa.peers[g] + c->PL.off_recv +
-              static_cast<size_t>(c->rank) * c->pa.n_max * h * 2);
-      }
+      if (c->p2p) set_p2p_out(c, dn, ns);
       CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, c->tm_xperm16, lw.tm_out, c->tm_H16, up, dn,
                                     c->tb.done, (c->cfg.flags & MOESHARD_FLAG_DYNAMIC_SCHED) != 0,
                                     /*early_tables=*/n > 0 && !c->ep, c->num_sms, s));
       c->mark(4, s);
       c->launches += 1;
+      if (c->p2p) {
+        CUDA_TRY(c, launch_p2p_signal_partials(c->pa, s));
+        c->launches += 1;
+      }
+    } else if (c->use_tc && (c->cfg.flags & kLaunchModes)) {
+      // Sec. 3.3 ablation: the launch fusion undone. One up + one down
+      // launch per expert (2 Et launches: the paper's per-expert mode after its first
+      // optimisation) or per (source rank, expert) (2 Et G launches: no optimisation). Each
+      // launch reads the device tables and exits at once when its token range is empty, so
+      // the host never synchronises (graph-capturable); the arithmetic is the grouped one.
+      const bool per_src = (c->cfg.flags & MOESHARD_FLAG_LAUNCH_PER_SOURCE) != 0;
+      const int n_src = c->coll ? c->world : 1;
+      TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), Et, c->tb,
+                  static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
+      TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), Et, c->tb,
+                  static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
+      for (TcParams* q : {&up, &dn}) {
+        q->block_base = c->block_base;
+        q->nbr = nbr;
+        q->n_src = n_src;
+      }
+      if (c->p2p) set_p2p_out(c, dn, ns);
+      for (int e = 0; e < Et; ++e)
+        for (int g = 0; g < (per_src ? n_src : 1); ++g) {
+          up.only_e = dn.only_e = e;
+          up.only_g = dn.only_g = per_src ? g : -1;
+          CUDA_TRY(c, launch_tc_gemm(false, lw.tm_in, c->tm_xperm, c->tm_xperm16, up, c->num_sms, s));
+          CUDA_TRY(c, launch_tc_gemm(true, lw.tm_out, c->tm_H, c->tm_H16, dn, c->num_sms, s));
+          c->launches += 2;
+        }
+      c->mark(4, s);
       if (c->p2p) {
         CUDA_TRY(c, launch_p2p_signal_partials(c->pa, s));
         c->launches += 1;

@@ -436,7 +436,7 @@ def test_c3_encoder_teacher_forced_moe_layers():
     enc.moe.close()
 
 
-@pytest.mark.parametrize("flag", ["DYNAMIC_SCHED", "FORCE_COLLECTIVES", "UNFUSED_GEMM", None])
+@pytest.mark.parametrize("flag", ["DYNAMIC_SCHED", "FORCE_COLLECTIVES", "UNFUSED_GEMM", "LAUNCH_PER_EXPERT", None])
 def test_forward_under_cuda_graph_replay(flag):
     """A captured forward replays correctly with new token values and new routing
     (no launch argument depends on the data: tables and counters live on the device)."""
@@ -855,3 +855,50 @@ def test_expert_parallel_baseline_matches_oracle(G, E, routing, cf):
             assert st["dropped"] > 0
     for L in layers:
         L.close()
+
+
+# --------------------------------------------------------------------- Sec. 3.3 launch-mode ablation
+@pytest.mark.parametrize("mode", ["LAUNCH_PER_EXPERT", "LAUNCH_PER_SOURCE"])
+@pytest.mark.parametrize("G,E,routing", [(1, 16, "zipf"), (2, 8, "uniform"), (4, 32, "skew")])
+def test_launch_mode_ablation_matches_fused(mode, G, E, routing):
+    """The paper's un-fused modes: one up + one down launch per expert
+    (2E launches) or per (source rank, expert) (2EG launches) instead of the single fused
+    grouped launch. G ranks share this GPU (peer-memory transport, lock-step stages; G = 1 is
+    a plain world-1 layer). Same routing tables, outputs within 2e-2 of the oracle and of the
+    fused path; the launch counter shows the launch structure."""
+    from paper_2503_08467_b200 import MoEShardLayer, shard_columns
+    from paper_2503_08467_b200 import moeshard as C
+    n, h, d_ff = 600, 256, 256 * G
+    N = G * n
+    inp = W.make_layer_inputs(91, N, h, d_ff, E, dtype=torch.bfloat16, routing=routing,
+                              k_r=max(1, E // 10))
+    outs, launches = [], []
+    for extra in (0, getattr(C, f"MOESHARD_FLAG_{mode}")):
+        flags = extra | (C.MOESHARD_FLAG_P2P if G > 1 else 0)
+        layers = [MoEShardLayer(h, d_ff, E, max_tokens_per_rank=n, dtype=torch.bfloat16, rank=r,
+                                world=G, flags=flags) for r in range(G)]
+        if G > 1:
+            MoEShardLayer.p2p_connect_local(layers)
+        for r, L in enumerate(layers):
+            c0, c1 = shard_columns(d_ff, G, r)
+            L.load_expert_shards(0, inp.w_i[:, :, c0:c1].cuda(), inp.w_o[:, c0:c1, :].cuda())
+        xs = [inp.x[r * n:(r + 1) * n].cuda().contiguous() for r in range(G)]
+        fs = [inp.forced[r * n:(r + 1) * n].cuda().contiguous() for r in range(G)]
+        ys = [torch.empty_like(x) for x in xs]
+        l0 = layers[0].stats()["kernel_launches"]
+        for stage in (C.MOESHARD_STAGE_ROUTE, C.MOESHARD_STAGE_COMPUTE, C.MOESHARD_STAGE_REDUCE):
+            for r, L in enumerate(layers):
+                L.forward(0, xs[r], inp.w_r.cuda(), forced_expert=fs[r], out=ys[r], stages=stage)
+        for L in layers:
+            L.check()
+        torch.cuda.synchronize()
+        launches.append(layers[0].stats()["kernel_launches"] - l0)
+        outs.append(torch.cat(ys).float().cpu().numpy())
+        for L in layers:
+            L.close()
+    per = 2 * E * (G if mode == "LAUNCH_PER_SOURCE" else 1)
+    assert launches[1] - launches[0] == per - 1, launches   # 2E(G) GEMM launches vs 1 fused
+    y_ref = O.moe_layer(inp.x, inp.w_r, inp.w_i, inp.w_o, forced=inp.forced.numpy())
+    for y in outs:
+        assert O.max_abs_rel(y, y_ref) <= BF16_TOL
+    print(f"{mode} G={G}: bitwise equal to fused: {np.array_equal(outs[0], outs[1])}")
