@@ -68,6 +68,15 @@ cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_
                               const TcParams& up, const TcParams& dn, int32_t* done, bool dynamic,
                               bool early_tables, int grid, cudaStream_t s);
 
+// Both products of one expert and <= 128 of its tokens per cluster of F/128 CTAs with H
+// kept on chip (expert_mlp.cu); applicable when expert_mlp_supported(h, F, E).
+//   tmX128: X_perm [N][h] box {64, 128}, 128-B swizzle; tmWi / tmWo: packed weight tiles
+//   dn: the down-projection parameters (output, perm_pad, route, P2P slots, tables, E)
+bool expert_mlp_supported(int h, int F, int E);
+cudaError_t launch_tc_expert_mlp(const CUtensorMap& tmX128, const CUtensorMap& tmWi,
+                                 const CUtensorMap& tmWo, const TcParams& dn, int h, int F,
+                                 int num_sms, cudaStream_t s);
+
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const CUtensorMap& tmB2, const TcParams& p, int grid, cudaStream_t s);
 

@@ -126,7 +126,7 @@ constexpr uint32_t kKnownFlags =
     MOESHARD_FLAG_FORCE_COLLECTIVES | MOESHARD_FLAG_SIMT_GEMM | MOESHARD_FLAG_UNFUSED_GEMM |
     MOESHARD_FLAG_NO_L2_PERSIST | MOESHARD_FLAG_DYNAMIC_SCHED | MOESHARD_FLAG_UNEVEN_TOKENS |
     MOESHARD_FLAG_P2P | MOESHARD_FLAG_SERIAL_AG | MOESHARD_FLAG_EXPERT_PARALLEL |
-    MOESHARD_FLAG_LAUNCH_PER_EXPERT | MOESHARD_FLAG_LAUNCH_PER_SOURCE;
+    MOESHARD_FLAG_LAUNCH_PER_EXPERT | MOESHARD_FLAG_LAUNCH_PER_SOURCE | MOESHARD_FLAG_SPLIT_FFN;
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -206,7 +206,7 @@ struct moeshard_ctx {
   int32_t *block_hist = nullptr, *block_base = nullptr, *block_tot = nullptr, *perm = nullptr;
   Tables tb{};
   void *x_all = nullptr, *x_perm = nullptr, *H = nullptr, *partial = nullptr;
-  CUtensorMap tm_xperm{}, tm_H{}, tm_xperm16{}, tm_H16{}, tm_wt_r{};
+  CUtensorMap tm_xperm{}, tm_H{}, tm_xperm16{}, tm_H16{}, tm_xperm128{}, tm_wt_r{};
   void* wt_r = nullptr;
   int EP = 16;
   std::vector<LayerW> layers;
@@ -490,6 +490,7 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
         !make_tmap(&c->tm_H, c->H, c->F, np, 32) ||
         !make_tmap(&c->tm_xperm16, c->x_perm, c->h, np, 16) ||
         !make_tmap(&c->tm_H16, c->H, c->F, np, 16) ||
+        !make_tmap(&c->tm_xperm128, c->x_perm, c->h, np, 128) ||
         !make_tmap(&c->tm_wt_r, c->wt_r, c->h, c->EP, c->EP)) {
       delete c;
       return fail(nullptr, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
@@ -713,7 +714,22 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     c->mark(3, s);
     // Step 4: expert computation, one grouped product per projection
     void* P = c->coll && !c->p2p ? c->partial : hidden_out;
-    if (fused) {
+    // narrow shards (F <= 512, e.g. G = 8): both products per expert chunk in one cluster,
+    // H on chip (expert_mlp.cu); MOESHARD_FLAG_SPLIT_FFN keeps the two-phase kernel
+    const bool mlp = fused && !(c->cfg.flags & MOESHARD_FLAG_SPLIT_FFN) &&
+                     expert_mlp_supported(h, F, Et);
+    if (mlp) {
+      TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), Et, c->tb,
+                  static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
+      if (c->p2p) set_p2p_out(c, dn, ns);
+      CUDA_TRY(c, launch_tc_expert_mlp(c->tm_xperm128, lw.tm_in, lw.tm_out, dn, h, F, c->num_sms, s));
+      c->mark(4, s);
+      c->launches += 1;
+      if (c->p2p) {
+        CUDA_TRY(c, launch_p2p_signal_partials(c->pa, s));
+        c->launches += 1;
+      }
+    } else if (fused) {
       TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), Et, c->tb,
                   static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
       TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), Et, c->tb,

@@ -902,3 +902,70 @@ def test_launch_mode_ablation_matches_fused(mode, G, E, routing):
     for y in outs:
         assert O.max_abs_rel(y, y_ref) <= BF16_TOL
     print(f"{mode} G={G}: bitwise equal to fused: {np.array_equal(outs[0], outs[1])}")
+
+
+# --------------------------------------------------------------------- on-chip-H expert MLP (narrow shards)
+@pytest.mark.parametrize("N,h,F,E,routing", [
+    (8192, 768, 384, 64, "uniform"),    # C2 at G = 8 per rank: cluster of 3, 2 output tiles per CTA
+    (8192, 768, 384, 64, "zipf"),       # hot experts: up to ~19 chunks of <= 128 rows
+    (6000, 1024, 512, 128, "uniform"),  # C5 shape at G = 8: cluster of 4
+    (1500, 256, 256, 16, "patho"),      # cluster of 2, one output tile per CTA, empty experts
+    (777, 512, 256, 8, "zipf"),         # cluster of 2, two output tiles, ragged chunks
+    (1, 768, 384, 4, "uniform"),        # a single token
+])
+def test_expert_mlp_on_chip_h_matches_oracle_and_split_path(N, h, F, E, routing):
+    """d_ff/G <= 512: both products of each (expert, <= 128-token chunk) run in one cluster of
+    F/128 CTAs with H kept in shared memory (expert_mlp.cu). Routing exact, every output row
+    within 2e-2 (global and per row) of the oracle, and equal to the two-phase fused kernel
+    (MOESHARD_FLAG_SPLIT_FFN) within bf16 rounding of identical fp32 accumulations."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200 import moeshard as C
+    inp = W.make_layer_inputs(95, N, h, F, E, dtype=torch.bfloat16, routing=routing, k=3, s=1.2)
+    f = inp.forced.cuda().contiguous()
+    ys = []
+    for flags in (0, C.MOESHARD_FLAG_SPLIT_FFN):
+        L = MoEShardLayer(h, F, E, max_tokens_per_rank=N, dtype=torch.bfloat16, flags=flags)
+        L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
+        for _ in range(2):
+            y = L.forward(0, inp.x.cuda(), inp.w_r.cuda(), forced_expert=f)
+        r = {k: v.cpu().numpy() for k, v in L.routing(N).items()}
+        L.check()
+        torch.cuda.synchronize()
+        ys.append(y.clone())
+        L.close()
+    _check_layer(inp, ys[0], r, tol=BF16_TOL)
+    y_ref = O.moe_layer(inp.x, inp.w_r, inp.w_i, inp.w_o, forced=inp.forced.numpy())
+    assert per_row_rel(ys[0].float().cpu().numpy(), y_ref) <= BF16_TOL
+    same = torch.equal(ys[0], ys[1])
+    d = (ys[0].float() - ys[1].float()).abs().max().item()
+    print(f"expert MLP N={N} h={h} F={F} E={E} {routing}: bitwise equal to split {same}, max diff {d:.3e}")
+    assert O.max_abs_rel(ys[0].float().cpu().numpy(), ys[1].float().cpu().numpy()) <= 1e-2
+
+
+def test_expert_mlp_under_graph_replay_and_natural_routing():
+    """The on-chip-H kernel captured in a CUDA graph and replayed with new tokens, natural router."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    N, h, F, E = 4096, 768, 384, 64
+    a = W.make_layer_inputs(96, N, h, F, E, dtype=torch.bfloat16, routing="natural")
+    L = MoEShardLayer(h, F, E, max_tokens_per_rank=N, dtype=torch.bfloat16)
+    L.load_expert_shards(0, a.w_i.cuda(), a.w_o.cuda())
+    x, w_r = a.x.cuda().clone(), a.w_r.cuda()
+    out = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        L.forward(0, x, w_r, out=out)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        L.forward(0, x, w_r, out=out)
+    for seed in (97, 98):
+        xn = W.make_tokens(seed, N, h)
+        x.copy_(xn.cuda())
+        g.replay()
+        torch.cuda.synchronize()
+        r = {k: v.cpu().numpy() for k, v in L.routing(N).items()}
+        inp = W.LayerInputs(xn, a.w_r, a.w_i, a.w_o, None)
+        _check_layer(inp, out, r, tol=BF16_TOL)
+    L.close()
