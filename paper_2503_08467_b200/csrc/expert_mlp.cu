@@ -19,6 +19,8 @@
 // each down unit wait for every up unit of its chunk). Units carry no cross-cluster
 // dependency, so the kernel is correct whether or not all clusters are resident.
 //
+// Issue order per cluster: up(0), up(1), dn(0), up(2), dn(1), ... (the next unit's up product
+// runs on the tensor core while this unit's H is drained and exchanged; two up accumulators).
 // Roles (256 threads): warp 0 TMA producer (one ring of 32 KB stages: X tile + W_i tile
 // for an up k-step, the CTA's 1-2 W_o tiles for a down k-step), warp 1 MMA issuer, warp 2
 // TMEM allocator, warps 4-7 epilogue (TMEM lane quadrant = warp % 4).
@@ -42,7 +44,7 @@ constexpr int kMlpTok = 128;            // tokens per unit (M of both products)
 constexpr int kTile = 128 * 64 * 2;     // one 128-row x 64-wide bf16 tile = 16 KB
 constexpr int kStage = 2 * kTile;       // ring stage: 32 KB
 constexpr int kThreadsMlp = 256;
-constexpr int kColUp = 0, kColDn = 128; // TMEM columns of the two accumulators
+constexpr int kColUp = 0, kColDn = 256; // TMEM columns: up accumulator x 2 buffers, down
 constexpr int kSmemBudget = 225 * 1024; // H + ring (barriers and alignment on top)
 constexpr size_t kMaxSmem = 232448;     // opt-in dynamic shared memory per CTA (sm_100)
 
@@ -99,9 +101,9 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
   uint8_t* sR = smem + h_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sR + S * kStage);
   uint64_t* empty = full + S;
-  uint64_t* upfull = empty + S;
-  uint64_t* uptempty = upfull + 1;
-  uint64_t* dnfull = uptempty + 1;
+  uint64_t* upfull = empty + S;        // [2]
+  uint64_t* uptempty = upfull + 2;     // [2]
+  uint64_t* dnfull = uptempty + 2;
   uint64_t* dntempty = dnfull + 1;
   uint64_t* hfull = dntempty + 1;
   uint64_t* hempty = hfull + 1;
@@ -123,8 +125,10 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(upfull, 1);
-    mbar_init(uptempty, 4);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&upfull[b], 1);
+      mbar_init(&uptempty[b], 4);
+    }
     mbar_init(dnfull, 1);
     mbar_init(dntempty, 4);
     mbar_init(hfull, 1);
@@ -153,6 +157,11 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
   const uint32_t tmem = *tmem_slot;
   const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
 
+  // This cluster's units in the software-pipelined issue order up(0), up(1), dn(0), up(2),
+  // dn(1), ...: step i issues up(i) (i < nu) then dn(i-1) (i >= 1), so the tensor core
+  // computes the next unit's up product while the epilogue drains this unit's H and the
+  // slices travel between the CTAs (the up accumulator is double-buffered in TMEM).
+  const int nu = cid < total ? (total - cid + ncl - 1) / ncl : 0;
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     const uint64_t pol_x = policy_evict_last();    // the chunk's rows: read by all CS CTAs
@@ -160,33 +169,39 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
     const int n_mt_up = F / 128, n_mt_dn = h / 128;
     int s = 0;
     uint32_t ph = 0;
-    for (int u = cid; u < total; u += ncl) {
-      int e, tok0, ntok;
-      mlp_unit(u, E, s_pref, s_pos, s_cnt, e, tok0, ntok);
-      for (int kb = 0; kb < nkb_up; ++kb) {
-        mbar_wait(&empty[s], ph ^ 1);
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&full[s], kStage);
-          uint8_t* st = sR + s * kStage;
-          tma_load_2d(&tmX, &full[s], st, kb * 64, tok0, pol_x);
-          tma_load_2d(&tmWi, &full[s], st + kTile, 0,
-                      ((e * n_mt_up + static_cast<int>(j)) * nkb_up + kb) * 128, pol_w);
+    for (int i = 0; i <= nu; ++i) {
+      if (i < nu) {
+        int e, tok0, ntok;
+        mlp_unit(cid + i * ncl, E, s_pref, s_pos, s_cnt, e, tok0, ntok);
+        for (int kb = 0; kb < nkb_up; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&full[s], kStage);
+            uint8_t* st = sR + s * kStage;
+            tma_load_2d(&tmX, &full[s], st, kb * 64, tok0, pol_x);
+            tma_load_2d(&tmWi, &full[s], st + kTile, 0,
+                        ((e * n_mt_up + static_cast<int>(j)) * nkb_up + kb) * 128, pol_w);
+          }
+          __syncwarp();
+          if (++s == S) { s = 0; ph ^= 1; }
         }
-        __syncwarp();
-        if (++s == S) { s = 0; ph ^= 1; }
       }
-      for (int kb = 0; kb < nkb_dn; ++kb) {
-        mbar_wait(&empty[s], ph ^ 1);
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&full[s], NCT * kTile);
-          uint8_t* st = sR + s * kStage;
+      if (i >= 1) {
+        int e, tok0, ntok;
+        mlp_unit(cid + (i - 1) * ncl, E, s_pref, s_pos, s_cnt, e, tok0, ntok);
+        for (int kb = 0; kb < nkb_dn; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&full[s], NCT * kTile);
+            uint8_t* st = sR + s * kStage;
 #pragma unroll
-          for (int q = 0; q < NCT; ++q)
-            tma_load_2d(&tmWo, &full[s], st + q * kTile, 0,
-                        ((e * n_mt_dn + static_cast<int>(j) * NCT + q) * nkb_dn + kb) * 128, pol_w);
+            for (int q = 0; q < NCT; ++q)
+              tma_load_2d(&tmWo, &full[s], st + q * kTile, 0,
+                          ((e * n_mt_dn + static_cast<int>(j) * NCT + q) * nkb_dn + kb) * 128, pol_w);
+          }
+          __syncwarp();
+          if (++s == S) { s = 0; ph ^= 1; }
         }
-        __syncwarp();
-        if (++s == S) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -195,49 +210,53 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
     const uint32_t id_dn = idesc_bf16_f32(128, NCT * 128);
     int s = 0;
     uint32_t ph = 0;
-    int k = 0;
-    for (int u = cid; u < total; u += ncl, ++k) {
-      const uint32_t par = k & 1;
-      mbar_wait(uptempty, par ^ 1);   // the previous unit's up accumulator was drained
-      tc_fence_after();
-      for (int kb = 0; kb < nkb_up; ++kb) {
-        mbar_wait(&full[s], ph);
+    for (int i = 0; i <= nu; ++i) {
+      if (i < nu) {
+        const int b = i & 1;                       // up accumulator buffer
+        mbar_wait(&uptempty[b], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint64_t ad = smem_desc_k_sw128(smem_u32(sR + s * kStage));
-          const uint64_t bd = smem_desc_k_sw128(smem_u32(sR + s * kStage + kTile));
+        for (int kb = 0; kb < nkb_up; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ad = smem_desc_k_sw128(smem_u32(sR + s * kStage));
+            const uint64_t bd = smem_desc_k_sw128(smem_u32(sR + s * kStage + kTile));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_bf16_ss(tmem + kColUp, ad + 2 * kk, bd + 2 * kk, id_up, (kb | kk) != 0);
-          mma_commit(&empty[s]);
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ss(tmem + kColUp + b * 128, ad + 2 * kk, bd + 2 * kk, id_up, (kb | kk) != 0);
+            mma_commit(&empty[s]);
+          }
+          __syncwarp();
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        if (elect_one()) mma_commit(&upfull[b]);
+        __syncwarp();
+      }
+      if (i >= 1) {
+        const uint32_t par = (i - 1) & 1;
+        mbar_wait(dntempty, par ^ 1);   // the previous unit's down accumulator was drained
+        mbar_wait(hfull, par);          // every slice of this unit's H is in this CTA's smem
+        tc_fence_after();
+        for (int kb = 0; kb < nkb_dn; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ad = smem_desc_k_sw128(smem_u32(sH + kb * kTile));
+            const uint64_t bd = smem_desc_k_sw128(smem_u32(sR + s * kStage));
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ss(tmem + kColDn, ad + 2 * kk, bd + 2 * kk, id_dn, (kb | kk) != 0);
+            mma_commit(&empty[s]);
+          }
+          __syncwarp();
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        if (elect_one()) {
+          mma_commit(dnfull);
+          mma_commit_mc(hempty, static_cast<uint16_t>((1u << CS) - 1));   // H free, cluster-wide
         }
         __syncwarp();
-        if (++s == S) { s = 0; ph ^= 1; }
       }
-      if (elect_one()) mma_commit(upfull);
-      __syncwarp();
-      mbar_wait(dntempty, par ^ 1);   // the previous unit's down accumulator was drained
-      mbar_wait(hfull, par);          // every slice of this unit's H is in this CTA's smem
-      tc_fence_after();
-      for (int kb = 0; kb < nkb_dn; ++kb) {
-        mbar_wait(&full[s], ph);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint64_t ad = smem_desc_k_sw128(smem_u32(sH + kb * kTile));
-          const uint64_t bd = smem_desc_k_sw128(smem_u32(sR + s * kStage));
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_bf16_ss(tmem + kColDn, ad + 2 * kk, bd + 2 * kk, id_dn, (kb | kk) != 0);
-          mma_commit(&empty[s]);
-        }
-        __syncwarp();
-        if (++s == S) { s = 0; ph ^= 1; }
-      }
-      if (elect_one()) {
-        mma_commit(dnfull);
-        mma_commit_mc(hempty, static_cast<uint16_t>((1u << CS) - 1));   // H free, cluster-wide
-      }
-      __syncwarp();
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- epilogue
@@ -251,13 +270,14 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
       int e, tok0, ntok;
       mlp_unit(u, E, s_pref, s_pos, s_cnt, e, tok0, ntok);
       // (a) up accumulator -> relu -> bf16 -> this CTA's H slice (k-blocks 2j, 2j+1)
-      mbar_wait(upfull, par);
+      const int b = k & 1;
+      mbar_wait(&upfull[b], (k >> 1) & 1);
       mbar_wait(hempty, par ^ 1);    // every CTA's down MMAs of the previous unit are done
       tc_fence_after();
 #pragma unroll
       for (int c0 = 0; c0 < 128; c0 += 32) {
         uint32_t r[32];
-        tmem_ld32(tmem + lane_off + kColUp + c0, r);
+        tmem_ld32(tmem + lane_off + kColUp + b * 128 + c0, r);
         tmem_ld_wait();
         uint8_t* tile = sH + (2 * j + c0 / 64) * kTile + t * 128;
 #pragma unroll
@@ -275,7 +295,7 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(uptempty);
+      if (lane == 0) mbar_arrive(&uptempty[b]);
       fence_proxy_async_shared();      // the generic H writes, before the async proxy reads them
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (wq == 0 && lane == 0) {
@@ -340,7 +360,7 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
 size_t mlp_smem_bytes(int E, int F) {
   const int h_bytes = (F / 64) * kTile;
   const int S = std::min(6, (kSmemBudget - h_bytes) / kStage);
-  return 1024 + h_bytes + S * kStage + (2 * S + 6) * 8 + 16 + (3 * E + 1 + 33) * 4;
+  return 1024 + h_bytes + S * kStage + (2 * S + 8) * 8 + 16 + (3 * E + 1 + 33) * 4;
 }
 
 template <int CS, int NCT>
@@ -355,7 +375,6 @@ cudaError_t launch_mlp(const CUtensorMap& tmX, const CUtensorMap& tmWi, const CU
     attr.done();
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((num_sms / CS) * CS);
   cfg.blockDim = dim3(kThreadsMlp);
   cfg.dynamicSmemBytes = mlp_smem_bytes(a.dn.E, a.F);
   cfg.stream = s;
@@ -367,6 +386,20 @@ cudaError_t launch_mlp(const CUtensorMap& tmX, const CUtensorMap& tmWi, const CU
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
+  cfg.numAttrs = 1;
+  // Persistent grid = the clusters that can be resident at once. A cluster must fit in one
+  // GPC, so e.g. only 45 three-CTA clusters fit on 148 SMs (not 49); launching more would
+  // run the rest as a second wave after the first finished.
+  static int max_cl[9] = {0};   // per cluster size, first device queried (all B200s alike)
+  if (max_cl[CS] == 0) {
+    cfg.gridDim = dim3((num_sms / CS) * CS);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, tc_expert_mlp<CS, NCT>, &cfg) != cudaSuccess || n <= 0)
+      n = num_sms / CS;
+    cudaGetLastError();
+    max_cl[CS] = std::min(n, num_sms / CS);
+  }
+  cfg.gridDim = dim3(max_cl[CS] * CS);
   cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, tc_expert_mlp<CS, NCT>, tmX, tmWi, tmWo, a);
 }
