@@ -7,9 +7,9 @@
 //
 //   CTA j (cluster rank j), chunk rows t < 128 (token on the TMEM lane axis, M = 128):
 //     up    D_up[t, f]  = sum_k X[t, k] Wi^T[128 j + f, k]        f < 128, K = h
-//           -> relu -> bf16 -> H[t, 128 j + f] in its own shared memory (K-major, 128-B
-//           swizzle, the MMA A-operand image), then bulk-copied (cp.async.bulk shared::cta ->
-//           shared::cluster, complete_tx on the peer's barrier) into every peer's H
+//           -> relu -> bf16 -> H[t, 128 j + f] stored straight into the shared memory of
+//           every CTA of the cluster (st.shared::cluster, the MMA A-operand image: K-major,
+//           128-B swizzle), then a release arrive on every CTA's hfull barrier
 //     down  D_dn[t, c]  = sum_f H[t, f] Wo^T[C_j + c, f]            c < h / CS, K = F
 //           -> gate[t] x -> bf16 -> row perm[t] (or its owner's receive slot, P2P) of the
 //           output, columns C_j = [j h/CS, (j+1) h/CS)
@@ -21,11 +21,15 @@
 //
 // Issue order per cluster: up(0), up(1), dn(0), up(2), dn(1), ... (the next unit's up product
 // runs on the tensor core while this unit's H is drained and exchanged; two up accumulators).
-// Roles (256 threads): warp 0 TMA producer (one ring of 32 KB stages: X tile + W_i tile
+// Roles (384 threads): warp 0 TMA producer (one ring of 32 KB stages: X tile + W_i tile
 // for an up k-step, the CTA's 1-2 W_o tiles for a down k-step), warp 1 MMA issuer, warp 2
-// TMEM allocator, warps 4-7 epilogue (TMEM lane quadrant = warp % 4).
+// TMEM allocator, warps 4-7 the H drain (TMEM -> relu -> every CTA's H), warps 8-11 the
+// output drain (TMEM -> gate x -> global), so a unit's output drain overlaps the next
+// unit's H drain and exchange (TMEM lane quadrant = warp % 4 for both groups). The H
+// exchange uses plain DSMEM stores rather than bulk copies: bulk copies queue behind the
+// producer's in-flight TMA loads in the SM's async-copy unit (measured 5-8 us per unit).
 // Barriers per CTA: full/empty per ring stage; upfull/uptempty and dnfull/dntempty between
-// MMA and epilogue; hfull (1 local arrival + the peers' bulk-copy bytes) before the down
+// MMA and drains; hfull (4 H-drain warps x CS CTAs arrive, release.cluster) before the down
 // MMAs read H; hempty (CS arrivals: every CTA's down-MMA commit, multicast) before the
 // next unit's H slices may be written into any CTA of the cluster.
 #include "common.cuh"
@@ -43,17 +47,20 @@ using namespace ptx;
 constexpr int kMlpTok = 128;            // tokens per unit (M of both products)
 constexpr int kTile = 128 * 64 * 2;     // one 128-row x 64-wide bf16 tile = 16 KB
 constexpr int kStage = 2 * kTile;       // ring stage: 32 KB
-constexpr int kThreadsMlp = 256;
+constexpr int kThreadsMlp = 384;
 constexpr int kColUp = 0, kColDn = 256; // TMEM columns: up accumulator x 2 buffers, down
 constexpr int kSmemBudget = 225 * 1024; // H + ring (barriers and alignment on top)
 constexpr size_t kMaxSmem = 232448;     // opt-in dynamic shared memory per CTA (sm_100)
 
-__device__ __forceinline__ void bulk_s2s_cluster(uint32_t dst_cluster, uint32_t src_cta,
-                                                 uint32_t bytes, uint32_t bar_cluster) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(dst_cluster), "r"(src_cta), "r"(bytes), "r"(bar_cluster)
-      : "memory");
+// make this thread's generic shared-memory writes (local and remote) visible to the async
+// proxy (the tensor core's operand reads) of the CTAs they were written to
+__device__ __forceinline__ void fence_proxy_async_all() {
+  asm volatile("fence.proxy.async;" ::: "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
 }
 // arrive once on the barrier at the same offset in every CTA of `mask` when this thread's
 // previously issued MMAs complete
@@ -131,7 +138,7 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
     }
     mbar_init(dnfull, 1);
     mbar_init(dntempty, 4);
-    mbar_init(hfull, 1);
+    mbar_init(hfull, 4 * CS);
     mbar_init(hempty, CS);
     fence_mbar_init();
   }
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
       if (i >= 1) {
         const uint32_t par = (i - 1) & 1;
         mbar_wait(dntempty, par ^ 1);   // the previous unit's down accumulator was drained
-        mbar_wait(hfull, par);          // every slice of this unit's H is in this CTA's smem
+        mbar_wait_acquire_cluster(hfull, par);   // every slice of this unit's H is in this CTA
         tc_fence_after();
         for (int kb = 0; kb < nkb_dn; ++kb) {
           mbar_wait(&full[s], ph);
@@ -258,58 +265,61 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
         __syncwarp();
       }
     }
-  } else if (warp >= 4) {
-    // ---------------------------------------------------------------- epilogue
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------------------------------------------------------- H drain + exchange
     const int wq = warp & 3;
     const int t = wq * 32 + lane;                         // chunk row = TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
-    const int cj = h / CS;                                // output columns of this CTA
-    int k = 0;
-    for (int u = cid; u < total; u += ncl, ++k) {
-      const uint32_t par = k & 1;
-      int e, tok0, ntok;
-      mlp_unit(u, E, s_pref, s_pos, s_cnt, e, tok0, ntok);
-      // (a) up accumulator -> relu -> bf16 -> this CTA's H slice (k-blocks 2j, 2j+1)
+    uint32_t hbar[CS], hrow[CS];                          // every CTA's hfull / H row base
+#pragma unroll
+    for (int q = 0; q < CS; ++q) {
+      hbar[q] = mapa_shared(smem_u32(hfull), q);
+      hrow[q] = mapa_shared(smem_u32(sH + t * 128), q);
+    }
+    for (int k = 0; k < nu; ++k) {
       const int b = k & 1;
       mbar_wait(&upfull[b], (k >> 1) & 1);
-      mbar_wait(hempty, par ^ 1);    // every CTA's down MMAs of the previous unit are done
+      mbar_wait(hempty, (k & 1) ^ 1);   // every CTA's down MMAs of the previous unit are done
       tc_fence_after();
 #pragma unroll
       for (int c0 = 0; c0 < 128; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + lane_off + kColUp + b * 128 + c0, r);
         tmem_ld_wait();
-        uint8_t* tile = sH + (2 * j + c0 / 64) * kTile + t * 128;
+        const uint32_t tile = (2 * j + c0 / 64) * kTile;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {   // 8 features = one 16-B chunk
+        for (int q8 = 0; q8 < 4; ++q8) {   // 8 features = one 16-B chunk
           uint32_t w[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const __nv_bfloat162 v = __floats2bfloat162_rn(fmaxf(__uint_as_float(r[8 * q + 2 * i]), 0.f),
-                                                           fmaxf(__uint_as_float(r[8 * q + 2 * i + 1]), 0.f));
+            const __nv_bfloat162 v = __floats2bfloat162_rn(fmaxf(__uint_as_float(r[8 * q8 + 2 * i]), 0.f),
+                                                           fmaxf(__uint_as_float(r[8 * q8 + 2 * i + 1]), 0.f));
             w[i] = *reinterpret_cast<const uint32_t*>(&v);
           }
-          const int chunk = ((c0 % 64) / 8 + q) ^ (t & 7);
-          *reinterpret_cast<uint4*>(tile + chunk * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+          const uint32_t off = tile + ((((c0 % 64) / 8 + q8) ^ (t & 7)) << 4);
+#pragma unroll
+          for (int q = 0; q < CS; ++q) st_cluster_v4(hrow[q] + off, make_uint4(w[0], w[1], w[2], w[3]));
         }
       }
       tc_fence_before();
+      fence_proxy_async_all();   // the H writes, before any CTA's tensor core reads them
       __syncwarp();
-      if (lane == 0) mbar_arrive(&uptempty[b]);
-      fence_proxy_async_shared();      // the generic H writes, before the async proxy reads them
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (wq == 0 && lane == 0) {
-        // local slice in place: arrive with the bytes the peers will deliver, then send ours
-        mbar_arrive_expect_tx(hfull, (CS - 1) * 2 * kTile);
-        const uint32_t src = smem_u32(sH + 2 * j * kTile);
+      if (lane == 0) {
+        mbar_arrive(&uptempty[b]);
 #pragma unroll
-        for (int q = 1; q < CS; ++q) {
-          const uint32_t peer = (j + q) % CS;
-          bulk_s2s_cluster(mapa_shared(src, peer), src, 2 * kTile, mapa_shared(smem_u32(hfull), peer));
-        }
+        for (int q = 0; q < CS; ++q) mbar_arrive_release_cluster(hbar[q]);
       }
-      // (b) down accumulator -> gate x -> bf16 -> output row of the token, columns C_j
-      mbar_wait(dnfull, par);
+    }
+  } else if (warp >= 8) {
+    // ---------------------------------------------------------------- output drain
+    const int wq = warp & 3;
+    const int t = wq * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+    const int cj = h / CS;                                // output columns of this CTA
+    for (int k = 0; k < nu; ++k) {
+      int e, tok0, ntok;
+      mlp_unit(cid + k * ncl, E, s_pref, s_pos, s_cnt, e, tok0, ntok);
+      mbar_wait(dnfull, k & 1);
       tc_fence_after();
       const bool valid = t < ntok;
       int row = 0;
