@@ -7,9 +7,9 @@
 //
 //   CTA j (cluster rank j), chunk rows t < 128 (token on the TMEM lane axis, M = 128):
 //     up    D_up[t, f]  = sum_k X[t, k] Wi^T[128 j + f, k]        f < 128, K = h
-//           -> relu -> bf16 -> H[t, 128 j + f] stored straight into the shared memory of
-//           every CTA of the cluster (st.shared::cluster, the MMA A-operand image: K-major,
-//           128-B swizzle), then a release arrive on every CTA's hfull barrier
+//           -> relu -> bf16 -> H[t, 128 j + f] stored into this CTA's shared memory and, with
+//           asynchronous DSMEM stores (st.async, byte completion on the peer's hfull), into
+//           every peer's (the MMA A-operand image: K-major, 128-B swizzle)
 //     down  D_dn[t, c]  = sum_f H[t, f] Wo^T[C_j + c, f]            c < h / CS, K = F
 //           -> gate[t] x -> bf16 -> row perm[t] (or its owner's receive slot, P2P) of the
 //           output, columns C_j = [j h/CS, (j+1) h/CS)
@@ -26,11 +26,11 @@
 // TMEM allocator, warps 4-7 the H drain (TMEM -> relu -> every CTA's H), warps 8-11 the
 // output drain (TMEM -> gate x -> global), so a unit's output drain overlaps the next
 // unit's H drain and exchange (TMEM lane quadrant = warp % 4 for both groups). The H
-// exchange uses plain DSMEM stores rather than bulk copies: bulk copies queue behind the
-// producer's in-flight TMA loads in the SM's async-copy unit (measured 5-8 us per unit).
+// exchange uses st.async rather than smem->smem bulk copies (those queue behind the
+// producer's in-flight TMA loads: 5-8 us per unit) or blocking st.shared::cluster (8 us).
 // Barriers per CTA: full/empty per ring stage; upfull/uptempty and dnfull/dntempty between
-// MMA and drains; hfull (4 H-drain warps x CS CTAs arrive, release.cluster) before the down
-// MMAs read H; hempty (CS arrivals: every CTA's down-MMA commit, multicast) before the
+// MMA and drains; hfull (the 4 local H-drain warps arrive, one with the (CS-1) x 32 KB the
+// peers deliver) before the down MMAs read H; hempty (CS arrivals: every CTA's down-MMA commit, multicast) before the
 // next unit's H slices may be written into any CTA of the cluster.
 #include "common.cuh"
 #include "gemm_tc.cuh"
@@ -57,10 +57,13 @@ constexpr size_t kMaxSmem = 232448;     // opt-in dynamic shared memory per CTA 
 __device__ __forceinline__ void fence_proxy_async_all() {
   asm volatile("fence.proxy.async;" ::: "memory");
 }
-__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint4 v) {
-  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
-               "r"(v.z), "r"(v.w)
-               : "memory");
+// asynchronous 16-B store into a peer CTA's shared memory; completion is counted (bytes) on
+// the peer's mbarrier at bar_cluster, the storing thread does not wait for it
+__device__ __forceinline__ void st_async_v4(uint32_t addr, uint4 v, uint32_t bar_cluster) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+      ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar_cluster)
+      : "memory");
 }
 // arrive once on the barrier at the same offset in every CTA of `mask` when this thread's
 // previously issued MMAs complete
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
     }
     mbar_init(dnfull, 1);
     mbar_init(dntempty, 4);
-    mbar_init(hfull, 4 * CS);
+    mbar_init(hfull, 4);
     mbar_init(hempty, CS);
     fence_mbar_init();
   }
@@ -242,7 +245,8 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
       if (i >= 1) {
         const uint32_t par = (i - 1) & 1;
         mbar_wait(dntempty, par ^ 1);   // the previous unit's down accumulator was drained
-        mbar_wait_acquire_cluster(hfull, par);   // every slice of this unit's H is in this CTA
+        mbar_wait(hfull, par);            // every slice of this unit's H is in this CTA
+        fence_proxy_async_shared();       // H was written by the generic proxy (st / st.async)
         tc_fence_after();
         for (int kb = 0; kb < nkb_dn; ++kb) {
           mbar_wait(&full[s], ph);
@@ -276,11 +280,15 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
       hbar[q] = mapa_shared(smem_u32(hfull), q);
       hrow[q] = mapa_shared(smem_u32(sH + t * 128), q);
     }
+    uint8_t* my_row = sH + t * 128;
     for (int k = 0; k < nu; ++k) {
       const int b = k & 1;
       mbar_wait(&upfull[b], (k >> 1) & 1);
       mbar_wait(hempty, (k & 1) ^ 1);   // every CTA's down MMAs of the previous unit are done
       tc_fence_after();
+      if (wq == 0 && lane == 0)         // the bytes the peers' st.async will deliver here
+        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(hfull)),
+                     "r"((CS - 1) * 2 * kTile) : "memory");
 #pragma unroll
       for (int c0 = 0; c0 < 128; c0 += 32) {
         uint32_t r[32];
@@ -297,17 +305,20 @@ __global__ void __launch_bounds__(kThreadsMlp, 1)
             w[i] = *reinterpret_cast<const uint32_t*>(&v);
           }
           const uint32_t off = tile + ((((c0 % 64) / 8 + q8) ^ (t & 7)) << 4);
+          const uint4 v4 = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(my_row + off) = v4;
 #pragma unroll
-          for (int q = 0; q < CS; ++q) st_cluster_v4(hrow[q] + off, make_uint4(w[0], w[1], w[2], w[3]));
+          for (int q = 1; q < CS; ++q) {
+            const uint32_t peer = (j + q) % CS;
+            st_async_v4(hrow[peer] + off, v4, hbar[peer]);
+          }
         }
       }
       tc_fence_before();
-      fence_proxy_async_all();   // the H writes, before any CTA's tensor core reads them
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&uptempty[b]);
-#pragma unroll
-        for (int q = 0; q < CS; ++q) mbar_arrive_release_cluster(hbar[q]);
+        mbar_arrive(hfull);
       }
     }
   } else if (warp >= 8) {

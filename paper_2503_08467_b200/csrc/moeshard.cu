@@ -126,7 +126,7 @@ constexpr uint32_t kKnownFlags =
     MOESHARD_FLAG_FORCE_COLLECTIVES | MOESHARD_FLAG_SIMT_GEMM | MOESHARD_FLAG_UNFUSED_GEMM |
     MOESHARD_FLAG_NO_L2_PERSIST | MOESHARD_FLAG_DYNAMIC_SCHED | MOESHARD_FLAG_UNEVEN_TOKENS |
     MOESHARD_FLAG_P2P | MOESHARD_FLAG_SERIAL_AG | MOESHARD_FLAG_EXPERT_PARALLEL |
-    MOESHARD_FLAG_LAUNCH_PER_EXPERT | MOESHARD_FLAG_LAUNCH_PER_SOURCE | MOESHARD_FLAG_SPLIT_FFN;
+    MOESHARD_FLAG_LAUNCH_PER_EXPERT | MOESHARD_FLAG_LAUNCH_PER_SOURCE | MOESHARD_FLAG_ONCHIP_H;
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -714,9 +714,9 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     c->mark(3, s);
     // Step 4: expert computation, one grouped product per projection
     void* P = c->coll && !c->p2p ? c->partial : hidden_out;
-    // narrow shards (F <= 512, e.g. G = 8): both products per expert chunk in one cluster,
-    // H on chip (expert_mlp.cu); MOESHARD_FLAG_SPLIT_FFN keeps the two-phase kernel
-    const bool mlp = fused && !(c->cfg.flags & MOESHARD_FLAG_SPLIT_FFN) &&
+    // opt-in for narrow shards (F <= 512, e.g. G = 8): both products per expert chunk in one
+    // cluster, H on chip (expert_mlp.cu)
+    const bool mlp = fused && (c->cfg.flags & MOESHARD_FLAG_ONCHIP_H) &&
                      expert_mlp_supported(h, F, Et);
     if (mlp) {
       TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), Et, c->tb,

@@ -29,7 +29,7 @@ MOESHARD_FLAG_SERIAL_AG = 0x4000
 MOESHARD_FLAG_EXPERT_PARALLEL = 0x8000
 MOESHARD_FLAG_LAUNCH_PER_EXPERT = 0x10000
 MOESHARD_FLAG_LAUNCH_PER_SOURCE = 0x20000
-MOESHARD_FLAG_SPLIT_FFN = 0x40000
+MOESHARD_FLAG_ONCHIP_H = 0x40000
 MOESHARD_STAGE_ROUTE = 0x1
 MOESHARD_STAGE_COMPUTE = 0x2
 MOESHARD_STAGE_REDUCE = 0x4

@@ -914,16 +914,16 @@ def test_launch_mode_ablation_matches_fused(mode, G, E, routing):
     (1, 768, 384, 4, "uniform"),        # a single token
 ])
 def test_expert_mlp_on_chip_h_matches_oracle_and_split_path(N, h, F, E, routing):
-    """d_ff/G <= 512: both products of each (expert, <= 128-token chunk) run in one cluster of
-    F/128 CTAs with H kept in shared memory (expert_mlp.cu). Routing exact, every output row
-    within 2e-2 (global and per row) of the oracle, and equal to the two-phase fused kernel
-    (MOESHARD_FLAG_SPLIT_FFN) within bf16 rounding of identical fp32 accumulations."""
+    """MOESHARD_FLAG_ONCHIP_H, d_ff/G <= 512: both products of each (expert, <= 128-token chunk)
+    run in one cluster of F/128 CTAs with H kept in shared memory (expert_mlp.cu). Routing
+    exact, every output row within 2e-2 (global and per row) of the oracle, and equal to the
+    default two-phase fused kernel within bf16 rounding of identical fp32 accumulations."""
     from paper_2503_08467_b200 import MoEShardLayer
     from paper_2503_08467_b200 import moeshard as C
     inp = W.make_layer_inputs(95, N, h, F, E, dtype=torch.bfloat16, routing=routing, k=3, s=1.2)
     f = inp.forced.cuda().contiguous()
     ys = []
-    for flags in (0, C.MOESHARD_FLAG_SPLIT_FFN):
+    for flags in (C.MOESHARD_FLAG_ONCHIP_H, 0):
         L = MoEShardLayer(h, F, E, max_tokens_per_rank=N, dtype=torch.bfloat16, flags=flags)
         L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
         for _ in range(2):
@@ -945,9 +945,11 @@ def test_expert_mlp_on_chip_h_matches_oracle_and_split_path(N, h, F, E, routing)
 def test_expert_mlp_under_graph_replay_and_natural_routing():
     """The on-chip-H kernel captured in a CUDA graph and replayed with new tokens, natural router."""
     from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200 import moeshard as C
     N, h, F, E = 4096, 768, 384, 64
     a = W.make_layer_inputs(96, N, h, F, E, dtype=torch.bfloat16, routing="natural")
-    L = MoEShardLayer(h, F, E, max_tokens_per_rank=N, dtype=torch.bfloat16)
+    L = MoEShardLayer(h, F, E, max_tokens_per_rank=N, dtype=torch.bfloat16,
+                      flags=C.MOESHARD_FLAG_ONCHIP_H)
     L.load_expert_shards(0, a.w_i.cuda(), a.w_o.cuda())
     x, w_r = a.x.cuda().clone(), a.w_r.cuda()
     out = torch.empty_like(x)
