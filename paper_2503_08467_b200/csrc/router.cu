@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 4) {
     // TMA producer (warp-uniform loop, one elected lane issues)
-    const uint64_t pol_x = policy_evict_first();
+    // x stays in L2 for the grouping launch, which re-reads every row (A/B: -0.35 us / step)
+    const uint64_t pol_x = policy_evict_normal();
     const uint64_t pol_w = policy_evict_last();
     int s = 0;
     uint32_t ph = 0;

@@ -19,21 +19,39 @@ CASES = {   # name: (E, h, d_ff, N, G, seed, routings)
     "c2_g8": (64, 768, 3072, 8192, 8, 2, ["uniform", ("zipf", {"s": 1.2})]),
     "c2_g4": (64, 768, 3072, 8192, 4, 2, ["uniform", ("zipf", {"s": 1.2})]),
     "c2_g2": (64, 768, 3072, 8192, 2, 2, ["uniform", ("zipf", {"s": 1.2})]),
+    "c3_g8": (128, 768, 3072, 16384, 8, 3, ["uniform", ("zipf", {"s": 1.2}), "skew"]),
+    "c5_g8": (128, 1024, 4096, 32768, 8, 5, ["uniform", ("zipf", {"s": 1.2})]),
 }
 
 
-def time_fwd(L, x, w_r, forced, out, nw, iters=60, warm=6):
-    # rotate over nw weight sets (>= 3x L2 in total) so every forward streams its weights from HBM
-    for k in range(warm):
-        L.forward(k % nw, x, w_r, forced_expert=forced, out=out)
+def graph_of(L, x, w_r, forced, out, nw):
+    """One CUDA graph holding nw forwards over the rotating weight sets (>= 3x L2 in total),
+    so every forward streams its weights from HBM and launches cost nothing."""
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        for k in range(nw + 2):
+            L.forward(k % nw, x, w_r, forced_expert=forced, out=out)
+    torch.cuda.current_stream().wait_stream(st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for k in range(nw):
+            L.forward(k % nw, x, w_r, forced_expert=forced, out=out)
+    return g
+
+
+def time_graph(g, nw, reps):
+    for _ in range(2):
+        g.replay()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for k in range(iters):
-        L.forward(k % nw, x, w_r, forced_expert=forced, out=out)
+    for _ in range(reps):
+        g.replay()
     e.record()
     torch.cuda.synchronize()
-    return s.elapsed_time(e) / iters * 1e3   # us
+    return s.elapsed_time(e) / (reps * nw) * 1e3   # us per forward
 
 
 def main():
@@ -58,17 +76,25 @@ def main():
         case = {"E": E, "h": h, "d_ff": d_ff, "N": N, "G": G, "d_ff_per_rank": F, "weight_sets": nw,
                 "note": "each virtual rank = the world-1 layer of all N tokens on its d_ff/G shard "
                         "(what a rank computes after the AllGather); collectives not included; "
-                        "eager launches, weights rotated over weight_sets copies",
+                        "CUDA-graph replay of weight_sets forwards, median of 5 interleaved rounds per rank",
                 "routings": {}}
         for r in routings:
             rname, kw = (r, {}) if isinstance(r, str) else r
             forced = W.draw_experts(seed, N, E, rname, device="cuda", **kw)
             label = rname + "".join(f"_{k}{v}" for k, v in kw.items())
-            t, tiles = [], []
+            graphs = [graph_of(L, x, w_r, forced, out, nw) for L in layers]
+            reps = max(2, 60 // nw)
+            samples = [[] for _ in layers]
+            for _ in range(5):          # ranks interleaved, 5 rounds: clock / power drift cancels
+                for gi, g in enumerate(graphs):
+                    samples[gi].append(time_graph(g, nw, reps))
+            t = [sorted(v)[len(v) // 2] for v in samples]
+            tiles = []
             for L in layers:
-                t.append(time_fwd(L, x, w_r, forced, out, nw))
+                L.forward(0, x, w_r, forced_expert=forced, out=out)
                 st = L.stats()
                 tiles.append((st["tiles_up"], st["tiles_down"]))
+            del graphs
             case["routings"][label] = {
                 "rank_us": [round(v, 2) for v in t], "max_over_min": round(max(t) / min(t), 4),
                 "tiles_equal_on_all_ranks": len(set(tiles)) == 1, "tiles": list(tiles[0]),
