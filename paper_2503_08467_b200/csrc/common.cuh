@@ -13,7 +13,10 @@ namespace moeshard {
 
 constexpr int kMaxExperts = 256;      // router instantiations cover E <= 256
 constexpr int kMaxWorld = 8;          // ranks of one NVLink/NVSwitch box (peer-memory exchange)
-constexpr int kTcTokTile = 256;       // max tokens per tcgen05 tile (UMMA N <= 256)
+#ifndef MOESHARD_TOK_TILE
+#define MOESHARD_TOK_TILE 256
+#endif
+constexpr int kTcTokTile = MOESHARD_TOK_TILE;  // max tokens per tcgen05 tile (UMMA N <= 256)
 constexpr int kTcFeatTile = 128;      // weight rows per tcgen05 tile (UMMA M)
 constexpr int kSimtTokTile = 64;      // tokens per SIMT tile
 constexpr int kSimtFeatTile = 64;     // output features per SIMT tile

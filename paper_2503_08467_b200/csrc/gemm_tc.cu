@@ -45,6 +45,7 @@ constexpr int A_BYTES = BM * BK * 2;       // 16 KB
 constexpr int B_BYTES = BN_MAX * BK * 2;   // 32 KB
 constexpr int B_BOX_BYTES = B_BOX * BK * 2;  // 4 KB
 constexpr int TMEM_COLS = 512;             // 2 accumulators x 256 fp32 columns
+constexpr int ACC_STRIDE = 256;            // TMEM columns between the two accumulators
 constexpr int kThreads = 256;
 
 struct Unit {
@@ -126,10 +127,12 @@ __device__ __forceinline__ Unit unit_at(const UnitList& L, int u, int n_mt, int 
 // -> bf16 -> a per-warp 1 KB shared staging buffer [16 tokens][32 features]
 // -> 16-B vector stores (up: row tok0+j of H; down: un-permute scatter to row
 // perm[tok0+j] of the output). One 16-token chunk at a time.
-template <bool kDown>
+// NH warps share one 32-feature quadrant: warp half eh (< NH) takes the 16-token column
+// chunks eh, eh + NH, ... (NH = 2 halves the drain latency of a tile).
+template <bool kDown, int NH = 1>
 __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok, int nmma,
                                            int fbase, uint32_t taddr, int lane, uint64_t pol_keep,
-                                           __nv_bfloat16* stage) {
+                                           __nv_bfloat16* stage, int eh = 0) {
   uint16_t* st16 = reinterpret_cast<uint16_t*>(stage);
   // down: the destination rows perm[j] and gates of the unit's tokens are fetched
   // up front (lane holds tokens lane + 32 i), so the loop below has no dependent
@@ -149,23 +152,37 @@ __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok
       g_r[i] = tk < ntok ? __ldg(&p.route[rows_r[i]].gate) : 0.f;
     }
   }
-  // TMEM reads are double-buffered: the load of columns c0+16.. is in flight while
-  // columns c0.. are converted and stored
+  // TMEM reads are double-buffered: the load of the next chunk is in flight while
+  // this one is converted and stored
   uint32_t rbuf[2][16];
-  tmem_ld16(taddr, rbuf[0]);
-  tmem_ld_wait(rbuf[0]);
+  const int first = 16 * eh;
+#ifdef MOESHARD_EXP_NO_TMEMLD
 #pragma unroll
-  for (int c0 = 0; c0 < BN_MAX; c0 += 16) {
+  for (int j = 0; j < 16; ++j) rbuf[0][j] = rbuf[1][j] = __float_as_uint(static_cast<float>(lane + j));
+#else
+  if (first < nmma) {
+    tmem_ld16(taddr + first, rbuf[0]);
+    tmem_ld_wait(rbuf[0]);
+  }
+#endif
+#pragma unroll
+  for (int it = 0; it < BN_MAX / (16 * NH); ++it) {
+    const int c0 = first + 16 * NH * it;
     if (c0 >= nmma) break;
-    uint32_t (&r)[16] = rbuf[(c0 / 16) & 1];
-    uint32_t (&rn)[16] = rbuf[((c0 / 16) + 1) & 1];
-    if (c0 + 16 < nmma) tmem_ld16(taddr + c0 + 16, rn);
+    uint32_t (&r)[16] = rbuf[it & 1];
+    uint32_t (&rn)[16] = rbuf[(it + 1) & 1];
+    const int cn = c0 + 16 * NH;
+#ifndef MOESHARD_EXP_NO_TMEMLD
+    if (cn < nmma) tmem_ld16(taddr + cn, rn);
+#endif
     int row = 0;
     if (kDown) {
       // token c0 + (lane & 15) lives in lane (c0 & 16) + (lane & 15), register c0 / 32
+      // (= 16 NH it / 32 for any eh: a compile-time index)
+      const int ri = (16 * NH * it) >> 5;
       const int src = (c0 & 16) + (lane & 15);
-      row = __shfl_sync(0xffffffffu, rows_r[c0 / 32], src);
-      const float g = __shfl_sync(0xffffffffu, g_r[c0 / 32], src);
+      row = __shfl_sync(0xffffffffu, rows_r[ri], src);
+      const float g = __shfl_sync(0xffffffffu, g_r[ri], src);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float gj = __shfl_sync(0xffffffffu, g, j);
@@ -195,14 +212,22 @@ __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok
           } else {
             dst = p.out + (size_t)rj * p.ld_out;
           }
+#ifdef MOESHARD_EXP_NO_STG
+          if (v.x == 0x12345678u && v.y == 0x9abcdefu)
+#endif
           *reinterpret_cast<uint4*>(dst + fbase + part * 8) = v;
         }
       } else if (c0 + j < ntok) {
+#ifdef MOESHARD_EXP_NO_STG
+        if (v.x == 0x12345678u && v.y == 0x9abcdefu)
+#endif
         st_v4_hint(p.out + (size_t)(tok0 + c0 + j) * p.ld_out + fbase + part * 8, v, pol_keep);
       }
     }
     __syncwarp();
-    if (c0 + 16 < nmma) tmem_ld_wait(rn);
+#ifndef MOESHARD_EXP_NO_TMEMLD
+    if (cn < nmma) tmem_ld_wait(rn);
+#endif
   }
 }
 
@@ -323,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = idesc_bf16_f32(BM, nmma);
       mbar_wait(&tempty[as], aphase ^ 1);
       tc_fence_after();
-      const uint32_t d = tmem_base + as * BN_MAX;
+      const uint32_t d = tmem_base + as * ACC_STRIDE;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&fullB[sb], pb);
         mbar_wait(&fullA[sa], pa);
@@ -364,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Unit w = unit_at(UL, u, n_mt, p.E, s_pref, s_off, s_end, s_cs);
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * BN_MAX;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * ACC_STRIDE;
       store_tile<kDown>(p, w.tok0, w.ntok, (w.ntok + 15) & ~15, w.mt * BM + wq * 32, taddr, lane,
                         pol_keep, stage);
       tc_fence_before();
@@ -521,7 +546,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + as * BN_MAX;
+        const uint32_t d = tmem_base + as * ACC_STRIDE;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&fullB[sb], pb);
           mbar_wait(&fullA[sa], pa);
@@ -559,7 +584,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const int mt = 2 * w.mt + static_cast<int>(rank);
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * BN_MAX;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * ACC_STRIDE;
       store_tile<kDown>(p, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
                         pol_keep, stage);
       tc_fence_before();
@@ -597,12 +622,29 @@ struct FusedParams {
   bool early_tables;   // tables via a release flag from the grouping launch's CTA 0 (see kernel)
 };
 
+#ifndef MOESHARD_EPI_WARPS
+#define MOESHARD_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = MOESHARD_EPI_WARPS;   // epilogue warps per CTA (multiple of 4)
+constexpr int kFusedThreads = 128 + 32 * kEpiWarps;
+static_assert(kEpiWarps % 4 == 0 && kEpiWarps <= 16, "1-4 epilogue warps per TMEM lane quadrant");
 constexpr int kUQ = 2;             // unit-queue slots (dynamic scheduling): small, so a
                                    // cluster never sits on units other clusters could run
-constexpr int kUQConsumers = 13;   // warps that read a slot: leader 0,1,3,4-7; follower 0,3,4-7
+#ifndef MOESHARD_REL_WARP
+#define MOESHARD_REL_WARP 0
+#endif
+#if MOESHARD_REL_WARP
+// warps that read a slot: leader 0,1,2,3 + epilogue; follower 0,2,3 + epilogue (the
+// follower's warp 1 runs the scheduler)
+constexpr int kUQConsumers = 7 + 2 * kEpiWarps;
+constexpr uint32_t kSchedRank = 1;
+#else
+constexpr int kUQConsumers = 5 + 2 * kEpiWarps;   // warps that read a slot: leader 0,1,3 + epilogue; follower 0,3 + epilogue
+constexpr uint32_t kSchedRank = 0;
+#endif
 
 template <int AS, int BS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     tc_moe_ffn_2sm(const __grid_constant__ CUtensorMap tmA_up, const __grid_constant__ CUtensorMap tmB_up,
                    const __grid_constant__ CUtensorMap tmA_dn, const __grid_constant__ CUtensorMap tmB_dn,
                    FusedParams fp) {
@@ -626,10 +668,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // per-warp epilogue staging (4 x 1 KB), then the unit queue (slots + barriers)
   __nv_bfloat16* s_stage = reinterpret_cast<__nv_bfloat16*>(
       (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15));
-  int* s_uq = reinterpret_cast<int*>(s_stage + 4 * 512);
+  int* s_uq = reinterpret_cast<int*>(s_stage + kEpiWarps * 512);
   uint64_t* uq_full = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(s_uq + kUQ) + 7) & ~static_cast<uintptr_t>(7));
   uint64_t* uq_empty = uq_full + kUQ;
+  uint64_t* hrel = uq_empty + kUQ;   // [2] epilogue warps -> release warp: H tile stored
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -653,12 +696,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
+      mbar_init(&tempty[a], 2 * kEpiWarps);
     }
     for (int q = 0; q < kUQ; ++q) {
       mbar_init(&uq_full[q], 1);
       mbar_init(&uq_empty[q], kUQConsumers);
     }
+    for (int a = 0; a < 2; ++a) mbar_init(&hrel[a], kEpiWarps);
     fence_mbar_init();
   }
   cluster_sync_all();
@@ -682,7 +726,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else {
     griddep_wait();
   }
-  for (int i = threadIdx.x; i <= E; i += kThreads) {
+  for (int i = threadIdx.x; i <= E; i += kFusedThreads) {
     s_pref[i] = fp.up.tb.tc_chunk_pref[i];
     s_off[i] = fp.up.tb.pos[i];
     if (i < E) {
@@ -705,7 +749,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int total = total_up + chunks * n_mp_dn;
   const int nkb_up = fp.up.K / BK, nkb_dn = fp.dn.K / BK;   // k-blocks per unit
   const int cid = static_cast<int>(cluster_id_x());
-  const uint32_t leader_uq_empty = mapa_shared(smem_u32(uq_empty), 0);
+  const uint32_t sched_uq_empty = mapa_shared(smem_u32(uq_empty), kSchedRank);
   // k-th unit of this cluster: static round robin, or the k-th queue slot (dynamic)
   auto fetch = [&](int k) -> int {
     if (!fp.dynamic) return cid + k * ncl;
@@ -714,8 +758,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int u = *reinterpret_cast<volatile int*>(&s_uq[slot]);
     __syncwarp();
     if (lane == 0) {
-      if (leader) mbar_arrive(&uq_empty[slot]);
-      else mbar_arrive_cluster(leader_uq_empty + slot * 8);
+      if (rank == kSchedRank) mbar_arrive(&uq_empty[slot]);
+      else mbar_arrive_cluster(sched_uq_empty + slot * 8);
     }
     return u;
   };
@@ -726,11 +770,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 : decode(u, n_mp_up, E, s_pref, s_off, s_end, s_cs);
   };
 
-  if (warp == 2) {
-    if (fp.dynamic && leader) {
-      // ------------------------------------------------------------ unit scheduler (leader)
-      const uint32_t peer_uq = mapa_shared(smem_u32(s_uq), 1);
-      const uint32_t peer_full = mapa_shared(smem_u32(uq_full), 1);
+  // unit scheduler (dynamic mode), on the CTA kSchedRank: the leader's idle warp 2, or
+  // (MOESHARD_REL_WARP, where warp 2 releases H tiles) the follower's idle warp 1
+  const bool sched_warp = fp.dynamic && rank == kSchedRank && warp == (MOESHARD_REL_WARP ? 1 : 2);
+  if (sched_warp) {
+    {
+      // ------------------------------------------------------------ unit scheduler
+      const uint32_t peer_uq = mapa_shared(smem_u32(s_uq), kSchedRank ^ 1);
+      const uint32_t peer_full = mapa_shared(smem_u32(uq_full), kSchedRank ^ 1);
       for (int k = 0;; ++k) {
         const int slot = k % kUQ;
         mbar_wait(&uq_empty[slot], static_cast<uint32_t>(((k / kUQ) & 1) ^ 1));
@@ -746,6 +793,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (u >= total) break;
       }
     }
+  } else if (warp == 2) {
+#if MOESHARD_REL_WARP
+    // -------------------------------------------------------------- H release (both CTAs)
+    // the epilogue warps arrive on hrel[as] after their H stores of an up unit (mbarrier
+    // arrive: release at CTA scope); this warp acquires it and publishes the tile with one
+    // red.release.gpu (cumulative: covers the stores it observed), so no epilogue warp
+    // waits on a CTA barrier or a GPU-scope fence
+    int as = 0;
+    uint32_t hph[2] = {0u, 0u};
+    for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
+      const bool down = u >= total_up;
+      if (!down) {
+        const Unit w = decode(u, n_mp_up, E, s_pref, s_off, s_end, s_cs);
+        mbar_wait(&hrel[as], hph[as]);
+        hph[as] ^= 1u;
+        if (lane == 0) red_release_gpu_add(fp.done + w.chunk, 1);
+        __syncwarp();
+      }
+      as ^= 1;
+    }
+#endif
   } else if (warp == 0) {
     // -------------------------------------------------------------- weight producer (both CTAs)
     // weight tiles are streamed once (evict_first) - except an expert's tiles when it has
@@ -814,11 +882,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mbar_wait(&emptyB[stage], phase ^ 1);
         const uint32_t fb = leader_full + stage * 8;
         if (elect_one()) {
+#ifdef MOESHARD_EXP_NO_BLOAD
+          if (leader) mbar_arrive(&fullB[stage]);
+          else mbar_arrive_cluster(fb);
+#else
           if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * stage_bytes);
           else mbar_arrive_cluster(fb);
           for (int i = 0; i < nb; ++i)
             tma_load_2d_2sm(tm, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
                             r0 + i * B2_BOX, pol_x);
+#endif
         }
         __syncwarp();
         if (++stage == BS) { stage = 0; phase ^= 1; }
@@ -839,7 +912,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + as * BN_MAX;
+        const uint32_t d = tmem_base + as * ACC_STRIDE;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&fullB[sb], pb);
           mbar_wait(&fullA[sa], pa);
@@ -847,9 +920,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (elect_one()) {
             const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
             const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B2_BYTES));
+#ifndef MOESHARD_EXP_NO_MMA
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
               mma_bf16_ss_2sm(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+#endif
             mma_commit_2sm(&emptyA[sa], 0x3);
             mma_commit_2sm(&emptyB[sb], 0x3);
           }
@@ -865,8 +940,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
-    const int wq = warp & 3;
-    __nv_bfloat16* stage = s_stage + wq * 512;
+    const int wq = warp & 3, eh = (warp - 4) >> 2;
+    __nv_bfloat16* stage = s_stage + (warp - 4) * 512;   // 1 KB per epilogue warp
     const uint64_t pol_keep = policy_evict_last();
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
     if (fp.early_tables) griddep_wait();   // perm / route of the grouping launch
@@ -878,24 +953,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const int mt = 2 * w.mt + static_cast<int>(rank);
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * BN_MAX;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * ACC_STRIDE;
+#ifdef MOESHARD_EXP_NO_EPI
+      if (false) {
+#else
       if (mt < (down ? fp.dn.n_mt : fp.up.n_mt)) {   // else: duplicate of the leader's tile
+#endif
         if (down)
-          store_tile<true>(fp.dn, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
-                           pol_keep, stage);
+          store_tile<true, kEpiWarps / 4>(fp.dn, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32,
+                                          taddr, lane, pol_keep, stage, eh);
         else
-          store_tile<false>(fp.up, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
-                            pol_keep, stage);
+          store_tile<false, kEpiWarps / 4>(fp.up, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32,
+                                           taddr, lane, pol_keep, stage, eh);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + as * 8);
       if (!down) {   // publish this CTA's H tile of the chunk
+#if MOESHARD_REL_WARP
+        if (lane == 0) mbar_arrive(&hrel[as]);   // the release warp publishes it
+#else
         // bar.sync orders every epilogue thread's H stores before thread 0's release
         // (cumulative at gpu scope), so the other warps need no fence of their own and
         // go straight on to the next tile
-        asm volatile("bar.sync 2, 128;" ::: "memory");   // the 4 epilogue warps
-        if (wq == 0 && lane == 0) red_release_gpu_add(fp.done + w.chunk, 1);
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");   // the epilogue warps
+        if (warp == 4 && lane == 0) red_release_gpu_add(fp.done + w.chunk, 1);
+#endif
       }
       as ^= 1;
       if (as == 0) aphase ^= 1;
@@ -916,7 +999,7 @@ size_t smem_bytes(int E, int as, int bs) {
 
 size_t smem_bytes_2sm(int E, int as, int bs) {
   return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (4 * E + 2) * 4 +
-         16 + 4 * 1024 + 96;   // + epilogue staging + unit queue
+         16 + kEpiWarps * 1024 + 96;   // + epilogue staging (1 KB per epilogue warp) + unit queue
 }
 
 template <bool kDown, int AS, int BS>
@@ -964,7 +1047,11 @@ cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
                               const TcParams& up, const TcParams& dn, int32_t* done, bool dynamic,
                               bool early_tables, int grid, cudaStream_t s) {
-  constexpr int AS = 6, BS = 6;
+#ifndef MOESHARD_FFN_AS
+#define MOESHARD_FFN_AS 6
+#define MOESHARD_FFN_BS 6
+#endif
+  constexpr int AS = MOESHARD_FFN_AS, BS = MOESHARD_FFN_BS;
   static PerDeviceOnce attr;
   if (attr.need()) {
     cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS>,
@@ -974,7 +1061,7 @@ cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_
     attr.done();
   }
   FusedParams fp{up, dn, done, dynamic, early_tables};
-  return launch_pdl(tc_moe_ffn_2sm<AS, BS>, dim3(grid & ~1), dim3(kThreads),
+  return launch_pdl(tc_moe_ffn_2sm<AS, BS>, dim3(grid & ~1), dim3(kFusedThreads),
                     smem_bytes_2sm(up.E, AS, BS), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
 }
 
