@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "gemm_tc.cuh"
 #include "ptx.cuh"
+#include "timeline.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -677,6 +678,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
+  if (threadIdx.x == 0) TL_MIN(0);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA_up);
     tma_prefetch_desc(&tmA_dn);
@@ -741,6 +743,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch_dependents();
+  if (threadIdx.x == 0) { TL_MIN(1); TL_MAX(1); }   // tables read, roles start
 
   // pair-units cover m-tiles (2q, 2q+1); with an odd count the last pair has
   // both CTAs on the same m-tile (the follower's copy is computed, not stored)
@@ -851,6 +854,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     // H rows (read by the down units) are kept in L2 (evict_last, persisting set-aside)
     const uint64_t pol_x = policy_evict_last();
     if (fp.early_tables) griddep_wait();   // X_perm rows and the route records are complete
+    if (lane == 0) { TL_MIN(2); TL_MAX(2); }
     const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -938,6 +942,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
         if (as == 0) aphase ^= 1;
       }
     }
+    if (leader && lane == 0) TL_MAX(3);   // last MMA issued
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
     const int wq = warp & 3, eh = (warp - 4) >> 2;
@@ -990,6 +995,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   cluster_sync_all();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+  if (threadIdx.x == 0) TL_MAX(0);
 }
 
 size_t smem_bytes(int E, int as, int bs) {
@@ -1042,6 +1048,8 @@ cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUten
 }
 
 }  // namespace
+
+TL_EXPORT(moeshard_tl_ffn)
 
 cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,

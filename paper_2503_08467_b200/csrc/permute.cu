@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "group.cuh"
 #include "ptx.cuh"
+#include "timeline.cuh"
 
 namespace moeshard {
 namespace {
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(128) group_block_scan(const int32_t* __restric
                                                         int32_t* __restrict__ tot) {
   ptx::griddep_wait();                 // hist comes from the router (or the AllGather)
   ptx::griddep_launch_dependents();
+  if (threadIdx.x == 0) { TL_MIN(0); TL_MAX(0); }
   __shared__ int32_t s_warp[33];
   const int e = blockIdx.x;
   const int q = ceil_div(NB, 128);
@@ -90,6 +92,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     int n_mt_up_tc, int n_mt_down_tc, const RouteRec* __restrict__ route,
     const uint4* __restrict__ x_all, int n, int nbr, int HB, int32_t* __restrict__ perm,
     int row_vecs, uint4* __restrict__ x_perm, int NB) {
+  if (threadIdx.x == 0) TL_MIN(1);
   constexpr int kThreads = 1024 / kSplit;
   constexpr int kRowsPerWarp = 4;                 // rows copied per warp
   constexpr int kColBlock = VPL * 32;             // 16-B vectors per column block
@@ -138,6 +141,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   if (blockIdx.x == 0) {   // the tables are out: the FFN's weight stream may start (early_tables)
     __syncthreads();
     if (threadIdx.x == 0) ptx::st_release_gpu(tb.stats + 6, 1);
+    if (threadIdx.x == 0) { TL_MIN(2); TL_MAX(2); }
   }
   // 2. stable ranks inside the block
   if (warp < 4) {
@@ -192,9 +196,12 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
         if (jj[u] >= 0 && col < row_vecs) x_perm[(size_t)jj[u] * row_vecs + col] = v[u][c];
       }
   }
+  if (threadIdx.x == 0) TL_MAX(1);
 }
 
 }  // namespace
+
+TL_EXPORT(moeshard_tl_group)
 
 void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int32_t* tot,
                          Tables tb, int n_mt_up_tc, int n_mt_down_tc, const RouteRec* route,

@@ -201,6 +201,7 @@ void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int 
 
 #include "gemm_tc.cuh"
 #include "ptx.cuh"
+#include "timeline.cuh"
 
 namespace moeshard {
 namespace {
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t ncols = EP <= 32 ? 32 : EP <= 64 ? 64 : EP <= 128 ? 128 : 256;
+  if (threadIdx.x == 0) TL_MIN(0);
 
   if (warp == 4 && lane == 0) {
     tma_prefetch_desc(&tmX);
@@ -279,6 +281,7 @@ __global__ void __launch_bounds__(192, 1)
   // PDL: x may come from the previous kernel, and the previous forward's FFN
   // still reads the route records this kernel overwrites
   griddep_wait();
+  if (threadIdx.x == 0) { TL_MIN(1); TL_MAX(1); }
   // the previous forward's FFN is done with the "tables published" flag (tb.stats[6],
   // = err_flag + 3): clear it for this forward's grouping launch to set
   if (blockIdx.x == 0 && threadIdx.x == 0) err_flag[3] = 0;
@@ -345,6 +348,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     mbar_wait(done, 0);
     tc_fence_after();
+    if (threadIdx.x == 0) { TL_MIN(2); TL_MAX(2); }
     const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     // one pass over the logit row, 32 columns per TMEM load: columns >= E are
     // masked to -inf; chunk max by a tree, argmax = the smallest column attaining
@@ -421,9 +425,12 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 0) tmem_dealloc(tmem, ncols);
+  if (threadIdx.x == 0) TL_MAX(0);
 }
 
 }  // namespace
+
+TL_EXPORT(moeshard_tl_router)
 
 size_t router_tc_smem_bytes(int EP, bool mn) {
   const int b = mn ? ((EP + 63) / 64) * 8192 : EP * 128;
