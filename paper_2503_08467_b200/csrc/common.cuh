@@ -41,6 +41,7 @@ struct Tables {
   int32_t* done;           // [chunks] up-projection tiles completed per token chunk (fused GEMM), zeroed by Step 2
   int32_t* pos;            // [E+1] internal segment starts (exclusive scan of round_up(count, 32))
   int32_t* perm_pad;       // [N + 32E] internal row -> global token id (padding rows: stale)
+  float* gate_pad;         // [N + 32E] internal row -> gate of that token (written with perm_pad)
   int32_t* next_unit;      // [1] the fused FFN's dynamic work counter, zeroed by Step 2
 };
 

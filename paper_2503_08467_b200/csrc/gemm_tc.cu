@@ -130,29 +130,36 @@ __device__ __forceinline__ Unit unit_at(const UnitList& L, int u, int n_mt, int 
 // perm[tok0+j] of the output). One 16-token chunk at a time.
 // NH warps share one 32-feature quadrant: warp half eh (< NH) takes the 16-token column
 // chunks eh, eh + NH, ... (NH = 2 halves the drain latency of a tile).
-template <bool kDown, int NH = 1>
-__device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok, int nmma,
-                                           int fbase, uint32_t taddr, int lane, uint64_t pol_keep,
-                                           __nv_bfloat16* stage, int eh = 0) {
-  uint16_t* st16 = reinterpret_cast<uint16_t*>(stage);
-  // down: the destination rows perm[j] and gates of the unit's tokens are fetched
-  // up front (lane holds tokens lane + 32 i), so the loop below has no dependent
-  // global loads - one perm latency and one gate latency per tile instead of one
-  // pair per 16 tokens (exposed when K is short, e.g. d_ff/G = 384)
-  int rows_r[BN_MAX / 32];
-  float g_r[BN_MAX / 32];
-  if (kDown) {
+// down: the destination rows perm[j] and gates of a unit's tokens, fetched up front
+// (lane holds tokens lane + 32 i) so the store loop has no dependent global loads. With
+// p.gate_pad (gate per expert-ordered row, written by Step 2 beside perm_pad) both loads
+// are independent: one latency instead of perm's then route[perm].gate's.
+__device__ __forceinline__ void load_rows_gates(const TcParams& p, int tok0, int ntok, int lane,
+                                                int (&rows_r)[BN_MAX / 32], float (&g_r)[BN_MAX / 32]) {
 #pragma unroll
-    for (int i = 0; i < BN_MAX / 32; ++i) {
-      const int tk = lane + 32 * i;
-      rows_r[i] = tk < ntok ? __ldg(p.perm + tok0 + tk) : 0;
-    }
+  for (int i = 0; i < BN_MAX / 32; ++i) {
+    const int tk = lane + 32 * i;
+    rows_r[i] = tk < ntok ? __ldg(p.perm + tok0 + tk) : 0;
+    if (p.gate_pad) g_r[i] = tk < ntok ? __ldg(p.gate_pad + tok0 + tk) : 0.f;
+  }
+  if (!p.gate_pad) {
 #pragma unroll
     for (int i = 0; i < BN_MAX / 32; ++i) {
       const int tk = lane + 32 * i;
       g_r[i] = tk < ntok ? __ldg(&p.route[rows_r[i]].gate) : 0.f;
     }
   }
+}
+
+// kPre: rows_r / g_r were loaded by the caller (load_rows_gates) ahead of the
+// accumulator wait; otherwise (down) they are loaded here.
+template <bool kDown, int NH = 1, bool kPre = false>
+__device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok, int nmma,
+                                           int fbase, uint32_t taddr, int lane, uint64_t pol_keep,
+                                           __nv_bfloat16* stage, int eh, int (&rows_r)[BN_MAX / 32],
+                                           float (&g_r)[BN_MAX / 32]) {
+  uint16_t* st16 = reinterpret_cast<uint16_t*>(stage);
+  if (kDown && !kPre) load_rows_gates(p, tok0, ntok, lane, rows_r, g_r);
   // TMEM reads are double-buffered: the load of the next chunk is in flight while
   // this one is converted and stored
   uint32_t rbuf[2][16];
@@ -391,8 +398,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * ACC_STRIDE;
+      int rows_r[BN_MAX / 32];
+      float g_r[BN_MAX / 32];
       store_tile<kDown>(p, w.tok0, w.ntok, (w.ntok + 15) & ~15, w.mt * BM + wq * 32, taddr, lane,
-                        pol_keep, stage);
+                        pol_keep, stage, 0, rows_r, g_r);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
@@ -586,8 +595,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int mt = 2 * w.mt + static_cast<int>(rank);
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * ACC_STRIDE;
+      int rows_r[BN_MAX / 32];
+      float g_r[BN_MAX / 32];
       store_tile<kDown>(p, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32, taddr, lane,
-                        pol_keep, stage);
+                        pol_keep, stage, 0, rows_r, g_r);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + as * 8);
@@ -875,6 +886,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
             __nanosleep(128);
           }
           fence_proxy_async_global();
+          if (leader) TR(cid, k, 7);
         }
         __syncwarp();
       }
@@ -914,13 +926,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
         const int nkb = down ? nkb_dn : nkb_up;
         const int nmma = (w.ntok + 31) & ~31;
         const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
+        if (lane == 0) TR(cid, k, 0);
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
+        if (lane == 0) TR(cid, k, 1);
         const uint32_t d = tmem_base + as * ACC_STRIDE;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&fullB[sb], pb);
+          if (kb == 0 && lane == 0) TR(cid, k, 2);
           mbar_wait(&fullA[sa], pa);
           tc_fence_after();
+          if (kb == 0 && lane == 0) TR(cid, k, 3);
           if (elect_one()) {
             const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
             const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B2_BYTES));
@@ -938,6 +954,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
         }
         if (elect_one()) mma_commit_2sm(&tfull[as], 0x3);
         __syncwarp();
+        if (lane == 0) TR(cid, k, 4);
         as ^= 1;
         if (as == 0) aphase ^= 1;
       }
@@ -955,8 +972,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
       bool down;
       const Unit w = unit_at(u, down);
+      // down: destination rows and gates loaded before the accumulator wait (their
+      // latency hides behind it; at short K it was exposed once per tile)
+      int rows_r[BN_MAX / 32];
+      float g_r[BN_MAX / 32];
+      if (down) load_rows_gates(fp.dn, w.tok0, w.ntok, lane, rows_r, g_r);
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
+      if (leader && warp == 4 && lane == 0) TR(cid, k, 5);
       const int mt = 2 * w.mt + static_cast<int>(rank);
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + as * ACC_STRIDE;
 #ifdef MOESHARD_EXP_NO_EPI
@@ -965,14 +988,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       if (mt < (down ? fp.dn.n_mt : fp.up.n_mt)) {   // else: duplicate of the leader's tile
 #endif
         if (down)
-          store_tile<true, kEpiWarps / 4>(fp.dn, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32,
-                                          taddr, lane, pol_keep, stage, eh);
+          store_tile<true, kEpiWarps / 4, true>(fp.dn, w.tok0, w.ntok, (w.ntok + 31) & ~31,
+                                                mt * BM + wq * 32, taddr, lane, pol_keep, stage, eh,
+                                                rows_r, g_r);
         else
-          store_tile<false, kEpiWarps / 4>(fp.up, w.tok0, w.ntok, (w.ntok + 31) & ~31, mt * BM + wq * 32,
-                                           taddr, lane, pol_keep, stage, eh);
+          store_tile<false, kEpiWarps / 4, true>(fp.up, w.tok0, w.ntok, (w.ntok + 31) & ~31,
+                                                 mt * BM + wq * 32, taddr, lane, pol_keep, stage, eh,
+                                                 rows_r, g_r);
       }
       tc_fence_before();
       __syncwarp();
+      if (leader && warp == 4 && lane == 0) TR(cid, k, 6);
       if (lane == 0) mbar_arrive_cluster(leader_tempty + as * 8);
       if (!down) {   // publish this CTA's H tile of the chunk
 #if MOESHARD_REL_WARP
@@ -1050,6 +1076,7 @@ cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUten
 }  // namespace
 
 TL_EXPORT(moeshard_tl_ffn)
+TR_EXPORT(moeshard_tr_ffn)
 
 cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,

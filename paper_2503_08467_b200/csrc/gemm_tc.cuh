@@ -28,6 +28,7 @@ struct TcParams {
   int ld_out;         // F (up) or h (down)
   const int32_t* perm;     // down: perm[j] = global token id of expert-ordered row j
   const RouteRec* route;   // down: gate per global token
+  const float* gate_pad = nullptr;   // down (fused kernel): gate per expert-ordered row
   // launch-mode ablation (Sec. 3.3, MOESHARD_FLAG_LAUNCH_PER_EXPERT / _PER_SOURCE): this
   // launch covers only expert only_e (>= 0) and, if only_g >= 0, only the tokens of source
   // rank only_g: rows [pos[e] + base[g*nbr][e], pos[e] + base[(g+1)*nbr][e]) of its segment

@@ -132,7 +132,7 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 // Workspace carve-up, shared by moeshard_workspace_size and moeshard_init.
 struct Layout {
-  size_t wt_r, route, block_hist, block_base, ints, done, perm, perm_pad, x_all, x_perm, H, partial,
+  size_t wt_r, route, block_hist, block_base, ints, done, perm, perm_pad, gate_pad, x_all, x_perm, H, partial,
       ep_route, ep_hist, ep_owner, total;
   int n_ints;
   size_t npad;   // rows of the internal expert-ordered layout: N_max + 32 per expert, rounded to 64
@@ -166,6 +166,7 @@ Layout make_layout(const moeshard_config& c, int world) {
   L.done = take((Nmax / kTcTokTile + E + 8) * 4);   // per token chunk: <= N/256 + E chunks
   L.perm = take(Nmax * 4);
   L.perm_pad = take(L.npad * 4);
+  L.gate_pad = take(L.npad * 4);
   L.x_all = coll ? take(Nmax * h * elt) : 0;
   L.x_perm = take(L.npad * h * elt);
   L.H = take(L.npad * F * elt);
@@ -466,6 +467,7 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->tb.pos = c->block_tot + E;
   c->tb.next_unit = c->tb.pos + (E + 1);
   c->tb.perm_pad = reinterpret_cast<int32_t*>(c->ws + L.perm_pad);
+  c->tb.gate_pad = reinterpret_cast<float*>(c->ws + L.gate_pad);
   c->perm = reinterpret_cast<int32_t*>(c->ws + L.perm);
   c->x_all = c->coll && !c->p2p ? c->ws + L.x_all : nullptr;
   c->x_perm = c->ws + L.x_perm;
@@ -734,6 +736,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
                   static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
       TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), Et, c->tb,
                   static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
+      dn.gate_pad = c->tb.gate_pad;
       if (c->p2p) set_p2p_out(c, dn, ns);
       CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, c->tm_xperm16, lw.tm_out, c->tm_H16, up, dn,
                                     c->tb.done, (c->cfg.flags & MOESHARD_FLAG_DYNAMIC_SCHED) != 0,

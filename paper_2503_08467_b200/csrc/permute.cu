@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   const int row_base = part * (128 / kSplit);     // this CTA's rows of the block
   ptx::griddep_wait();            // the router's records and histograms
   ptx::griddep_launch_dependents();   // the FFN's prologue may start now
+  if (threadIdx.x == 0) { TL_MIN(3); TL_MAX(3); }
   const bool has_block = b < NB;
   // issue this CTA's row loads first: the sources are known, only the
   // destinations depend on the scan below
@@ -126,9 +127,14 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     }
   }
   int e = -1, rank_w = 0, t = 0;
+  float gate = 0.f;
   if (warp < 4 && has_block) {
     t = t0 + threadIdx.x;
-    e = (t < t1) ? __ldg(&route[t].expert) : -1;
+    if (t < t1) {
+      const RouteRec rec = route[t];
+      e = rec.expert;
+      gate = rec.gate;
+    }
   }
   for (int k = threadIdx.x; k < E; k += kThreads) {
     s_tot[k] = __ldg(btot + k);                        // tokens of expert k overall
@@ -136,8 +142,10 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   }
   for (int k = threadIdx.x; k < 4 * E; k += kThreads) whist[k / E][k % E] = 0;
   __syncthreads();
+  if (threadIdx.x == 0) { TL_MIN(4); TL_MAX(4); }
   segment_tables<kThreads>(E, s_tot, s_pre, s_base, s_bpad, s_warp, blockIdx.x == 0, tb,
                            n_mt_up_tc, n_mt_down_tc);
+  if (threadIdx.x == 0) { TL_MIN(5); TL_MAX(5); }
   if (blockIdx.x == 0) {   // the tables are out: the FFN's weight stream may start (early_tables)
     __syncthreads();
     if (threadIdx.x == 0) ptx::st_release_gpu(tb.stats + 6, 1);
@@ -159,6 +167,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
       if (part == 0) {
         perm[j] = t;
         tb.perm_pad[jp] = t;
+        tb.gate_pad[jp] = gate;   // the down epilogue reads row and gate without an indirection
       }
       s_j[threadIdx.x] = jp;
     } else {
@@ -167,6 +176,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   }
   __syncthreads();
   // 3. row stores (first column block loaded at the top)
+  if (threadIdx.x == 0) { TL_MIN(6); TL_MAX(6); }
   if (x_perm == nullptr || !has_block) return;
   int jj[kRowsPerWarp];
 #pragma unroll

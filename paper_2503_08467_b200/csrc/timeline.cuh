@@ -22,8 +22,27 @@ __device__ __forceinline__ unsigned long long tl_now() {
     }                                                                             \
     return static_cast<int>(cudaDeviceSynchronize());                             \
   }
+// per-unit trace of the fused FFN: [cluster < 148][unit slot < 16][8 stamps]
+static __device__ unsigned long long g_tr[148 * 16 * 8];
+#define TR(cl, k, j)                                              \
+  do {                                                            \
+    if ((cl) < 148 && (k) < 16) g_tr[((cl) * 16 + (k)) * 8 + (j)] = tl_now(); \
+  } while (0)
+#define TR_EXPORT(name)                                                          \
+  extern "C" int name(unsigned long long* out, int reset) {                       \
+    if (out) cudaMemcpyFromSymbol(out, g_tr, sizeof(g_tr));                       \
+    if (reset) cudaMemset(reinterpret_cast<void*>(0), 0, 0);                      \
+    if (reset) {                                                                 \
+      void* p = nullptr;                                                         \
+      cudaGetSymbolAddress(&p, g_tr);                                            \
+      cudaMemset(p, 0, sizeof(g_tr));                                            \
+    }                                                                            \
+    return static_cast<int>(cudaDeviceSynchronize());                            \
+  }
 #else
 #define TL_MIN(i)
 #define TL_MAX(i)
 #define TL_EXPORT(name)
+#define TR(cl, k, j)
+#define TR_EXPORT(name)
 #endif
