@@ -40,7 +40,7 @@ for g in graphs:
     g.replay()
 torch.cuda.synchronize()
 names = {"router": ["start/end", "after griddep_wait", "mainloop done"],
-         "group": ["scan after wait", "grouping start/end", "tables published"],
+         "group": ["scan after wait", "grouping start/end", "tables published", "grp after wait", "grp before tables", "grp after tables", "grp ranks done"],
          "ffn": ["start/end", "tables read", "token producer go", "last MMA issued"]}
 acc = {}
 reps = 12
