@@ -642,18 +642,8 @@ constexpr int kFusedThreads = 128 + 32 * kEpiWarps;
 static_assert(kEpiWarps % 4 == 0 && kEpiWarps <= 16, "1-4 epilogue warps per TMEM lane quadrant");
 constexpr int kUQ = 2;             // unit-queue slots (dynamic scheduling): small, so a
                                    // cluster never sits on units other clusters could run
-#ifndef MOESHARD_REL_WARP
-#define MOESHARD_REL_WARP 0
-#endif
-#if MOESHARD_REL_WARP
-// warps that read a slot: leader 0,1,2,3 + epilogue; follower 0,2,3 + epilogue (the
-// follower's warp 1 runs the scheduler)
-constexpr int kUQConsumers = 7 + 2 * kEpiWarps;
-constexpr uint32_t kSchedRank = 1;
-#else
 constexpr int kUQConsumers = 5 + 2 * kEpiWarps;   // warps that read a slot: leader 0,1,3 + epilogue; follower 0,3 + epilogue
-constexpr uint32_t kSchedRank = 0;
-#endif
+constexpr uint32_t kSchedRank = 0;   // the unit scheduler's CTA (leader)
 
 template <int AS, int BS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
@@ -684,7 +674,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   uint64_t* uq_full = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(s_uq + kUQ) + 7) & ~static_cast<uintptr_t>(7));
   uint64_t* uq_empty = uq_full + kUQ;
-  uint64_t* hrel = uq_empty + kUQ;   // [2] epilogue warps -> release warp: H tile stored
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -715,7 +704,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       mbar_init(&uq_full[q], 1);
       mbar_init(&uq_empty[q], kUQConsumers);
     }
-    for (int a = 0; a < 2; ++a) mbar_init(&hrel[a], kEpiWarps);
     fence_mbar_init();
   }
   cluster_sync_all();
@@ -784,9 +772,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
                 : decode(u, n_mp_up, E, s_pref, s_off, s_end, s_cs);
   };
 
-  // unit scheduler (dynamic mode), on the CTA kSchedRank: the leader's idle warp 2, or
-  // (MOESHARD_REL_WARP, where warp 2 releases H tiles) the follower's idle warp 1
-  const bool sched_warp = fp.dynamic && rank == kSchedRank && warp == (MOESHARD_REL_WARP ? 1 : 2);
+  // unit scheduler (dynamic mode): the leader's otherwise idle warp 2
+  const bool sched_warp = fp.dynamic && rank == kSchedRank && warp == 2;
   if (sched_warp) {
     {
       // ------------------------------------------------------------ unit scheduler
@@ -807,27 +794,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
         if (u >= total) break;
       }
     }
-  } else if (warp == 2) {
-#if MOESHARD_REL_WARP
-    // -------------------------------------------------------------- H release (both CTAs)
-    // the epilogue warps arrive on hrel[as] after their H stores of an up unit (mbarrier
-    // arrive: release at CTA scope); this warp acquires it and publishes the tile with one
-    // red.release.gpu (cumulative: covers the stores it observed), so no epilogue warp
-    // waits on a CTA barrier or a GPU-scope fence
-    int as = 0;
-    uint32_t hph[2] = {0u, 0u};
-    for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
-      const bool down = u >= total_up;
-      if (!down) {
-        const Unit w = decode(u, n_mp_up, E, s_pref, s_off, s_end, s_cs);
-        mbar_wait(&hrel[as], hph[as]);
-        hph[as] ^= 1u;
-        if (lane == 0) red_release_gpu_add(fp.done + w.chunk, 1);
-        __syncwarp();
-      }
-      as ^= 1;
-    }
-#endif
   } else if (warp == 0) {
     // -------------------------------------------------------------- weight producer (both CTAs)
     // weight tiles are streamed once (evict_first) - except an expert's tiles when it has
@@ -1001,15 +967,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       if (leader && warp == 4 && lane == 0) TR(cid, k, 6);
       if (lane == 0) mbar_arrive_cluster(leader_tempty + as * 8);
       if (!down) {   // publish this CTA's H tile of the chunk
-#if MOESHARD_REL_WARP
-        if (lane == 0) mbar_arrive(&hrel[as]);   // the release warp publishes it
-#else
         // bar.sync orders every epilogue thread's H stores before thread 0's release
         // (cumulative at gpu scope), so the other warps need no fence of their own and
         // go straight on to the next tile
         asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");   // the epilogue warps
         if (warp == 4 && lane == 0) red_release_gpu_add(fp.done + w.chunk, 1);
-#endif
       }
       as ^= 1;
       if (as == 0) aphase ^= 1;
