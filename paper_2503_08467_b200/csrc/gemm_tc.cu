@@ -151,6 +151,31 @@ __device__ __forceinline__ void load_rows_gates(const TcParams& p, int tok0, int
   }
 }
 
+// The same for an epilogue warp that drains column chunks eh, eh + NH, ... of a tile
+// (store_tile_stm): register `it` holds the token of its it-th chunk at lane & 15, so every
+// register index in the drain loop is a compile-time constant whatever eh is.
+template <int NH>
+__device__ __forceinline__ void load_rows_gates_chunked(const TcParams& p, int tok0, int ntok,
+                                                        int lane, int eh,
+                                                        int (&rows_r)[BN_MAX / 32],
+                                                        float (&g_r)[BN_MAX / 32]) {
+  constexpr int kChunks = (BN_MAX / 16 + NH - 1) / NH;
+  static_assert(kChunks <= BN_MAX / 32, "two or more warps per lane quadrant");
+#pragma unroll
+  for (int it = 0; it < kChunks; ++it) {
+    const int tk = 16 * eh + 16 * NH * it + (lane & 15);
+    rows_r[it] = tk < ntok ? __ldcg(p.perm + tok0 + tk) : 0;
+    if (p.gate_pad) g_r[it] = tk < ntok ? __ldcg(p.gate_pad + tok0 + tk) : 0.f;
+  }
+  if (!p.gate_pad) {
+#pragma unroll
+    for (int it = 0; it < kChunks; ++it) {
+      const int tk = 16 * eh + 16 * NH * it + (lane & 15);
+      g_r[it] = tk < ntok ? __ldg(&p.route[rows_r[it]].gate) : 0.f;
+    }
+  }
+}
+
 // kPre: rows_r / g_r were loaded by the caller (load_rows_gates) ahead of the
 // accumulator wait; otherwise (down) they are loaded here.
 template <bool kDown, int NH = 1, bool kPre = false>
@@ -174,7 +199,7 @@ __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok
   }
 #endif
 #pragma unroll
-  for (int it = 0; it < BN_MAX / (16 * NH); ++it) {
+  for (int it = 0; it < (BN_MAX / 16 + NH - 1) / NH; ++it) {
     const int c0 = first + 16 * NH * it;
     if (c0 >= nmma) break;
     uint32_t (&r)[16] = rbuf[it & 1];
@@ -236,6 +261,97 @@ __device__ __forceinline__ void store_tile(const TcParams& p, int tok0, int ntok
 #ifndef MOESHARD_EXP_NO_TMEMLD
     if (cn < nmma) tmem_ld_wait(rn);
 #endif
+  }
+}
+
+// The fused kernel's epilogue of one tile, transposed by stmatrix: each 16-token column
+// chunk is read from TMEM in the mma fragment layout (tcgen05.ld 16x256b: a thread holds two
+// features x two adjacent tokens per 8 x 8 block), packed to bf16 pairs and written to the
+// warp's staging buffer [16 tokens][32 features] with two stmatrix.trans.x4 (instead of 16
+// two-byte shared stores), then stored as 16-B row segments as in store_tile. Rows of the
+// staging buffer are kStmRow = 80 B apart (conflict-free stmatrix rows).
+constexpr int kStmRow = 80;
+constexpr int kStmStage = 16 * kStmRow;   // bytes per epilogue warp
+template <bool kDown, int NH>
+__device__ __forceinline__ void store_tile_stm(const TcParams& p, int tok0, int ntok, int nmma,
+                                               int fbase, uint32_t taddr, int lane,
+                                               uint64_t pol_keep, uint8_t* stage, int eh,
+                                               int (&rows_r)[BN_MAX / 32],
+                                               float (&g_r)[BN_MAX / 32]) {
+  const int m = lane >> 3, k = lane & 7;   // stmatrix: matrix m, stored row (token) k
+  const uint32_t row_addr = smem_u32(stage) + ((m >> 1) * 8 + k) * kStmRow + (m & 1) * 16;
+  const int tq = 2 * (lane & 3);           // this thread's first token of each 8-token block
+  uint32_t rb[2][2][8];                    // [buffer][lane half][regs]
+  const int first = 16 * eh;
+  if (first < nmma) {
+    tmem_ld_16x256b_x2(taddr + first, rb[0][0]);
+    tmem_ld_16x256b_x2(taddr + (16u << 16) + first, rb[0][1]);
+    tmem_ld_wait8(rb[0][0], rb[0][1]);
+  }
+#pragma unroll
+  for (int it = 0; it < (BN_MAX / 16 + NH - 1) / NH; ++it) {
+    const int c0 = first + 16 * NH * it;
+    if (c0 >= nmma) break;
+    uint32_t (&ra)[2][8] = rb[it & 1];
+    uint32_t (&rn)[2][8] = rb[(it + 1) & 1];
+    const int cn = c0 + 16 * NH;
+    if (cn < nmma) {
+      tmem_ld_16x256b_x2(taddr + cn, rn[0]);
+      tmem_ld_16x256b_x2(taddr + (16u << 16) + cn, rn[1]);
+    }
+    int row = 0;
+    float g0 = 1.f, g1 = 1.f, g8 = 1.f, g9 = 1.f;
+    if (kDown) {
+      // this warp's it-th chunk: token c0 + i lives in lane i of register it
+      // (load_rows_gates_chunked)
+      row = __shfl_sync(0xffffffffu, rows_r[it], lane & 15);
+      g0 = __shfl_sync(0xffffffffu, g_r[it], tq);
+      g1 = __shfl_sync(0xffffffffu, g_r[it], tq + 1);
+      g8 = __shfl_sync(0xffffffffu, g_r[it], tq + 8);
+      g9 = __shfl_sync(0xffffffffu, g_r[it], tq + 9);
+    }
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const uint32_t* r = ra[hh];
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+      if (kDown) {
+        v[0] *= g0; v[1] *= g1; v[2] *= g0; v[3] *= g1;
+        v[4] *= g8; v[5] *= g9; v[6] *= g8; v[7] *= g9;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+      }
+      // matrices: 0 = features 16hh+0..7 x tokens 0..7, 1 = features +8..15 x tokens 0..7,
+      // 2 = features 0..7 x tokens 8..15, 3 = features 8..15 x tokens 8..15
+      stmatrix_x4_trans(row_addr + hh * 32, pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                        pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int q = lane + 32 * i;  // 64 vectors of 16 B: 16 tokens x 4 parts
+      const int j = q >> 2, part = q & 3;
+      const uint4 v = *reinterpret_cast<const uint4*>(stage + j * kStmRow + part * 16);
+      if (kDown) {
+        const int rj = __shfl_sync(0xffffffffu, row, j);
+        if (c0 + j < ntok) {
+          __nv_bfloat16* dst;
+          if (p.p2p_n > 0) {   // the owner's receive slot for this rank, over NVLink
+            const int o = rj / p.p2p_n;
+            dst = p.p2p_out[o] + (size_t)(rj - o * p.p2p_n) * p.ld_out;
+          } else {
+            dst = p.out + (size_t)rj * p.ld_out;
+          }
+          *reinterpret_cast<uint4*>(dst + fbase + part * 8) = v;
+        }
+      } else if (c0 + j < ntok) {
+        st_v4_hint(p.out + (size_t)(tok0 + c0 + j) * p.ld_out + fbase + part * 8, v, pol_keep);
+      }
+    }
+    __syncwarp();
+    if (cn < nmma) tmem_ld_wait8(rn[0], rn[1]);
   }
 }
 
@@ -637,9 +753,14 @@ struct FusedParams {
 #ifndef MOESHARD_EPI_WARPS
 #define MOESHARD_EPI_WARPS 8
 #endif
+#ifndef MOESHARD_EPI_STM
+#define MOESHARD_EPI_STM 1
+#endif
 constexpr int kEpiWarps = MOESHARD_EPI_WARPS;   // epilogue warps per CTA (multiple of 4)
 constexpr int kFusedThreads = 128 + 32 * kEpiWarps;
 static_assert(kEpiWarps % 4 == 0 && kEpiWarps <= 16, "1-4 epilogue warps per TMEM lane quadrant");
+static_assert(MOESHARD_EPI_STM || kEpiWarps <= 8,
+              "store_tile indexes its row registers statically only for 1-2 warps per quadrant");
 constexpr int kUQ = 2;             // unit-queue slots (dynamic scheduling): small, so a
                                    // cluster never sits on units other clusters could run
 constexpr int kUQConsumers = 5 + 2 * kEpiWarps;   // warps that read a slot: leader 0,1,3 + epilogue; follower 0,3 + epilogue
@@ -670,7 +791,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   // per-warp epilogue staging (4 x 1 KB), then the unit queue (slots + barriers)
   __nv_bfloat16* s_stage = reinterpret_cast<__nv_bfloat16*>(
       (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15));
-  int* s_uq = reinterpret_cast<int*>(s_stage + kEpiWarps * 512);
+  int* s_uq = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(s_stage) + kEpiWarps * kStmStage);
   uint64_t* uq_full = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(s_uq + kUQ) + 7) & ~static_cast<uintptr_t>(7));
   uint64_t* uq_empty = uq_full + kUQ;
@@ -942,7 +1063,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       // latency hides behind it; at short K it was exposed once per tile)
       int rows_r[BN_MAX / 32];
       float g_r[BN_MAX / 32];
+#if MOESHARD_EPI_STM
+      if (down) load_rows_gates_chunked<kEpiWarps / 4>(fp.dn, w.tok0, w.ntok, lane, eh, rows_r, g_r);
+#else
       if (down) load_rows_gates(fp.dn, w.tok0, w.ntok, lane, rows_r, g_r);
+#endif
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       if (leader && warp == 4 && lane == 0) TR(cid, k, 5);
@@ -953,6 +1078,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
 #else
       if (mt < (down ? fp.dn.n_mt : fp.up.n_mt)) {   // else: duplicate of the leader's tile
 #endif
+#if MOESHARD_EPI_STM
+        uint8_t* stg = reinterpret_cast<uint8_t*>(s_stage) + (warp - 4) * kStmStage;
+        if (down)
+          store_tile_stm<true, kEpiWarps / 4>(fp.dn, w.tok0, w.ntok, (w.ntok + 31) & ~31,
+                                              mt * BM + wq * 32, taddr, lane, pol_keep, stg, eh,
+                                              rows_r, g_r);
+        else
+          store_tile_stm<false, kEpiWarps / 4>(fp.up, w.tok0, w.ntok, (w.ntok + 31) & ~31,
+                                               mt * BM + wq * 32, taddr, lane, pol_keep, stg, eh,
+                                               rows_r, g_r);
+#else
         if (down)
           store_tile<true, kEpiWarps / 4, true>(fp.dn, w.tok0, w.ntok, (w.ntok + 31) & ~31,
                                                 mt * BM + wq * 32, taddr, lane, pol_keep, stage, eh,
@@ -961,6 +1097,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
           store_tile<false, kEpiWarps / 4, true>(fp.up, w.tok0, w.ntok, (w.ntok + 31) & ~31,
                                                  mt * BM + wq * 32, taddr, lane, pol_keep, stage, eh,
                                                  rows_r, g_r);
+#endif
       }
       tc_fence_before();
       __syncwarp();
@@ -993,7 +1130,7 @@ size_t smem_bytes(int E, int as, int bs) {
 
 size_t smem_bytes_2sm(int E, int as, int bs) {
   return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (4 * E + 2) * 4 +
-         16 + kEpiWarps * 1024 + 96;   // + epilogue staging (1 KB per epilogue warp) + unit queue
+         16 + kEpiWarps * kStmStage + 96;   // + epilogue staging (per epilogue warp) + unit queue
 }
 
 template <bool kDown, int AS, int BS>
