@@ -52,48 +52,81 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
 // pre, s_bpad[e] = internal padded start + pre, where pre = tokens of e in
 // earlier hist-blocks. If `publish`, also writes the tables the grouped
 // GEMMs read (counts, offsets, chunking, padded starts, done = 0, stats).
+// The five exclusive prefixes (count, padded count, tcgen05 chunks, SIMT chunks, tcgen05
+// rows) are computed in ONE pass: warp-level scans of all five, one exchange of the warp
+// totals through s_warp (>= 5 * kThreads / 32 + 5 ints), two CTA barriers in total (the
+// grouping CTAs sit on this before their row copies; five separate CTA-wide scans cost
+// 1-2.6 us of the pre-FFN critical path).
 template <int kThreads>
 __device__ __forceinline__ void segment_tables(int E, const int* s_tot, const int* s_pre,
                                                int* s_base, int* s_bpad, int* s_warp, bool publish,
                                                Tables tb, int n_mt_up_tc, int n_mt_down_tc) {
-  const int e = threadIdx.x;
-  int cnt = 0, nc = 0, cs = 0, rows = 0, sc = 0;
+  constexpr int kWarps = kThreads / 32;
+  const int e = threadIdx.x, lane = e & 31, w = e >> 5;
+  int v[5] = {0, 0, 0, 0, 0};   // count, padded count, tc chunks, simt chunks, tc rows
+  int cs = 0;
   if (e < E) {
-    cnt = s_tot[e];
+    const int cnt = s_tot[e];
+    int nc;
     tc_chunking(cnt, &nc, &cs);
-    rows = nc > 0 ? (cnt / cs) * cs + round_up(cnt % cs, 32) : 0;
-    sc = ceil_div(cnt, kSimtTokTile);
+    v[0] = cnt;
+    v[1] = round_up(cnt, kSegAlign);
+    v[2] = nc;
+    v[3] = ceil_div(cnt, kSimtTokTile);
+    v[4] = nc > 0 ? (cnt / cs) * cs + round_up(cnt % cs, 32) : 0;
   }
-  int tot_cnt, tot_pad;
-  const int off = block_excl_scan<kThreads>(cnt, s_warp, tot_cnt);
-  const int pos = block_excl_scan<kThreads>(round_up(cnt, kSegAlign), s_warp, tot_pad);
+  int inc[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    inc[i] = v[i];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, inc[i], off);
+      if (lane >= off) inc[i] += o;
+    }
+  }
+  __syncthreads();   // s_warp may still be read by an earlier scan
+  if (lane == 31) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) s_warp[i * kWarps + w] = inc[i];
+  }
+  __syncthreads();
+  int ex[5], tot[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    int before = 0, all = 0;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) {
+      const int ws = s_warp[i * kWarps + q];
+      before += q < w ? ws : 0;
+      all += ws;
+    }
+    ex[i] = before + inc[i] - v[i];
+    tot[i] = all;
+  }
   if (e < E) {
-    s_base[e] = off + s_pre[e];
-    s_bpad[e] = pos + s_pre[e];
+    s_base[e] = ex[0] + s_pre[e];
+    s_bpad[e] = ex[1] + s_pre[e];
   }
   if (publish) {
-    int tot_tc, tot_sc, tot_rows;
-    const int tcp = block_excl_scan<kThreads>(nc, s_warp, tot_tc);
-    const int smp = block_excl_scan<kThreads>(sc, s_warp, tot_sc);
-    block_excl_scan<kThreads>(rows, s_warp, tot_rows);
-    for (int i = threadIdx.x; i < tot_tc; i += kThreads) tb.done[i] = 0;   // per token chunk
+    for (int i = threadIdx.x; i < tot[2]; i += kThreads) tb.done[i] = 0;   // per token chunk
     if (e < E) {
-      tb.pos[e] = pos;
-      tb.counts[e] = cnt;
+      tb.pos[e] = ex[1];
+      tb.counts[e] = v[0];
       tb.tc_chunk_size[e] = cs;
-      tb.offsets[e] = off;
-      tb.tc_chunk_pref[e] = tcp;
-      tb.simt_chunk_pref[e] = smp;
+      tb.offsets[e] = ex[0];
+      tb.tc_chunk_pref[e] = ex[2];
+      tb.simt_chunk_pref[e] = ex[3];
     }
     if (threadIdx.x == 0) {
       tb.next_unit[0] = 0;
-      tb.pos[E] = tot_pad;
-      tb.offsets[E] = tot_cnt;
-      tb.tc_chunk_pref[E] = tot_tc;
-      tb.simt_chunk_pref[E] = tot_sc;
-      tb.stats[0] = tot_tc * n_mt_up_tc;
-      tb.stats[1] = tot_tc * n_mt_down_tc;
-      tb.stats[2] = tot_rows * n_mt_up_tc;
+      tb.pos[E] = tot[1];
+      tb.offsets[E] = tot[0];
+      tb.tc_chunk_pref[E] = tot[2];
+      tb.simt_chunk_pref[E] = tot[3];
+      tb.stats[0] = tot[2] * n_mt_up_tc;
+      tb.stats[1] = tot[2] * n_mt_down_tc;
+      tb.stats[2] = tot[4] * n_mt_up_tc;
     }
   }
 }

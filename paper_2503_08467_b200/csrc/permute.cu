@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   __shared__ int32_t s_bpad[kMaxExperts];   // padded internal position
   __shared__ int32_t whist[4][kMaxExperts];
   __shared__ int32_t s_j[128];
-  __shared__ int32_t s_warp[33];
+  __shared__ int32_t s_warp[5 * (kThreads / 32)];   // segment_tables' warp totals
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x / kSplit, part = blockIdx.x % kSplit;
   const int r = b / nbr, i = b - r * nbr;
