@@ -17,8 +17,11 @@
 //   warp 0      TMA producer of the weight tiles (one lane), A_STAGES-deep ring
 //   warp 3      TMA producer of the token tiles (one lane), B_STAGES-deep ring
 //   warp 1      MMA issuer (one lane), double-buffered TMEM accumulator
-//   warp 2      TMEM allocator
-//   warps 4-7   epilogue: tcgen05.ld -> registers -> global (lane quadrant = warp % 4)
+//   warp 2      TMEM allocator (and, dynamic scheduling, the unit scheduler)
+//   warps 4-    epilogue: tcgen05.ld -> registers -> global (lane quadrant = warp % 4);
+//               the fused kernel (tc_moe_ffn_2sm, the product path) has 8 of them, two per
+//               quadrant, and transposes each 16-token chunk through stmatrix (the drain of
+//               the accumulators bounds it: profiles/r02/experiments_r02.md)
 // Work units (expert e, 128-feature tile mt, token chunk c) are decoded on
 // the device from the segment tables written by the grouping kernels, so no
 // host round-trip is needed (CUDA-graph capturable). Units of the same
