@@ -110,12 +110,14 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   const int t0 = r * n + i * HB;
   const int t1 = min(t0 + HB, (r + 1) * n);
   const int row_base = part * (128 / kSplit);     // this CTA's rows of the block
-  ptx::griddep_wait();            // the router's records and histograms
-  ptx::griddep_launch_dependents();   // the FFN's prologue may start now
-  if (threadIdx.x == 0) { TL_MIN(3); TL_MAX(3); }
+  // Everything that needs only the routing runs before the wait for the block scan: this
+  // grid is launched once the scan has passed its own wait, so the route records and token
+  // rows (router, AllGather or peer pushes, all before the scan) are complete. The stable
+  // ranks inside the block (match_any) and the row loads overlap the scan; only the
+  // segment starts need it.
   const bool has_block = b < NB;
   // issue this CTA's row loads first: the sources are known, only the
-  // destinations depend on the scan below
+  // destinations depend on the scan
   uint4 v[kRowsPerWarp][VPL];
 #pragma unroll
   for (int u = 0; u < kRowsPerWarp; ++u) {
@@ -136,21 +138,8 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
       gate = rec.gate;
     }
   }
-  for (int k = threadIdx.x; k < E; k += kThreads) {
-    s_tot[k] = __ldg(btot + k);                        // tokens of expert k overall
-    s_pre[k] = __ldg(bbase + (size_t)b * E + k);       // ... in blocks before this one
-  }
   for (int k = threadIdx.x; k < 4 * E; k += kThreads) whist[k / E][k % E] = 0;
   __syncthreads();
-  if (threadIdx.x == 0) { TL_MIN(4); TL_MAX(4); }
-  segment_tables<kThreads>(E, s_tot, s_pre, s_base, s_bpad, s_warp, blockIdx.x == 0, tb,
-                           n_mt_up_tc, n_mt_down_tc);
-  if (threadIdx.x == 0) { TL_MIN(5); TL_MAX(5); }
-  if (blockIdx.x == 0) {   // the tables are out: the FFN's weight stream may start (early_tables)
-    __syncthreads();
-    if (threadIdx.x == 0) ptx::st_release_gpu(tb.stats + 6, 1);
-    if (threadIdx.x == 0) { TL_MIN(2); TL_MAX(2); }
-  }
   // 2. stable ranks inside the block
   if (warp < 4) {
     const unsigned peers = __match_any_sync(0xffffffffu, e);
@@ -158,12 +147,29 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     if (e >= 0 && rank_w == 0) whist[warp][e] = __popc(peers);
   }
   __syncthreads();
+  if (warp < 4 && e >= 0)
+    for (int w = 0; w < warp; ++w) rank_w += whist[w][e];   // rank inside the block
+  ptx::griddep_wait();            // the block scan (base, tot)
+  ptx::griddep_launch_dependents();   // the FFN's prologue may start now
+  if (threadIdx.x == 0) { TL_MIN(3); TL_MAX(3); }
+  for (int k = threadIdx.x; k < E; k += kThreads) {
+    s_tot[k] = __ldg(btot + k);                        // tokens of expert k overall
+    s_pre[k] = __ldg(bbase + (size_t)b * E + k);       // ... in blocks before this one
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) { TL_MIN(4); TL_MAX(4); }
+  segment_tables<kThreads>(E, s_tot, s_pre, s_base, s_bpad, s_warp, blockIdx.x == 0, tb,
+                           n_mt_up_tc, n_mt_down_tc);
+  if (threadIdx.x == 0) { TL_MIN(5); TL_MAX(5); }
+  __syncthreads();   // s_base / s_bpad of every expert
+  if (blockIdx.x == 0) {   // the tables are out: the FFN's weight stream may start (early_tables)
+    if (threadIdx.x == 0) ptx::st_release_gpu(tb.stats + 6, 1);
+    if (threadIdx.x == 0) { TL_MIN(2); TL_MAX(2); }
+  }
   if (warp < 4) {
     if (e >= 0) {
-      int before = 0;
-      for (int w = 0; w < warp; ++w) before += whist[w][e];
-      const int j = s_base[e] + before + rank_w;         // public, compact
-      const int jp = s_bpad[e] + before + rank_w;        // internal, padded segments
+      const int j = s_base[e] + rank_w;         // public, compact
+      const int jp = s_bpad[e] + rank_w;        // internal, padded segments
       if (part == 0) {
         perm[j] = t;
         tb.perm_pad[jp] = t;
