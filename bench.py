@@ -227,6 +227,35 @@ ENCODERS = {
 }
 
 
+def self_check(layer, cfg, seed, x, w_r, out, r, t0, G, dist, dev, n_check=8):
+    """Output check of the measured configuration (every rank, after the timed regions):
+    this rank's first n_check tokens of the last forward (out = the rank's rows after the
+    exchange) against the fp64 oracle, with the GPU's expert choices (R13) and one expert's
+    full weights generated at a time. Max over ranks."""
+    import numpy as np
+    import oracle
+    import workload as W
+    torch = __import__("torch")
+    E, h, d_ff = cfg["E"], cfg["h"], cfg["d_ff"]
+    xs = x[:n_check].float().cpu().numpy()
+    experts = r["expert"][t0:t0 + n_check].cpu().numpy()
+
+    def weights(e):
+        wi, wo = W.make_expert_weights(seed, E, h, d_ff, device=dev, experts=[e], layer=0)
+        return wi[0].double().cpu().numpy(), wo[0].double().cpu().numpy()
+
+    y_ref, _ = oracle.moe_layer_tokens(xs, w_r.float().cpu().numpy(), weights, forced_rows=experts)
+    err = oracle.max_abs_rel(out[:n_check].float().cpu().numpy(), y_ref)
+    if G > 1:
+        t = torch.tensor([err], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        err = t.item()
+    return {"tokens_per_rank": n_check, "max_abs_rel": float(err), "tolerance": 2e-2,
+            "ok": bool(err <= 2e-2),
+            "how": "each rank's first tokens of the last forward vs the fp64 oracle "
+                   "(oracle.moe_layer_tokens, the GPU's expert choice), max over ranks"}
+
+
 def encoder_ttft(name, G, rank, local, barrier, dist, reps=10, oracle_sample=2048):
     """TTFT = one encoder forward over the batch, max over ranks:
     torch attention / dense FFN replicated data-parallel, MoE FFNs through the
@@ -468,6 +497,8 @@ def main():
     launches = launch_count["timed"] if args.eager else per_fwd * args.steps
     st_uniform = layer.stats()
     r = layer.routing(n)
+    torch.cuda.synchronize()
+    check = self_check(layer, cfg, seed, x, w_r, out, r, t0, G, dist, dev)
     counts = r["counts"].cpu()
     e_active_u = int((counts > 0).sum())
     max_tok_u = int(counts.max())
@@ -625,6 +656,7 @@ def main():
         "timing_mode": "eager launches" if args.eager else "CUDA-graph replay of one forward per step",
         "step_us": dict(dist_us, mean=round(ms * 1e3, 2), eager_mean=round(ms_eager * 1e3, 2)),
         "clocks": clk.summary(),
+        "self_check": check,
     }
     if e2e is not None:
         line["e2e"] = e2e
