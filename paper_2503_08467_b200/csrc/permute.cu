@@ -231,8 +231,12 @@ void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int3
   auto* xd = static_cast<uint4*>(x_perm);
   // each hist-block's rows are copied by kSplit = 4 CTAs of 256 threads; rows wider
   // than 8 * 32 vectors (4 KB) are copied in column blocks of 4 KB
+#ifndef MOESHARD_GROUP_SPLIT
+#define MOESHARD_GROUP_SPLIT 4
+#endif
+  constexpr int kSp = MOESHARD_GROUP_SPLIT;
 #define SG(V)                                                                                  \
-  launch_pdl(group_scatter_gather<V, 4>, dim3(NB * 4), dim3(256), 0, s, base, tot, E, tb,      \
+  launch_pdl(group_scatter_gather<V, kSp>, dim3(NB * kSp), dim3(1024 / kSp), 0, s, base, tot, E, tb, \
              n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm, row_vecs, xd, NB)
   switch (vpl) {
     case 1: SG(1); break;
