@@ -830,7 +830,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     }
     fence_mbar_init();
   }
-  cluster_sync_all();
+  // no cluster barrier here: the mbarrier inits reach the peer through the cluster barrier
+  // after the tables below, before any remote arrive (A/B: -0.3 us)
   if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
   // PDL: everything above overlapped the grouping kernel's tail. early_tables: the
   // grouping launch's CTA 0 publishes the segment tables (release on tb.stats[6]) before
