@@ -201,7 +201,7 @@ def run_reference(args, cfg, seed):
                          "sample": f"{n_s} consecutive tokens per step of the {N}-token layer"},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    _emit(line)
 
 
 def _config_json(cfg, args, G):
@@ -351,7 +351,23 @@ def encoder_ttft(name, G, rank, local, barrier, dist, reps=10, oracle_sample=204
 
 
 # ------------------------------------------------------------------ our arm
+# stdout carries exactly one JSON line: the process's stdout (fd 1) is pointed at stderr for
+# everything else - libraries that print at C level (NCCL's version / init lines) included -
+# and the JSON line is written to a duplicate of the original stdout
+_JSON_OUT = None
+
+
+def _emit(line: dict) -> None:
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=300)
@@ -394,8 +410,10 @@ def main():
     G = world
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
+    # NCCL's log (its version line, and at G > 1 the communicator init lines: rank / nranks /
+    # NVLS, for the scaling record) goes to stderr: stdout carries only the JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if G > 1:
-        # communicator init lines (rank / nranks / NVLS) in the log, for the scaling record
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device(dev))
@@ -676,7 +694,7 @@ def main():
         except Exception as ex:  # report, never hide
             line["cpu_baseline"] = {"error": repr(ex)}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        _emit(line)
     layer.close()
     if G > 1:
         dist.destroy_process_group()

@@ -54,6 +54,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  // optional (NCCL >= 2.18): a second communicator over the same ranks for the side stream
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
@@ -86,6 +88,7 @@ NcclApi& nccl() {
   LOAD(GroupEnd, "ncclGroupEnd");
   LOAD(GetErrorString, "ncclGetErrorString");
 #undef LOAD
+  api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(dlsym(h, "ncclCommSplit"));
   api.ok = true;
   return api;
 }
@@ -212,6 +215,9 @@ struct moeshard_ctx {
   int EP = 16;
   std::vector<LayerW> layers;
   ncclComm_t comm = nullptr;
+  // the token AllGather forked onto s_x runs on its own communicator (split from comm): two
+  // streams never issue concurrent operations on one communicator, whatever NCCL's ordering
+  ncclComm_t comm_x = nullptr;
   // Step 3 token AllGather overlapped with Step 1 (x does not depend on the routing): the
   // AllGather of x runs on s_x, forked from the caller's stream before the router and joined
   // after the metadata AllGather (MOESHARD_FLAG_SERIAL_AG: everything on the caller's stream)
@@ -287,7 +293,8 @@ int allgather_tokens(moeshard_ctx* c, const void* hidden, int n, int ns, bool un
                                   cudaMemcpyDeviceToDevice, st));
     xsend = slot;
   }
-  NCCL_TRY(c, nccl().AllGather(xsend, c->x_all, static_cast<size_t>(ns) * c->h, ndt, c->comm, st));
+  NCCL_TRY(c, nccl().AllGather(xsend, c->x_all, static_cast<size_t>(ns) * c->h, ndt,
+                               st == c->s_x && c->comm_x ? c->comm_x : c->comm, st));
   return MOESHARD_OK;
 }
 
@@ -540,7 +547,16 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
       delete c;
       return fail(nullptr, MOESHARD_ERR_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
     }
-    c->overlap_ag = !(c->cfg.flags & MOESHARD_FLAG_SERIAL_AG);
+    // the side-stream token AllGather needs its own communicator (collective over the ranks:
+    // every rank's moeshard_init reaches this point); without ncclCommSplit it runs serially
+    c->overlap_ag = !(c->cfg.flags & MOESHARD_FLAG_SERIAL_AG) && nccl().CommSplit != nullptr;
+    if (c->overlap_ag) {
+      r = nccl().CommSplit(c->comm, 0, rank, &c->comm_x, nullptr);
+      if (r != ncclSuccess) {
+        moeshard_destroy(c);
+        return fail(nullptr, MOESHARD_ERR_NCCL, "ncclCommSplit: %s", nccl().GetErrorString(r));
+      }
+    }
     if (c->overlap_ag &&
         (cudaStreamCreateWithFlags(&c->s_x, cudaStreamNonBlocking) != cudaSuccess ||
          cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -985,6 +1001,7 @@ int moeshard_check(moeshard_ctx* c, void* stream) {
 
 int moeshard_destroy(moeshard_ctx* c) {
   if (!c) return MOESHARD_OK;
+  if (c->comm_x && nccl().ok) nccl().CommDestroy(c->comm_x);
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
   cudaSetDevice(c->device);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
