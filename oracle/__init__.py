@@ -24,7 +24,10 @@ Readings of the paper (R1-R19) used here:
   R4  argmax ties -> lowest expert index;
   R12 error metric max|y - y_ref| / max|y_ref|;
   R20 expert-parallel baseline: capacity ceil(CF n / |E|), CF = min(|E|, 50),
-      first-come admission per GPU, dropped tokens give a zero MoE output.
+      first-come admission per GPU, dropped tokens give a zero MoE output;
+  R21 top-k routing ("typically one or two" experts per token): the k
+      largest logits, ordered by logit then lowest index, gate g_tj = softmax(l_t)[e_tj]
+      (not renormalised: k = 1 is R2), y_t = sum_j g_tj FFN_{e_tj}(x_t).
 
 Parity status: every function below is pinned by a ``-m "not gpu"`` test in
 tests/test_oracle.py (worked examples under tests/golden/, closed forms,
@@ -43,6 +46,7 @@ __all__ = [
     "transfer_entries", "shard_storage_entries", "scatter_payload_bytes",
     "macs_per_rank", "max_abs_rel", "routing_margin", "Routing",
     "ep_capacity", "ep_admit", "moe_layer_ep",
+    "route_topk", "routing_margin_topk", "moe_layer_topk", "brute_force_layer_topk",
 ]
 
 
@@ -222,6 +226,98 @@ def moe_layer_tokens(x_rows, w_r, expert_weights, forced_rows=None):
         wi, wo = expert_weights(int(e))
         y[rows] = rt.gate[rows, None] * expert_ffn(x[rows], wi, wo)
     return y, rt
+
+
+# ---------------------------------------------------------------------------
+# top-k routing (R21)                    PAPER.md:85 ("typically one or two")
+# ---------------------------------------------------------------------------
+def route_topk(x, w_r, k: int) -> Routing:
+    """Step 1 with k experts per token (R21): expert [T,k] = the k largest logits in
+    descending order (ties: lowest index first), gate [T,k] = softmax(l_t)[e_tj]."""
+    x, w_r = _f64(x), _f64(w_r)
+    if x.ndim != 2 or w_r.ndim != 2 or x.shape[1] != w_r.shape[0]:
+        raise ValueError(f"route_topk: shape mismatch x{tuple(x.shape)} vs W_r{tuple(w_r.shape)}")
+    E = w_r.shape[1]
+    if not 1 <= k <= E:
+        raise ValueError(f"route_topk: k={k} not in [1, E={E}]")
+    logits = x @ w_r
+    T = x.shape[0]
+    # stable sort of -logit: equal logits keep ascending expert order
+    order = np.argsort(-logits, axis=1, kind="stable")[:, :k].astype(np.int64)
+    top = np.take_along_axis(logits, order, axis=1)
+    z = np.exp(logits - top[:, :1]).sum(axis=1, keepdims=True) if T else np.ones((0, 1))
+    gate = np.exp(top - top[:, :1]) / z
+    return Routing(order, gate, logits)
+
+
+def routing_margin_topk(logits: np.ndarray, k: int) -> np.ndarray:
+    """Smallest gap between consecutive logits among the k + 1 largest of each token (the
+    expert set and its order are decided at these gaps; inf when E <= 1)."""
+    E = logits.shape[1]
+    if E < 2:
+        return np.full(logits.shape[0], np.inf)
+    s = -np.sort(-logits, axis=1)[:, :min(k + 1, E)]
+    return np.min(s[:, :-1] - s[:, 1:], axis=1)
+
+
+def moe_layer_topk(x, w_r, w_i, w_o, k: int, return_routing: bool = False):
+    """Top-k MoE FFN (R21): y_t = sum_j g_tj relu(x_t W_i^{e_tj}) W_o^{e_tj}.
+
+    The k (token, expert) assignments of token t are numbered a = t k + j; Step 2 groups
+    the assignments per expert (stable in a), each expert runs once over its group, and the
+    results are summed per token. Returns (y, routing, counts, offsets, perm over a)."""
+    x = _f64(x)
+    w_i, w_o = _f64(w_i), _f64(w_o)
+    E = w_i.shape[0]
+    rt = route_topk(x, w_r, k)
+    T = x.shape[0]
+    counts, offsets, perm = group_per_expert(rt.expert.reshape(-1), E)
+    y = np.zeros_like(x)
+    g = rt.gate.reshape(-1)
+    for e in range(E):
+        a = perm[offsets[e]:offsets[e + 1]]
+        if a.size == 0:
+            continue
+        t = a // k
+        np.add.at(y, t, g[a, None] * expert_ffn(x[t], w_i[e], w_o[e]))
+    if return_routing:
+        return y, rt, counts, offsets, perm
+    return y
+
+
+def brute_force_layer_topk(x, w_r, w_i, w_o, k: int):
+    """Per token, pure Python: logits by explicit sums, the k largest by repeated scans
+    (strictly larger wins, so ties keep the lowest index), explicit FFN loops, summed."""
+    import math
+    x = _f64(x).tolist()
+    w_r = _f64(w_r).tolist()
+    w_i = _f64(w_i).tolist()
+    w_o = _f64(w_o).tolist()
+    T, h = len(x), len(x[0]) if x else 0
+    E = len(w_i)
+    d_ff = len(w_i[0][0]) if E else 0
+    out = []
+    for t in range(T):
+        logits = [sum(x[t][kk] * w_r[kk][e] for kk in range(h)) for e in range(E)]
+        chosen = []
+        for _ in range(k):
+            best = -1
+            for e in range(E):
+                if e in chosen:
+                    continue
+                if best < 0 or logits[e] > logits[best]:
+                    best = e
+            chosen.append(best)
+        m = logits[chosen[0]]
+        z = sum(math.exp(logits[e] - m) for e in range(E))
+        row = [0.0] * h
+        for e in chosen:
+            g = math.exp(logits[e] - m) / z
+            hid = [max(0.0, sum(x[t][kk] * w_i[e][kk][j] for kk in range(h))) for j in range(d_ff)]
+            for c in range(h):
+                row[c] += g * sum(hid[j] * w_o[e][j][c] for j in range(d_ff))
+        out.append(row)
+    return np.array(out, dtype=np.float64).reshape(T, h)
 
 
 # ---------------------------------------------------------------------------

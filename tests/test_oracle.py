@@ -387,3 +387,69 @@ def test_ep_per_rank_load_under_pathological_routing():
     st2 = {}
     O.moe_layer_sharded(xs, inp.w_r, inp.w_i, inp.w_o, forced_per_gpu=fs, stats=st2)
     assert len(set(st2["macs_per_rank"])) == 1
+
+
+# ------------------------------------------------------------------ top-k routing (R21)
+def test_topk_k1_is_the_top1_layer():
+    x, w_r, w_i, w_o = _rand_layer(37, 6, 10, 5, seed=21)
+    y1 = O.moe_layer(x, w_r, w_i, w_o)
+    yk, rt, counts, offsets, perm = O.moe_layer_topk(x, w_r, w_i, w_o, 1, return_routing=True)
+    assert np.max(np.abs(y1 - yk)) <= 1e-12 * max(1.0, np.max(np.abs(y1)))
+    r1 = O.route(x, w_r)
+    assert np.array_equal(rt.expert[:, 0], r1.expert)
+    assert np.allclose(rt.gate[:, 0], r1.gate, rtol=0, atol=1e-15)
+
+
+def test_topk_all_experts_is_the_dense_softmax_mixture():
+    # k = E: every expert, weighted by its softmax probability (a closed form with no routing)
+    x, w_r, w_i, w_o = _rand_layer(9, 5, 7, 4, seed=22)
+    y = O.moe_layer_topk(x, w_r, w_i, w_o, 4)
+    logits = x @ w_r
+    p = np.exp(logits - logits.max(axis=1, keepdims=True))
+    p /= p.sum(axis=1, keepdims=True)
+    ref = np.zeros_like(x)
+    for e in range(4):
+        ref += p[:, e:e + 1] * (np.maximum(x @ w_i[e], 0.0) @ w_o[e])
+    assert np.max(np.abs(y - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_topk_layer_matches_brute_force(k):
+    x, w_r, w_i, w_o = _rand_layer(7, 4, 6, 5, seed=23 + k)
+    y = O.moe_layer_topk(x, w_r, w_i, w_o, k)
+    ref = O.brute_force_layer_topk(x, w_r, w_i, w_o, k)
+    assert np.max(np.abs(y - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_topk_routing_order_ties_gates_and_droplessness():
+    # planted logits: token 0 ties experts 1 and 3 at the top, token 1 has a clear order
+    x = np.eye(2)
+    w_r = np.array([[0.0, 2.0, 1.0, 2.0], [0.5, 3.0, 4.0, -1.0]])
+    rt = O.route_topk(x, w_r, 2)
+    assert rt.expert.tolist() == [[1, 3], [2, 1]]
+    for t in range(2):
+        l = x[t] @ w_r
+        p = np.exp(l - l.max()) / np.exp(l - l.max()).sum()
+        assert np.allclose(rt.gate[t], p[rt.expert[t]], rtol=0, atol=1e-15)
+        assert rt.gate[t, 0] >= rt.gate[t, 1] and rt.gate[t].sum() <= 1.0
+    # every token keeps all k assignments (no capacity): counts sum to T k
+    x2, w_r2, w_i2, w_o2 = _rand_layer(50, 6, 8, 6, seed=31)
+    _, rt2, counts, _, perm = O.moe_layer_topk(x2, w_r2, w_i2, w_o2, 2, return_routing=True)
+    assert counts.sum() == 100 and sorted(perm.tolist()) == list(range(100))
+    assert all(len(set(r)) == 2 for r in rt2.expert.tolist())
+    m = O.routing_margin_topk(rt2.logits, 2)
+    s = -np.sort(-rt2.logits, axis=1)
+    assert np.allclose(m, np.minimum(s[:, 0] - s[:, 1], s[:, 1] - s[:, 2]))
+
+
+def test_topk_expert_shards_sum_to_the_unsharded_layer():
+    # the MoEShard identity does not depend on the routing: the layer on
+    # each GPU's column / row shard of every expert sums to the unsharded top-2 layer
+    x, w_r, w_i, w_o = _rand_layer(40, 8, 16, 6, seed=41)
+    full = O.moe_layer_topk(x, w_r, w_i, w_o, 2)
+    for G in (2, 4):
+        acc = np.zeros_like(full)
+        for g in range(G):
+            wi_g, wo_g = O.extract_shard(w_i, w_o, g, G)
+            acc += O.moe_layer_topk(x, w_r, wi_g, wo_g, 2)
+        assert np.max(np.abs(acc - full)) <= 1e-12 * np.max(np.abs(full))
