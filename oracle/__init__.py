@@ -231,9 +231,10 @@ def moe_layer_tokens(x_rows, w_r, expert_weights, forced_rows=None):
 # ---------------------------------------------------------------------------
 # top-k routing (R21)                    PAPER.md:85 ("typically one or two")
 # ---------------------------------------------------------------------------
-def route_topk(x, w_r, k: int) -> Routing:
+def route_topk(x, w_r, k: int, forced=None) -> Routing:
     """Step 1 with k experts per token (R21): expert [T,k] = the k largest logits in
-    descending order (ties: lowest index first), gate [T,k] = softmax(l_t)[e_tj]."""
+    descending order (ties: lowest index first), gate [T,k] = softmax(l_t)[e_tj]. With
+    ``forced`` [T,k] the experts are taken from the input (gates still softmax(l_t)[e])."""
     x, w_r = _f64(x), _f64(w_r)
     if x.ndim != 2 or w_r.ndim != 2 or x.shape[1] != w_r.shape[0]:
         raise ValueError(f"route_topk: shape mismatch x{tuple(x.shape)} vs W_r{tuple(w_r.shape)}")
@@ -242,11 +243,17 @@ def route_topk(x, w_r, k: int) -> Routing:
         raise ValueError(f"route_topk: k={k} not in [1, E={E}]")
     logits = x @ w_r
     T = x.shape[0]
-    # stable sort of -logit: equal logits keep ascending expert order
-    order = np.argsort(-logits, axis=1, kind="stable")[:, :k].astype(np.int64)
+    if forced is None:
+        # stable sort of -logit: equal logits keep ascending expert order
+        order = np.argsort(-logits, axis=1, kind="stable")[:, :k].astype(np.int64)
+    else:
+        order = np.asarray(forced, dtype=np.int64).reshape(T, k)
+        if order.size and (order.min() < 0 or order.max() >= E):
+            raise IndexError("route_topk: forced expert id out of range")
     top = np.take_along_axis(logits, order, axis=1)
-    z = np.exp(logits - top[:, :1]).sum(axis=1, keepdims=True) if T else np.ones((0, 1))
-    gate = np.exp(top - top[:, :1]) / z
+    m = logits.max(axis=1, keepdims=True) if T else np.zeros((0, 1))
+    z = np.exp(logits - m).sum(axis=1, keepdims=True) if T else np.ones((0, 1))
+    gate = np.exp(top - m) / z
     return Routing(order, gate, logits)
 
 
@@ -260,7 +267,7 @@ def routing_margin_topk(logits: np.ndarray, k: int) -> np.ndarray:
     return np.min(s[:, :-1] - s[:, 1:], axis=1)
 
 
-def moe_layer_topk(x, w_r, w_i, w_o, k: int, return_routing: bool = False):
+def moe_layer_topk(x, w_r, w_i, w_o, k: int, return_routing: bool = False, forced=None):
     """Top-k MoE FFN (R21): y_t = sum_j g_tj relu(x_t W_i^{e_tj}) W_o^{e_tj}.
 
     The k (token, expert) assignments of token t are numbered a = t k + j; Step 2 groups
@@ -269,8 +276,7 @@ def moe_layer_topk(x, w_r, w_i, w_o, k: int, return_routing: bool = False):
     x = _f64(x)
     w_i, w_o = _f64(w_i), _f64(w_o)
     E = w_i.shape[0]
-    rt = route_topk(x, w_r, k)
-    T = x.shape[0]
+    rt = route_topk(x, w_r, k, forced)
     counts, offsets, perm = group_per_expert(rt.expert.reshape(-1), E)
     y = np.zeros_like(x)
     g = rt.gate.reshape(-1)

@@ -427,6 +427,8 @@ def test_topk_routing_order_ties_gates_and_droplessness():
     w_r = np.array([[0.0, 2.0, 1.0, 2.0], [0.5, 3.0, 4.0, -1.0]])
     rt = O.route_topk(x, w_r, 2)
     assert rt.expert.tolist() == [[1, 3], [2, 1]]
+    rf = O.route_topk(x, w_r, 2, forced=rt.expert)     # the replaced-router hook
+    assert np.array_equal(rf.gate, rt.gate) and np.array_equal(rf.expert, rt.expert)
     for t in range(2):
         l = x[t] @ w_r
         p = np.exp(l - l.max()) / np.exp(l - l.max()).sum()
