@@ -121,6 +121,12 @@ typedef struct {
   int32_t dtype;               /* moeshard_dtype */
   uint32_t flags;              /* MOESHARD_FLAG_* */
   float ep_capacity_factor;    /* MOESHARD_FLAG_EXPERT_PARALLEL only: CF (<= 0: min(E, 50)) */
+  int32_t top_k;               /* experts per token (0 or 1: Switch top-1; 2: top-2 - PAPER.md:85
+                                * "typically one or two" - the 2 largest logits, each weighted by
+                                * its softmax probability, the two expert outputs summed, reading
+                                * R21). top_k = 2 needs bf16 and the fused tcgen05 path (no P2P,
+                                * EP, UNEVEN_TOKENS, SIMT/UNFUSED/LAUNCH_* or ONCHIP_H), and
+                                * moeshard_forward's forced_expert then [n_local*2]. */
 } moeshard_config;
 
 typedef struct moeshard_ctx moeshard_ctx;
@@ -192,6 +198,8 @@ int moeshard_forward(moeshard_ctx* ctx, int layer, const void* hidden, int n_loc
 
 /* Routing of the most recent forward (Steps 1-2), copied on `stream` into
  * caller device buffers (any may be NULL):
+ *   (top_k = 2: one entry per (token, choice) assignment a = 2 t + j, j = 0 the larger logit:
+ *    expert_all / gate_all / perm have world*n_local*2 entries, perm lists assignment ids)
  *   expert_all [dev] int32 [world*n_local]  e_t for all global tokens t = r*n + i
  *              (MOESHARD_FLAG_UNEVEN_TOKENS: [world*max_tokens_per_rank], t = r*cap + i,
  *              -1 where slot r has no token i; gate_all / perm likewise)

@@ -122,10 +122,14 @@ void launch_router(int dtype, const void* x, int n, int h, const void* w_r, int 
 void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int32_t* tot,
                          Tables tb, int n_mt_up_tc, int n_mt_down_tc, const RouteRec* route,
                          const void* x_all, int n, int nbr, int HB, int row_bytes, int32_t* perm,
-                         void* x_perm, cudaStream_t s);
+                         void* x_perm, cudaStream_t s, int top_k = 1);
 
 void launch_transpose(int dtype, const void* src, void* dst, int batch, int rows, int cols,
                       cudaStream_t s);
+
+// top_k > 1 (bf16): y[t] = sum_{j < K} y_assign[K t + j] over the n_tok tokens (rows of row_bytes).
+void launch_combine_assignments(const void* y_assign, void* y, int n_tok, int row_bytes, int K,
+                                int num_sms, cudaStream_t s);
 
 // SIMT grouped GEMMs (fp32 validation mode, and bf16 ablation).
 void launch_simt_up(int dtype, const void* x_perm, const void* wt_in, int K, int F, int E, Tables tb,

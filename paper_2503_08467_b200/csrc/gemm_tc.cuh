@@ -51,7 +51,7 @@ size_t router_tc_smem_bytes(int EP, bool mn_major);
 cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
                              const void* w_r, void* wt_r, int n, int h, int E, int EP,
                              const int32_t* forced, RouteRec* out, int32_t* hist_out,
-                             int32_t* err_flag, cudaStream_t s);
+                             int32_t* err_flag, cudaStream_t s, int top_k = 1);
 
 // grid = number of persistent CTAs (normally the SM count).
 //   tmA:  packed weight tiles as a [rows][64] bf16 tensor, box {64, 128}, no swizzle

@@ -136,6 +136,7 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 // Workspace carve-up, shared by moeshard_workspace_size and moeshard_init.
 struct Layout {
   size_t wt_r, route, block_hist, block_base, ints, done, perm, perm_pad, gate_pad, x_all, x_perm, H, partial,
+      y_assign,
       ep_route, ep_hist, ep_owner, total;
   int n_ints;
   size_t npad;   // rows of the internal expert-ordered layout: N_max + 32 per expert, rounded to 64
@@ -146,6 +147,8 @@ Layout make_layout(const moeshard_config& c, int world) {
   const bool coll = !p2p && (world > 1 || (c.flags & MOESHARD_FLAG_FORCE_COLLECTIVES));
   const size_t elt = c.dtype == MOESHARD_BF16 ? 2 : 4;
   const size_t Nmax = static_cast<size_t>(world) * c.max_tokens_per_rank;
+  const size_t K = c.top_k > 1 ? static_cast<size_t>(c.top_k) : 1;   // assignments per token
+  const size_t Amax = Nmax * K;
   // hist-blocks: >= 64 tokens each (128 for the tcgen05 router), per rank
   const size_t nb = std::max<size_t>(1, world * ((c.max_tokens_per_rank + 63) / 64));
   const bool ep = (c.flags & MOESHARD_FLAG_EXPERT_PARALLEL) != 0;
@@ -158,22 +161,23 @@ Layout make_layout(const moeshard_config& c, int world) {
     return o;
   };
   L.wt_r = take(static_cast<size_t>(round_up(c.n_experts, 16)) * h * elt);  // W_r^T, padded
-  L.route = take(Nmax * sizeof(RouteRec));
+  L.route = take(Amax * sizeof(RouteRec));
   L.block_hist = take(nb * E * 4);
   L.block_base = take(nb * E * 4);
   // counts, offsets, tc_chunk_pref, tc_chunk_size, simt_chunk_pref, stats[8], block_tot, pos,
   // next_unit
   L.n_ints = static_cast<int>(E + (E + 1) + (E + 1) + E + (E + 1) + 8 + E + (E + 1) + 1);
-  L.npad = (Nmax + kSegAlign * E + 63) / 64 * 64;
+  L.npad = (Amax + kSegAlign * E + 63) / 64 * 64;
   L.ints = take(L.n_ints * 4);
-  L.done = take((Nmax / kTcTokTile + E + 8) * 4);   // per token chunk: <= N/256 + E chunks
-  L.perm = take(Nmax * 4);
+  L.done = take((Amax / kTcTokTile + E + 8) * 4);   // per token chunk: <= A/256 + E chunks
+  L.perm = take(Amax * 4);
   L.perm_pad = take(L.npad * 4);
   L.gate_pad = take(L.npad * 4);
   L.x_all = coll ? take(Nmax * h * elt) : 0;
   L.x_perm = take(L.npad * h * elt);
   L.H = take(L.npad * F * elt);
   L.partial = coll ? take(Nmax * h * elt) : 0;
+  L.y_assign = K > 1 ? take(Amax * h * elt) : 0;   // top-k: one output row per assignment
   // EP baseline: this rank's own routing (the regions carry the hosts' copies)
   const size_t nmax = static_cast<size_t>(c.max_tokens_per_rank);
   L.ep_route = ep ? take(nmax * sizeof(RouteRec)) : 0;
@@ -210,6 +214,8 @@ struct moeshard_ctx {
   int32_t *block_hist = nullptr, *block_base = nullptr, *block_tot = nullptr, *perm = nullptr;
   Tables tb{};
   void *x_all = nullptr, *x_perm = nullptr, *H = nullptr, *partial = nullptr;
+  int K = 1;                    // top_k: (token, expert) assignments per token
+  void* y_assign = nullptr;     // top_k > 1: [A_max][h] one output row per assignment
   CUtensorMap tm_xperm{}, tm_H{}, tm_xperm16{}, tm_H16{}, tm_xperm128{}, tm_wt_r{};
   void* wt_r = nullptr;
   int EP = 16;
@@ -331,6 +337,18 @@ int validate(const moeshard_config* c, int world) {
                 "MOESHARD_FLAG_EXPERT_PARALLEL needs MOESHARD_FLAG_P2P, E %% world == 0 and d_ff %% 128 "
                 "== 0 (E=%d, world=%d, d_ff=%d)", c->n_experts, world, c->d_ff);
   if (c->n_layers < 1) return fail(nullptr, MOESHARD_ERR_CONFIG, "n_layers=%d < 1", c->n_layers);
+  if (c->top_k < 0 || c->top_k > 2 || c->top_k > c->n_experts)
+    return fail(nullptr, MOESHARD_ERR_CONFIG, "top_k=%d not in {0, 1, 2} or > n_experts=%d",
+                c->top_k, c->n_experts);
+  if (c->top_k == 2 &&
+      (c->dtype != MOESHARD_BF16 ||
+       (c->flags & (MOESHARD_FLAG_P2P | MOESHARD_FLAG_EXPERT_PARALLEL | MOESHARD_FLAG_UNEVEN_TOKENS |
+                    MOESHARD_FLAG_SIMT_GEMM | MOESHARD_FLAG_UNFUSED_GEMM |
+                    MOESHARD_FLAG_LAUNCH_PER_EXPERT | MOESHARD_FLAG_LAUNCH_PER_SOURCE |
+                    MOESHARD_FLAG_ONCHIP_H))))
+    return fail(nullptr, MOESHARD_ERR_CONFIG,
+                "top_k=2 needs bf16 and the fused tcgen05 path (no P2P / EXPERT_PARALLEL / "
+                "UNEVEN_TOKENS / SIMT_GEMM / UNFUSED_GEMM / LAUNCH_* / ONCHIP_H)");
   if (c->flags & ~kKnownFlags)
     return fail(nullptr, MOESHARD_ERR_INVALID_ARG, "flags=0x%x has unknown bits (0x%x)", c->flags,
                 c->flags & ~kKnownFlags);
@@ -480,6 +498,8 @@ int moeshard_init(moeshard_ctx** out, const moeshard_config* cfg, int rank, int 
   c->x_perm = c->ws + L.x_perm;
   c->H = c->ws + L.H;
   c->partial = c->coll && !c->p2p ? c->ws + L.partial : nullptr;
+  c->K = cfg->top_k > 1 ? cfg->top_k : 1;
+  c->y_assign = c->K > 1 ? c->ws + L.y_assign : nullptr;
   if (c->ep) {
     c->ep_route = reinterpret_cast<RouteRec*>(c->ws + L.ep_route);
     c->ep_hist = reinterpret_cast<int32_t*>(c->ws + L.ep_hist);
@@ -661,7 +681,8 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   }
   // Step 1: route local tokens
   // (EP: the router's output stays in the workspace; the dispatch writes the hosts' copies)
-  RouteRec* my_route = c->ep ? c->ep_route : c->route + (c->coll ? static_cast<size_t>(c->rank) * ns : 0);
+  RouteRec* my_route =
+      c->ep ? c->ep_route : c->route + (c->coll ? static_cast<size_t>(c->rank) * ns * c->K : 0);
   // tokens per hist-block = tokens per router CTA (128 for the tcgen05 router, 64 for SIMT)
   const int HB = c->use_tc ? kRouterTok : 64;
   const int nbr_own = (n + HB - 1) / HB;                // hist-blocks this rank's router fills
@@ -681,7 +702,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
         (mn && !make_tmap(&tm_w, router_w, E, h, 64)))
       return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden/router_w");
     CUDA_TRY(c, launch_router_tc(tm_x, mn ? tm_w : c->tm_wt_r, mn, router_w, c->wt_r, n, h, E,
-                                 c->EP, forced, my_route, my_hist, err_flag, s));
+                                 c->EP, forced, my_route, my_hist, err_flag, s, c->K));
     c->launches += mn ? 1 : 2;
   } else {
     launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, my_hist, err_flag, s);
@@ -711,7 +732,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   } else if (st_route && c->coll) {
     if (!ag_x_side) CUDA_TRY_RET(c, allgather_tokens(c, hidden, n, ns, uneven, ndt, s));
     NCCL_TRY(c, nccl().GroupStart());
-    NCCL_TRY(c, nccl().AllGather(my_route, c->route, static_cast<size_t>(ns) * 2, ncclInt32,
+    NCCL_TRY(c, nccl().AllGather(my_route, c->route, static_cast<size_t>(ns) * 2 * c->K, ncclInt32,
                                  c->comm, s));
     NCCL_TRY(c, nccl().AllGather(my_hist, c->block_hist, static_cast<size_t>(nbr) * E, ncclInt32,
                                  c->comm, s));
@@ -727,7 +748,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     // Step 2 grouping + Sec. 3.3 per-expert concatenation across GPUs
     launch_group_blocks(c->block_hist, NB, Et, c->block_base, c->block_tot, c->tb,
                         F / kTcFeatTile, h / kTcFeatTile, c->route, x_all, ns, nbr, HB,
-                        h * c->elt, c->perm, c->x_perm, s);
+                        h * c->elt, c->perm, c->x_perm, s, c->K);
     c->launches += 2;
     c->mark(3, s);
     // Step 4: expert computation, one grouped product per projection
@@ -750,13 +771,20 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     } else if (fused) {
       TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), Et, c->tb,
                   static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
+      // top_k > 1: each (token, expert) assignment's row goes to y_assign, summed per token below
       TcParams dn{F, h / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_out), Et, c->tb,
-                  static_cast<__nv_bfloat16*>(P), h, c->tb.perm_pad, c->route};
+                  static_cast<__nv_bfloat16*>(c->K > 1 ? c->y_assign : P), h, c->tb.perm_pad,
+                  c->route};
       dn.gate_pad = c->tb.gate_pad;
       if (c->p2p) set_p2p_out(c, dn, ns);
       CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, c->tm_xperm16, lw.tm_out, c->tm_H16, up, dn,
                                     c->tb.done, (c->cfg.flags & MOESHARD_FLAG_DYNAMIC_SCHED) != 0,
                                     /*early_tables=*/n > 0 && !c->ep, c->num_sms, s));
+      if (c->K > 1) {   // y[t] = sum_j y_assign[K t + j] (R21); rank-major rows of all ranks
+        launch_combine_assignments(c->y_assign, P, (c->coll ? c->world : 1) * ns, h * c->elt, c->K,
+                                   c->num_sms, s);
+        c->launches += 1;
+      }
       c->mark(4, s);
       c->launches += 1;
       if (c->p2p) {
@@ -890,7 +918,7 @@ int moeshard_get_routing(moeshard_ctx* c, int32_t* expert_all, float* gate_all, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool uneven = c->coll && (c->cfg.flags & (MOESHARD_FLAG_UNEVEN_TOKENS | MOESHARD_FLAG_EXPERT_PARALLEL));
   const size_t N = static_cast<size_t>(c->coll ? c->world : 1) *
-                   (uneven ? c->cfg.max_tokens_per_rank : c->last_n);
+                   (uneven ? c->cfg.max_tokens_per_rank : c->last_n) * c->K;   // assignments
   if (N > 0) {
     if (expert_all)
       CUDA_TRY(c, cudaMemcpy2DAsync(expert_all, 4, &c->route[0].expert, sizeof(RouteRec), 4, N,

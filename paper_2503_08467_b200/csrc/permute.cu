@@ -91,25 +91,29 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     const int32_t* __restrict__ bbase, const int32_t* __restrict__ btot, int E, Tables tb,
     int n_mt_up_tc, int n_mt_down_tc, const RouteRec* __restrict__ route,
     const uint4* __restrict__ x_all, int n, int nbr, int HB, int32_t* __restrict__ perm,
-    int row_vecs, uint4* __restrict__ x_perm, int NB) {
+    int row_vecs, uint4* __restrict__ x_perm, int NB, int K) {
+  // K = top_k: a block of HB tokens holds HB K (token, expert) assignments a = K t + j
+  // (route records, histograms and the expert-ordered rows are per assignment)
   if (threadIdx.x == 0) TL_MIN(1);
   constexpr int kThreads = 1024 / kSplit;
   constexpr int kRowsPerWarp = 4;                 // rows copied per warp
   constexpr int kColBlock = VPL * 32;             // 16-B vectors per column block
-  static_assert(kThreads >= 128, "ranks need 128 threads");
+  static_assert(kThreads >= 256, "ranks need 128 K threads (K <= 2)");
+  static_assert(kRowsPerWarp * (kThreads / 32) == 128 / kSplit, "one row group = 128 / kSplit rows");
   __shared__ int32_t s_tot[kMaxExperts];
   __shared__ int32_t s_pre[kMaxExperts];
   __shared__ int32_t s_base[kMaxExperts];   // compact (public perm) position of this block's first e
   __shared__ int32_t s_bpad[kMaxExperts];   // padded internal position
-  __shared__ int32_t whist[4][kMaxExperts];
-  __shared__ int32_t s_j[128];
+  __shared__ int32_t whist[8][kMaxExperts];
+  __shared__ int32_t s_j[256];
   __shared__ int32_t s_warp[5 * (kThreads / 32)];   // segment_tables' warp totals
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x / kSplit, part = blockIdx.x % kSplit;
   const int r = b / nbr, i = b - r * nbr;
   const int t0 = r * n + i * HB;
   const int t1 = min(t0 + HB, (r + 1) * n);
-  const int row_base = part * (128 / kSplit);     // this CTA's rows of the block
+  const int a0 = t0 * K, na = (t1 - t0) * K;     // the block's assignments
+  const int row_base = part * (128 * K / kSplit); // this CTA's assignment rows of the block
   // Everything that needs only the routing runs before the wait for the block scan: this
   // grid is launched once the scan has passed its own wait, so the route records and token
   // rows (router, AllGather or peer pushes, all before the scan) are complete. The stable
@@ -121,33 +125,35 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   uint4 v[kRowsPerWarp][VPL];
 #pragma unroll
   for (int u = 0; u < kRowsPerWarp; ++u) {
-    const int tt = has_block ? t0 + row_base + warp * kRowsPerWarp + u : t1;
+    const int q = row_base + warp * kRowsPerWarp + u;   // assignment row of the block
+    const int tt = has_block && q < na ? t0 + q / K : t1;
 #pragma unroll
     for (int c = 0; c < VPL; ++c) {
       const int col = lane + 32 * c;
       if (tt < t1 && col < row_vecs) v[u][c] = __ldg(x_all + (size_t)tt * row_vecs + col);
     }
   }
-  int e = -1, rank_w = 0, t = 0;
+  const int rank_warps = 4 * K;                   // warps holding one assignment per thread
+  int e = -1, rank_w = 0, a = 0;
   float gate = 0.f;
-  if (warp < 4 && has_block) {
-    t = t0 + threadIdx.x;
-    if (t < t1) {
-      const RouteRec rec = route[t];
+  if (warp < rank_warps && has_block) {
+    a = a0 + threadIdx.x;
+    if (threadIdx.x < na) {
+      const RouteRec rec = route[a];
       e = rec.expert;
       gate = rec.gate;
     }
   }
-  for (int k = threadIdx.x; k < 4 * E; k += kThreads) whist[k / E][k % E] = 0;
+  for (int k = threadIdx.x; k < rank_warps * E; k += kThreads) whist[k / E][k % E] = 0;
   __syncthreads();
-  // 2. stable ranks inside the block
-  if (warp < 4) {
+  // 2. stable ranks inside the block (assignment order)
+  if (warp < rank_warps) {
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     rank_w = __popc(peers & lanemask_lt());
     if (e >= 0 && rank_w == 0) whist[warp][e] = __popc(peers);
   }
   __syncthreads();
-  if (warp < 4 && e >= 0)
+  if (warp < rank_warps && e >= 0)
     for (int w = 0; w < warp; ++w) rank_w += whist[w][e];   // rank inside the block
   ptx::griddep_wait();            // the block scan (base, tot)
   ptx::griddep_launch_dependents();   // the FFN's prologue may start now
@@ -166,13 +172,13 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     if (threadIdx.x == 0) ptx::st_release_gpu(tb.stats + 6, 1);
     if (threadIdx.x == 0) { TL_MIN(2); TL_MAX(2); }
   }
-  if (warp < 4) {
+  if (warp < rank_warps) {
     if (e >= 0) {
       const int j = s_base[e] + rank_w;         // public, compact
       const int jp = s_bpad[e] + rank_w;        // internal, padded segments
       if (part == 0) {
-        perm[j] = t;
-        tb.perm_pad[jp] = t;
+        perm[j] = a;                            // global token id (K = 1) / assignment id
+        tb.perm_pad[jp] = a;
         tb.gate_pad[jp] = gate;   // the down epilogue reads row and gate without an indirection
       }
       s_j[threadIdx.x] = jp;
@@ -184,9 +190,26 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   // 3. row stores (first column block loaded at the top)
   if (threadIdx.x == 0) { TL_MIN(6); TL_MAX(6); }
   if (x_perm == nullptr || !has_block) return;
+  for (int g = 0; g < K; ++g) {   // groups of 32 assignment rows (kRowsPerWarp x 8 warps)
+  const int gbase = row_base + g * kRowsPerWarp * (kThreads / 32);
+  if (g > 0) {
+#pragma unroll
+    for (int u = 0; u < kRowsPerWarp; ++u) {
+      const int q = gbase + warp * kRowsPerWarp + u;
+      const int tt = q < na ? t0 + q / K : t1;
+#pragma unroll
+      for (int c = 0; c < VPL; ++c) {
+        const int col = lane + 32 * c;
+        if (tt < t1 && col < row_vecs) v[u][c] = __ldg(x_all + (size_t)tt * row_vecs + col);
+      }
+    }
+  }
   int jj[kRowsPerWarp];
 #pragma unroll
-  for (int u = 0; u < kRowsPerWarp; ++u) jj[u] = s_j[row_base + warp * kRowsPerWarp + u];
+  for (int u = 0; u < kRowsPerWarp; ++u) {
+    const int q = gbase + warp * kRowsPerWarp + u;
+    jj[u] = q < na ? s_j[q] : -1;
+  }
 #pragma unroll
   for (int u = 0; u < kRowsPerWarp; ++u)
 #pragma unroll
@@ -197,7 +220,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   for (int c0 = kColBlock; c0 < row_vecs; c0 += kColBlock) {   // rows wider than one block
 #pragma unroll
     for (int u = 0; u < kRowsPerWarp; ++u) {
-      const int tt = t0 + row_base + warp * kRowsPerWarp + u;
+      const int tt = t0 + (gbase + warp * kRowsPerWarp + u) / K;
 #pragma unroll
       for (int c = 0; c < VPL; ++c) {
         const int col = c0 + lane + 32 * c;
@@ -212,6 +235,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
         if (jj[u] >= 0 && col < row_vecs) x_perm[(size_t)jj[u] * row_vecs + col] = v[u][c];
       }
   }
+  }   // groups
   if (threadIdx.x == 0) TL_MAX(1);
 }
 
@@ -222,7 +246,7 @@ TL_EXPORT(moeshard_tl_group)
 void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int32_t* tot,
                          Tables tb, int n_mt_up_tc, int n_mt_down_tc, const RouteRec* route,
                          const void* x_all, int n, int nbr, int HB, int row_bytes, int32_t* perm,
-                         void* x_perm, cudaStream_t s) {
+                         void* x_perm, cudaStream_t s, int K) {
   if (NB <= 0) return;
   launch_pdl(group_block_scan, dim3(E), dim3(128), 0, s, hist, NB, E, base, tot);
   const int row_vecs = row_bytes / 16;
@@ -237,7 +261,7 @@ void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int3
   constexpr int kSp = MOESHARD_GROUP_SPLIT;
 #define SG(V)                                                                                  \
   launch_pdl(group_scatter_gather<V, kSp>, dim3(NB * kSp), dim3(1024 / kSp), 0, s, base, tot, E, tb, \
-             n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm, row_vecs, xd, NB)
+             n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm, row_vecs, xd, NB, K)
   switch (vpl) {
     case 1: SG(1); break;
     case 2: SG(2); break;
@@ -247,6 +271,48 @@ void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int3
     default: SG(8); break;
   }
 #undef SG
+}
+
+namespace {
+// top_k > 1: the token's output is the sum of its K assignments' gate-scaled expert rows
+// (R21), y[t] = sum_j y_assign[K t + j], fp32 sum, one bf16 rounding; 8 features per thread.
+__global__ void __launch_bounds__(256) combine_assignments(const uint4* __restrict__ ya,
+                                                           uint4* __restrict__ y, int n_tok,
+                                                           int vecs, int K) {
+  ptx::griddep_wait();   // the FFN's down epilogue wrote ya
+  ptx::griddep_launch_dependents();
+  const long long total = static_cast<long long>(n_tok) * vecs;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long t = q / vecs, c = q - t * vecs;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < K; ++j) {
+      const uint4 v = __ldcg(ya + (t * K + j) * vecs + c);
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(p[i]);
+        acc[2 * i] += f.x;
+        acc[2 * i + 1] += f.y;
+      }
+    }
+    uint4 o;
+    __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) po[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+    y[t * vecs + c] = o;
+  }
+}
+}  // namespace
+
+void launch_combine_assignments(const void* y_assign, void* y, int n_tok, int row_bytes, int K,
+                                int num_sms, cudaStream_t s) {
+  if (n_tok <= 0) return;
+  const int vecs = row_bytes / 16;
+  const long long total = static_cast<long long>(n_tok) * vecs;
+  const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 4LL * num_sms));
+  launch_pdl(combine_assignments, dim3(grid), dim3(256), 0, s, static_cast<const uint4*>(y_assign),
+             static_cast<uint4*>(y), n_tok, vecs, K);
 }
 
 void launch_transpose(int dtype, const void* src, void* dst, int batch, int rows, int cols,

@@ -236,7 +236,9 @@ __global__ void router_transpose(const __nv_bfloat16* __restrict__ w_r, int h, i
 // otherwise B = the transposed copy [EP][h] (K-major).
 // One CTA = 128 tokens (one hist-block); 6 warps: 0-3 epilogue (thread = token =
 // TMEM lane), 4 TMA producer, 5 MMA issuer.
-template <bool kMN>
+// kK = 2 (top-2, reading R21): the two largest logits per token (ties: lowest index), two
+// records per token (out[2 t + j], j = 0 the larger), both counted in the histogram.
+template <bool kMN, int kK = 1>
 __global__ void __launch_bounds__(192, 1)
     router_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      int n, int h, int E, int EP, const int32_t* __restrict__ forced,
@@ -337,13 +339,20 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // epilogue: warps 0-3, thread = token (TMEM lane 32*warp + lane)
     const int t = tok0 + warp * 32 + lane;
-    int sel = -1;
+    int sel = -1, sel2 = -1;
     bool bad = false;
     if (forced != nullptr && t < n) {
-      sel = forced[t];
+      sel = forced[static_cast<size_t>(t) * kK];
       if (sel < 0 || sel >= E) {
         bad = true;
         sel = sel < 0 ? 0 : E - 1;
+      }
+      if (kK == 2) {
+        sel2 = forced[static_cast<size_t>(t) * kK + 1];
+        if (sel2 < 0 || sel2 >= E) {
+          bad = true;
+          sel2 = sel2 < 0 ? 0 : E - 1;
+        }
       }
     }
     mbar_wait(done, 0);
@@ -357,8 +366,10 @@ __global__ void __launch_bounds__(192, 1)
     // replaces the running argmax only with a strictly larger max, so ties across
     // chunks also resolve to the lowest index.
     constexpr float kLog2e = 1.4426950408889634f;
-    float best = -INFINITY, lsel = 0.f, sum = 0.f;
+    float best = -INFINITY, lsel = 0.f, lsel2 = 0.f, sum = 0.f;
     int best_e = 0;
+    float top1 = -INFINITY, top2 = -INFINITY;   // kK == 2: the two largest logits ...
+    int top1_e = 0, top2_e = 0;                 // ... and their experts (lowest index on ties)
     for (int c0 = 0; c0 < EP; c0 += 32) {
       uint32_t r[32];
       if (c0 + 16 < EP) {
@@ -394,6 +405,28 @@ __global__ void __launch_bounds__(192, 1)
         for (int j = 0; j < 32; ++j)
           if (c0 + j == sel) lsel = v[j];
       }
+      if (kK == 2) {
+        if (sel2 >= c0 && sel2 < c0 + 32) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j == sel2) lsel2 = v[j];
+        }
+        // insertion in scan order: only a strictly larger value displaces, so ties keep the
+        // lower expert index ahead
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float x = v[j];
+          if (x > top1) {
+            top2 = top1;
+            top2_e = top1_e;
+            top1 = x;
+            top1_e = c0 + j;
+          } else if (x > top2) {
+            top2 = x;
+            top2_e = c0 + j;
+          }
+        }
+      }
       if (cmax > best) {
         sum *= fast_exp2((best - cmax) * kLog2e);   // best = -inf on the first chunk -> 0
         best = cmax;
@@ -410,12 +443,23 @@ __global__ void __launch_bounds__(192, 1)
       }
       sum += (p0 + p1) + (p2 + p3);
     }
-    if (t < n) {
+    if (t < n && kK == 1) {
       RouteRec rec;
       rec.expert = sel >= 0 ? sel : best_e;
       rec.gate = (sel >= 0 ? fast_exp2((lsel - best) * kLog2e) : 1.f) / sum;
       out[t] = rec;
       atomicAdd(&s_hist[rec.expert], 1);
+      if (bad) atomicOr(err_flag, 1);
+    } else if (t < n) {
+      RouteRec r0, r1;
+      r0.expert = sel >= 0 ? sel : top1_e;
+      r1.expert = sel >= 0 ? sel2 : top2_e;
+      r0.gate = fast_exp2(((sel >= 0 ? lsel : top1) - best) * kLog2e) / sum;
+      r1.gate = fast_exp2(((sel >= 0 ? lsel2 : top2) - best) * kLog2e) / sum;
+      out[2 * static_cast<size_t>(t)] = r0;
+      out[2 * static_cast<size_t>(t) + 1] = r1;
+      atomicAdd(&s_hist[r0.expert], 1);
+      atomicAdd(&s_hist[r1.expert], 1);
       if (bad) atomicOr(err_flag, 1);
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");  // the epilogue warps
@@ -439,32 +483,46 @@ size_t router_tc_smem_bytes(int EP, bool mn) {
   return 1024 + st * (a + b) + (2 * st + 1) * 8 + 16;
 }
 
-cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
-                             const void* w_r, void* wt_r, int n, int h, int E, int EP,
-                             const int32_t* forced, RouteRec* out, int32_t* hist_out,
-                             int32_t* err_flag, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
+namespace {
+template <int kK>
+cudaError_t launch_router_tc_k(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
+                               const void* w_r, void* wt_r, int n, int h, int E, int EP,
+                               const int32_t* forced, RouteRec* out, int32_t* hist_out,
+                               int32_t* err_flag, cudaStream_t s) {
   static PerDeviceOnce attr;
   if (attr.need()) {
-    cudaError_t e = cudaFuncSetAttribute(router_tc_kernel<true>,
+    cudaError_t e = cudaFuncSetAttribute(router_tc_kernel<true, kK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          RTC_SMEM_BUDGET + 2048);  // >= router_tc_smem_bytes(any EP)
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(router_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               RTC_SMEM_BUDGET + 2048);
+      e = cudaFuncSetAttribute(router_tc_kernel<false, kK>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, RTC_SMEM_BUDGET + 2048);
     if (e != cudaSuccess) return e;
     attr.done();
   }
   const dim3 grid(ceil_div(n, RTC_TOK));
   if (mn_major)
-    return launch_pdl(router_tc_kernel<true>, grid, dim3(192), router_tc_smem_bytes(EP, true), s,
-                      tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
+    return launch_pdl(router_tc_kernel<true, kK>, grid, dim3(192), router_tc_smem_bytes(EP, true),
+                      s, tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
   dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
   router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,
                                      static_cast<__nv_bfloat16*>(wt_r));
-  router_tc_kernel<false><<<grid, 192, router_tc_smem_bytes(EP, false), s>>>(
+  router_tc_kernel<false, kK><<<grid, 192, router_tc_smem_bytes(EP, false), s>>>(
       tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
+                             const void* w_r, void* wt_r, int n, int h, int E, int EP,
+                             const int32_t* forced, RouteRec* out, int32_t* hist_out,
+                             int32_t* err_flag, cudaStream_t s, int top_k) {
+  if (n <= 0) return cudaSuccess;
+  if (top_k == 2)
+    return launch_router_tc_k<2>(tmX, tmW, mn_major, w_r, wt_r, n, h, E, EP, forced, out, hist_out,
+                                 err_flag, s);
+  return launch_router_tc_k<1>(tmX, tmW, mn_major, w_r, wt_r, n, h, E, EP, forced, out, hist_out,
+                               err_flag, s);
 }
 
 }  // namespace moeshard

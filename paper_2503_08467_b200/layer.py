@@ -53,11 +53,13 @@ class MoEShardLayer:
     def __init__(self, d_model: int, d_ff: int, n_experts: int, *, n_layers: int = 1,
                  max_tokens_per_rank: int, dtype=torch.bfloat16, rank: int = 0, world: int = 1,
                  device: Optional[int] = None, flags: int = 0, group=None,
-                 ep_capacity_factor: float = 0.0):
+                 ep_capacity_factor: float = 0.0, top_k: int = 1):
         """flags & MOESHARD_FLAG_EXPERT_PARALLEL builds the paper's expert-parallel baseline
         instead (needs MOESHARD_FLAG_P2P): this rank then hosts experts
         [rank*E/world, (rank+1)*E/world) whole, and load_expert_shards takes
-        [E/world, h, d_ff] / [E/world, d_ff, h]; ep_capacity_factor <= 0 means min(E, 50)."""
+        [E/world, h, d_ff] / [E/world, d_ff, h]; ep_capacity_factor <= 0 means min(E, 50).
+        top_k = 2: two experts per token (R21); routing tables then have one entry per
+        (token, choice) assignment and forced_expert is int32 [n, 2]."""
         if dtype not in _DTYPES:
             raise ValueError(f"dtype must be bf16 or fp32, got {dtype}")
         self.device = torch.cuda.current_device() if device is None else device
@@ -66,8 +68,9 @@ class MoEShardLayer:
         self.ep = bool(flags & C.MOESHARD_FLAG_EXPERT_PARALLEL)
         self.F = d_ff if self.ep else d_ff // world
         self.E_host = n_experts // world if self.ep else n_experts   # experts computed here
+        self.top_k = max(1, top_k)
         self.cfg = C.moeshard_config(d_model, d_ff, n_experts, n_layers, max_tokens_per_rank,
-                                     _DTYPES[dtype], flags, ep_capacity_factor)
+                                     _DTYPES[dtype], flags, ep_capacity_factor, top_k)
         ws = C.moeshard_workspace_size(self.cfg, world)
         self.workspace = torch.empty(ws, dtype=torch.uint8, device=f"cuda:{self.device}")
         self._wbytes = C.moeshard_weight_storage_size(self.cfg, world)
@@ -150,8 +153,9 @@ class MoEShardLayer:
         if out is None:
             out = torch.empty_like(hidden)
         if forced_expert is not None:
-            if forced_expert.dtype != torch.int32 or forced_expert.shape != (n,):
-                raise C.MoEShardError(-2, f"forced_expert must be int32 [{n}]")
+            shape = (n,) if self.top_k == 1 else (n, self.top_k)
+            if forced_expert.dtype != torch.int32 or tuple(forced_expert.shape) != shape:
+                raise C.MoEShardError(-2, f"forced_expert must be int32 {list(shape)}")
         if stages == C.MOESHARD_STAGE_ALL:
             C.moeshard_forward(self.ctx, layer, hidden.data_ptr(), n, router_w.data_ptr(),
                                out.data_ptr(), _ptr(forced_expert), self._stream())
@@ -168,7 +172,7 @@ class MoEShardLayer:
         if self._collective() and (self.cfg.flags & (C.MOESHARD_FLAG_UNEVEN_TOKENS |
                                                      C.MOESHARD_FLAG_EXPERT_PARALLEL)):
             n_local = self.cfg.max_tokens_per_rank
-        N = n_local * (self.world if self._collective() else 1)
+        N = n_local * (self.world if self._collective() else 1) * self.top_k   # assignments
         dev = f"cuda:{self.device}"
         r = {
             "expert": torch.empty(N, dtype=torch.int32, device=dev),

@@ -66,7 +66,7 @@ class moeshard_config(ctypes.Structure):
         ("d_model", ctypes.c_int32), ("d_ff", ctypes.c_int32), ("n_experts", ctypes.c_int32),
         ("n_layers", ctypes.c_int32), ("max_tokens_per_rank", ctypes.c_int32),
         ("dtype", ctypes.c_int32), ("flags", ctypes.c_uint32),
-        ("ep_capacity_factor", ctypes.c_float),
+        ("ep_capacity_factor", ctypes.c_float), ("top_k", ctypes.c_int32),
     ]
 
 

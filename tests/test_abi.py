@@ -96,3 +96,21 @@ def test_shard_and_token_helpers():
     with pytest.raises(ValueError):
         shard_columns(6, 4, 0)
     assert local_token_range(8192, 4, 3) == (6144, 8192)
+
+
+def test_top_k_config_validation():
+    # top_k (R21): 0 / 1 = top-1, 2 = top-2 on the bf16 fused tcgen05 path only
+    from paper_2503_08467_b200 import moeshard as C
+    w1 = C.moeshard_workspace_size(_cfg(top_k=1), 1)
+    assert C.moeshard_workspace_size(_cfg(top_k=0), 1) == w1
+    w2 = C.moeshard_workspace_size(_cfg(top_k=2), 1)
+    assert w2 > w1 + 1024 * 768 * 2 * 2        # assignment rows: X_perm, H, y_assign grow
+    for bad in (dict(top_k=3), dict(top_k=-1), dict(top_k=2, n_experts=1),
+                dict(top_k=2, dtype=C.MOESHARD_FP32), dict(top_k=2, flags=C.MOESHARD_FLAG_P2P),
+                dict(top_k=2, flags=C.MOESHARD_FLAG_UNFUSED_GEMM),
+                dict(top_k=2, flags=C.MOESHARD_FLAG_SIMT_GEMM),
+                dict(top_k=2, flags=C.MOESHARD_FLAG_LAUNCH_PER_EXPERT),
+                dict(top_k=2, flags=C.MOESHARD_FLAG_ONCHIP_H)):
+        with pytest.raises(C.MoEShardError) as ei:
+            C.moeshard_workspace_size(_cfg(**bad), 1)
+        assert ei.value.code == -5, bad

@@ -971,3 +971,102 @@ def test_expert_mlp_under_graph_replay_and_natural_routing():
         inp = W.LayerInputs(xn, a.w_r, a.w_i, a.w_o, None)
         _check_layer(inp, out, r, tol=BF16_TOL)
     L.close()
+
+
+# --------------------------------------------------------------------- top-2 routing (R21)
+def _check_topk(inp, y, r, k, *, tol, forced=None):
+    """Top-k parity: expert sets / order exact where the fp64 logits are clear of the fp32
+    accumulation bound at every decisive gap (routing_margin_topk), otherwise the GPU's picks
+    must be candidates within the bound and the oracle runs with them; counts, offsets and
+    the assignment permutation exact; gates 1e-5; outputs within tol."""
+    x = inp.x
+    rt = O.route_topk(x, inp.w_r, k, None if forced is None else forced)
+    gpu_e = r["expert"].reshape(-1, k).astype(np.int64)
+    if forced is not None:
+        np.testing.assert_array_equal(gpu_e, rt.expert)
+    else:
+        bound = _fp32_logit_bound(x, inp.w_r).max(axis=1)
+        clear = O.routing_margin_topk(rt.logits, k) > 2 * bound
+        # k decisive gaps per token instead of one: about k times the top-1 ambiguity rate
+        assert clear.mean() > 1 - 0.01 * (k + 1)
+        np.testing.assert_array_equal(gpu_e[clear], rt.expert[clear])
+        kth = -np.sort(-rt.logits, axis=1)[:, k - 1]
+        for t in np.nonzero(~clear)[0]:
+            assert len(set(gpu_e[t].tolist())) == k
+            assert all(rt.logits[t, e] >= kth[t] - 2 * bound[t] for e in gpu_e[t])
+    y_ref, rt2, counts, offsets, perm = O.moe_layer_topk(x, inp.w_r, inp.w_i, inp.w_o, k,
+                                                         return_routing=True, forced=gpu_e)
+    np.testing.assert_array_equal(r["counts"], counts)
+    np.testing.assert_array_equal(r["offsets"], offsets)
+    np.testing.assert_array_equal(r["perm"], perm)
+    np.testing.assert_allclose(r["gate"].reshape(-1, k), rt2.gate, rtol=1e-5, atol=1e-6)
+    yg = y.float().cpu().numpy()
+    err = O.max_abs_rel(yg, y_ref)
+    assert err <= tol, f"max-abs-rel {err:.3e} > {tol}"
+    row = np.max(np.abs(yg - y_ref), axis=1) / np.maximum(np.max(np.abs(y_ref), axis=1), 1e-30)
+    assert row.max() <= tol, f"per-row max-abs-rel {row.max():.3e} > {tol}"
+    return err
+
+
+def _run_topk(inp, k, *, flags=0, forced=None):
+    from paper_2503_08467_b200 import MoEShardLayer
+    N, h = inp.x.shape
+    E, _, d_ff = inp.w_i.shape
+    L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16, flags=flags,
+                      top_k=k)
+    L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
+    y = L.forward(0, inp.x.cuda(), inp.w_r.cuda(),
+                  forced_expert=None if forced is None else forced.cuda())
+    r = L.routing(N)
+    L.check()
+    torch.cuda.synchronize()
+    return L, y, {key: v.cpu().numpy() for key, v in r.items()}
+
+
+@pytest.mark.parametrize("N,h,d_ff,E", [
+    (1000, 256, 512, 8),       # ragged tail, several tiles
+    (3000, 256, 384, 64),      # odd up-tile count (F = 384), several chunks
+    (8192, 768, 3072, 64),     # the C2 shape: 16384 assignments
+])
+def test_top2_natural_routing_matches_oracle(N, h, d_ff, E):
+    inp = W.make_layer_inputs(31, N, h, d_ff, E, dtype=torch.bfloat16, routing="natural")
+    L, y, r = _run_topk(inp, 2)
+    _check_topk(inp, y, r, 2, tol=BF16_TOL)
+    assert L.stats()["n_tokens_global"] == N
+
+
+def test_top2_forced_skewed_and_one_rank_collectives():
+    # forced pairs (the replaced router, R18) with a hot expert; then the same layer through
+    # the NCCL exchange path with a 1-rank communicator
+    N, h, d_ff, E = 2048, 256, 512, 16
+    inp = W.make_layer_inputs(32, N, h, d_ff, E, dtype=torch.bfloat16, routing="natural")
+    g = np.random.default_rng(5)
+    first = np.where(g.random(N) < 0.5, 3, g.integers(0, E, N))
+    second = (first + 1 + g.integers(0, E - 1, N)) % E     # distinct from the first
+    forced = torch.from_numpy(np.stack([first, second], axis=1).astype(np.int32))
+    for flags in (0, __import__("paper_2503_08467_b200").moeshard.MOESHARD_FLAG_FORCE_COLLECTIVES):
+        L, y, r = _run_topk(inp, 2, flags=flags, forced=forced)
+        _check_topk(inp, y, r, 2, tol=BF16_TOL, forced=forced.numpy())
+
+
+def test_top2_graph_replay_with_new_tokens():
+    from paper_2503_08467_b200 import MoEShardLayer
+    N, h, d_ff, E = 1536, 256, 512, 16
+    a = W.make_layer_inputs(33, N, h, d_ff, E, dtype=torch.bfloat16, routing="natural")
+    b = W.make_layer_inputs(34, N, h, d_ff, E, dtype=torch.bfloat16, routing="natural")
+    L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16, top_k=2)
+    L.load_expert_shards(0, a.w_i.cuda(), a.w_o.cuda())
+    x = a.x.cuda().clone()
+    w_r = a.w_r.cuda()
+    out = torch.empty_like(x)
+    L.forward(0, x, w_r, out=out)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        L.forward(0, x, w_r, out=out)
+    x.copy_(b.x.cuda())
+    gr.replay()
+    torch.cuda.synchronize()
+    r = {key: v.cpu().numpy() for key, v in L.routing(N).items()}
+    inp_b = W.LayerInputs(b.x, a.w_r, a.w_i, a.w_o, None)
+    _check_topk(inp_b, out, r, 2, tol=BF16_TOL)
