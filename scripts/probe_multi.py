@@ -12,12 +12,14 @@ SHAPES = {"c2g1": (64, 768, 3072, 8192, 1), "c2g8": (64, 768, 3072, 8192, 8),
           "c3g4": (128, 768, 3072, 16384, 4), "c5g1": (128, 1024, 4096, 32768, 1),
           "c5g8": (128, 1024, 4096, 32768, 8), "c4g8": (256, 768, 3072, 16384, 8),
           "c3g1": (128, 768, 3072, 16384, 1)}
+# "<shape>k2": the same layer with top-2 routing (R21), natural router only
 
 
-def probe(E, h, d_ff, N, G, steps=120):
+def probe(E, h, d_ff, N, G, steps=120, top_k=1):
     F = d_ff // G
     NW = max(1, math.ceil(3 * 126 * 2**20 / (2 * E * h * F * 2)))
-    L = MoEShardLayer(h, F, E, n_layers=NW, max_tokens_per_rank=N, dtype=torch.bfloat16)
+    L = MoEShardLayer(h, F, E, n_layers=NW, max_tokens_per_rank=N, dtype=torch.bfloat16,
+                      top_k=top_k)
     c0, c1 = shard_columns(d_ff, G, 0)
     for j in range(NW):
         wi, wo = W.make_expert_weights(2, E, h, d_ff, cols=(c0, c1), device="cuda", layer=j % 3)
@@ -27,8 +29,8 @@ def probe(E, h, d_ff, N, G, steps=120):
     w_r = W.make_router_weight(2, h, E, device="cuda")
     out = torch.empty_like(x)
     res = {}
-    for routing in ("uniform", "zipf"):
-        f = W.draw_experts(2, N, E, routing, device="cuda")
+    for routing in (("uniform", "zipf") if top_k == 1 else ("natural",)):
+        f = W.draw_experts(2, N, E, routing, device="cuda") if routing != "natural" else None
         fwd = lambda k: L.forward(k % NW, x, w_r, forced_expert=f, out=out)
         st = torch.cuda.Stream()
         st.wait_stream(torch.cuda.current_stream())
@@ -59,4 +61,5 @@ def probe(E, h, d_ff, N, G, steps=120):
 
 if __name__ == "__main__":
     names = sys.argv[1:] or ["c2g1", "c2g8", "c5g1"]
-    print(json.dumps({n: probe(*SHAPES[n]) for n in names}), flush=True)
+    print(json.dumps({n: probe(*SHAPES[n.replace("k2", "")], top_k=2 if n.endswith("k2") else 1)
+                      for n in names}), flush=True)
