@@ -86,12 +86,12 @@ __global__ void __launch_bounds__(128) group_block_scan(const int32_t* __restric
 //     wider rows continue in column blocks of VPL*32 vectors).
 // kSplit CTAs share one hist-block: all compute its ranks, each copies
 // 128/kSplit of its rows (spreads the row traffic over more SMs).
-template <int VPL, int kSplit>
+template <int VPL, int kSplit, int K>
 __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
     const int32_t* __restrict__ bbase, const int32_t* __restrict__ btot, int E, Tables tb,
     int n_mt_up_tc, int n_mt_down_tc, const RouteRec* __restrict__ route,
     const uint4* __restrict__ x_all, int n, int nbr, int HB, int32_t* __restrict__ perm,
-    int row_vecs, uint4* __restrict__ x_perm, int NB, int K) {
+    int row_vecs, uint4* __restrict__ x_perm, int NB) {
   // K = top_k: a block of HB tokens holds HB K (token, expert) assignments a = K t + j
   // (route records, histograms and the expert-ordered rows are per assignment)
   if (threadIdx.x == 0) TL_MIN(1);
@@ -104,8 +104,8 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   __shared__ int32_t s_pre[kMaxExperts];
   __shared__ int32_t s_base[kMaxExperts];   // compact (public perm) position of this block's first e
   __shared__ int32_t s_bpad[kMaxExperts];   // padded internal position
-  __shared__ int32_t whist[8][kMaxExperts];
-  __shared__ int32_t s_j[256];
+  __shared__ int32_t whist[4 * K][kMaxExperts];
+  __shared__ int32_t s_j[128 * K];
   __shared__ int32_t s_warp[5 * (kThreads / 32)];   // segment_tables' warp totals
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x / kSplit, part = blockIdx.x % kSplit;
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
       if (tt < t1 && col < row_vecs) v[u][c] = __ldg(x_all + (size_t)tt * row_vecs + col);
     }
   }
-  const int rank_warps = 4 * K;                   // warps holding one assignment per thread
+  constexpr int rank_warps = 4 * K;               // warps holding one assignment per thread
   int e = -1, rank_w = 0, a = 0;
   float gate = 0.f;
   if (warp < rank_warps && has_block) {
@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   // 3. row stores (first column block loaded at the top)
   if (threadIdx.x == 0) { TL_MIN(6); TL_MAX(6); }
   if (x_perm == nullptr || !has_block) return;
+#pragma unroll
   for (int g = 0; g < K; ++g) {   // groups of 32 assignment rows (kRowsPerWarp x 8 warps)
   const int gbase = row_base + g * kRowsPerWarp * (kThreads / 32);
   if (g > 0) {
@@ -260,8 +261,12 @@ void launch_group_blocks(const int32_t* hist, int NB, int E, int32_t* base, int3
 #endif
   constexpr int kSp = MOESHARD_GROUP_SPLIT;
 #define SG(V)                                                                                  \
-  launch_pdl(group_scatter_gather<V, kSp>, dim3(NB * kSp), dim3(1024 / kSp), 0, s, base, tot, E, tb, \
-             n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm, row_vecs, xd, NB, K)
+  (K == 2 ? launch_pdl(group_scatter_gather<V, kSp, 2>, dim3(NB * kSp), dim3(1024 / kSp), 0, s,    \
+                       base, tot, E, tb, n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm,     \
+                       row_vecs, xd, NB)                                                           \
+          : launch_pdl(group_scatter_gather<V, kSp, 1>, dim3(NB * kSp), dim3(1024 / kSp), 0, s,    \
+                       base, tot, E, tb, n_mt_up_tc, n_mt_down_tc, route, xs, n, nbr, HB, perm,     \
+                       row_vecs, xd, NB))
   switch (vpl) {
     case 1: SG(1); break;
     case 2: SG(2); break;
