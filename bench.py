@@ -644,7 +644,7 @@ def main():
                   "roof_us": round(roof3, 2), "roof_ns_us": round(max(t_tc, t_nv), 2),
                   "frac": round(roof3 / (ms * 1e3), 4),
                   "note": "roof = max(T_tc at bf16 burst peak, T_hbm weights+x+out at measured HBM, "
-                          "T_nv AG+RS bf16 at 770 GB/s measured peer bw); roof_ns = north-star two-term"}
+                          "T_nv AG+RS bf16 at 770 GB/s, the peer-copy bandwidth per direction B200_PROFILING.md measured; MEASURED_PEAKS.json has no NVLink entry); roof_ns = north-star two-term"}
 
     line = {
         "metric": "MoE-layer tokens/s", "value": N / (ms * 1e-3), "unit": "tokens/s",
