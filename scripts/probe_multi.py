@@ -19,6 +19,7 @@ def probe(E, h, d_ff, N, G, steps=120, top_k=1):
     F = d_ff // G
     NW = max(1, math.ceil(3 * 126 * 2**20 / (2 * E * h * F * 2)))
     L = MoEShardLayer(h, F, E, n_layers=NW, max_tokens_per_rank=N, dtype=torch.bfloat16,
+                      flags=int(os.environ.get("PROBE_FLAGS", "0")),
                       top_k=top_k)
     c0, c1 = shard_columns(d_ff, G, 0)
     for j in range(NW):
