@@ -133,6 +133,26 @@ int main() {
                    best * 1e3, gb / (best * 1e-3));
           }
   }
+  // per-SM rate with only part of the GPU streaming (the FFN's tail: do the late clusters
+  // speed up when the others have finished?) - fixed tiles per CTA, growing CTA count
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  for (int S : {6, 12})
+    for (int grid : {16, 37, 74, 111, sms}) {
+      float best = 1e9f;
+      for (int rep = 0; rep < 6; ++rep) {
+        const int k = rep % NSETS;
+        cudaEventRecord(a);
+        stream<<<grid, 128, S * TILE + 1024>>>(tm[k], buf + k * bytes, ntiles, S, 1, 1, 1, per_cta, sink);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep >= 2 && ms < best) best = ms;
+      }
+      const double gb = static_cast<double>(per_cta) * grid * TILE / 1e9;
+      printf("partial grid %3d CTAs  stages %2d: %7.1f us  %6.0f GB/s total  %5.1f GB/s per SM\n", grid, S,
+             best * 1e3, gb / (best * 1e-3), gb / (best * 1e-3) / grid);
+    }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) printf("error: %s\n", cudaGetErrorString(e));
   return 0;
