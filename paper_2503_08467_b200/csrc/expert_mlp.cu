@@ -52,11 +52,6 @@ constexpr int kColUp = 0, kColDn = 256; // TMEM columns: up accumulator x 2 buff
 constexpr int kSmemBudget = 225 * 1024; // H + ring (barriers and alignment on top)
 constexpr size_t kMaxSmem = 232448;     // opt-in dynamic shared memory per CTA (sm_100)
 
-// make this thread's generic shared-memory writes (local and remote) visible to the async
-// proxy (the tensor core's operand reads) of the CTAs they were written to
-__device__ __forceinline__ void fence_proxy_async_all() {
-  asm volatile("fence.proxy.async;" ::: "memory");
-}
 // asynchronous 16-B store into a peer CTA's shared memory; completion is counted (bytes) on
 // the peer's mbarrier at bar_cluster, the storing thread does not wait for it
 __device__ __forceinline__ void st_async_v4(uint32_t addr, uint4 v, uint32_t bar_cluster) {

@@ -1054,7 +1054,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
     const int wq = warp & 3, eh = (warp - 4) >> 2;
+#if !MOESHARD_EPI_STM
     __nv_bfloat16* stage = s_stage + (warp - 4) * 512;   // 1 KB per epilogue warp
+#endif
     const uint64_t pol_keep = policy_evict_last();
     const uint32_t leader_tempty = mapa_shared(smem_u32(tempty), 0);
     if (fp.early_tables) griddep_wait();   // perm / route of the grouping launch

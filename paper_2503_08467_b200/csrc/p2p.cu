@@ -120,12 +120,9 @@ __global__ void rs_signal(P2PArgs a) {
 __global__ void __launch_bounds__(256) reduce_partials(P2PArgs a, int n, int row_vecs,
                                                        uint4* __restrict__ out, int32_t* err) {
   const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
-  __shared__ int s_ok;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0)
     wait_flags(reinterpret_cast<const int32_t*>(a.self) + 32 * (1 + a.world), a.world, epoch + 1,
                err);
-    s_ok = 1;
-  }
   __syncthreads();
   const size_t nv = static_cast<size_t>(n) * row_vecs;
   const size_t slot = static_cast<size_t>(a.n_max) * row_vecs;
@@ -177,7 +174,6 @@ __global__ void __launch_bounds__(256) reduce_partials(P2PArgs a, int n, int row
       __threadfence();
     }
   }
-  (void)s_ok;
 }
 
 // grouping-side wait for Step 3 (one CTA; launched just before the grouping kernels)
