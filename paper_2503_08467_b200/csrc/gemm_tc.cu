@@ -759,6 +759,22 @@ struct FusedParams {
 #ifndef MOESHARD_EPI_STM
 #define MOESHARD_EPI_STM 1
 #endif
+// Paired token chunks (kernel template kPair, chosen per launch): an expert whose segment
+// is cut into several chunks of <= kPairMaxCs tokens is processed two chunks per unit - one
+// weight stage feeds two MMAs (chunk a into accumulator slot s, chunk b into slot s ^ 1),
+// so a weight tile enters shared memory once per two chunks instead of once per chunk (a
+// unit's time is its weight stream, ~50 GB/s per SM: scripts/micro/wstream.cu). The two
+// chunks are two "virtual tiles" of the accumulator sequence; a single-chunk unit is one.
+// Pays where most experts get ~2 chunks of ~130-160 tokens (C5: 256 tokens per expert on
+// average, -8 %); the launch picks it only when the assignments per expert average >= 256,
+// since the extra decode costs ~2 us where no expert is split (C2, C3).
+#ifndef MOESHARD_PAIR_MAX_CS
+#define MOESHARD_PAIR_MAX_CS 192
+#endif
+// only chunks of <= kPairMaxCs tokens are paired: a pair of 256-token chunks is tensor-bound
+// (2 x 0.385 us of MMA per k-step against 0.33 us for the weight tile) and would only lose
+// the accumulator double buffering
+constexpr int kPairMaxCs = MOESHARD_PAIR_MAX_CS;
 constexpr int kEpiWarps = MOESHARD_EPI_WARPS;   // epilogue warps per CTA (multiple of 4)
 constexpr int kFusedThreads = 128 + 32 * kEpiWarps;
 static_assert(kEpiWarps % 4 == 0 && kEpiWarps <= 16, "1-4 epilogue warps per TMEM lane quadrant");
@@ -769,7 +785,7 @@ constexpr int kUQ = 2;             // unit-queue slots (dynamic scheduling): sma
 constexpr int kUQConsumers = 5 + 2 * kEpiWarps;   // warps that read a slot: leader 0,1,3 + epilogue; follower 0,3 + epilogue
 constexpr uint32_t kSchedRank = 0;   // the unit scheduler's CTA (leader)
 
-template <int AS, int BS>
+template <int AS, int BS, bool kPair>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     tc_moe_ffn_2sm(const __grid_constant__ CUtensorMap tmA_up, const __grid_constant__ CUtensorMap tmB_up,
                    const __grid_constant__ CUtensorMap tmA_dn, const __grid_constant__ CUtensorMap tmB_dn,
@@ -791,9 +807,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   int32_t* s_off = s_pref + (E + 1);     // internal segment starts (pos)
   int32_t* s_cs = s_off + (E + 1);
   int32_t* s_end = s_cs + E;             // pos + count
+  int32_t* s_ppref = s_end + E;          // [E+1] cumulative units per (expert, m-tile pair)
   // per-warp epilogue staging (4 x 1 KB), then the unit queue (slots + barriers)
   __nv_bfloat16* s_stage = reinterpret_cast<__nv_bfloat16*>(
-      (reinterpret_cast<uintptr_t>(s_end + E) + 15) & ~static_cast<uintptr_t>(15));
+      (reinterpret_cast<uintptr_t>(s_ppref + E + 1) + 15) & ~static_cast<uintptr_t>(15));
   int* s_uq = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(s_stage) + kEpiWarps * kStmStage);
   uint64_t* uq_full = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(s_uq + kUQ) + 7) & ~static_cast<uintptr_t>(7));
@@ -862,6 +879,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   }
   const int n_mp_up = (fp.up.n_mt + 1) / 2, n_mp_dn = (fp.dn.n_mt + 1) / 2;
   const int ncl = static_cast<int>(nclusters_x());
+  if (kPair) {   // units per (expert, m-tile pair): ceil(chunks / 2), prefix by warp 0
+    __syncthreads();
+    if (warp == 0) {
+      int run = 0;
+      for (int b0 = 0; b0 < E; b0 += 32) {
+        const int e = b0 + lane;
+        const int nc = e < E ? s_pref[e + 1] - s_pref[e] : 0;
+        const int np = (e < E && s_cs[e] <= kPairMaxCs) ? (nc + 1) >> 1 : nc;
+        int inc = np;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += t;
+        }
+        if (e < E) s_ppref[e] = run + inc - np;
+        run += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) s_ppref[E] = run;
+    }
+  }
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -871,7 +908,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
 
   // pair-units cover m-tiles (2q, 2q+1); with an odd count the last pair has
   // both CTAs on the same m-tile (the follower's copy is computed, not stored)
-  const int chunks = s_pref[E];
+  const int chunks = kPair ? s_ppref[E] : s_pref[E];   // (paired) chunk units
   const int total_up = chunks * n_mp_up;
   const int total = total_up + chunks * n_mp_dn;
   const int nkb_up = fp.up.K / BK, nkb_dn = fp.dn.K / BK;   // k-blocks per unit
@@ -890,11 +927,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     }
     return u;
   };
-  // list position u -> (down?, decoded unit)
-  auto unit_at = [&](int u, bool& down) -> Unit {
+  // list position u -> (down?, decoded unit); with paired chunks, b = the unit's second
+  // chunk (b.ntok = 0: a single-chunk unit)
+  auto unit_at2 = [&](int u, bool& down, Unit& b) -> Unit {
     down = u >= total_up;
-    return down ? decode(u - total_up, n_mp_dn, E, s_pref, s_off, s_end, s_cs)
-                : decode(u, n_mp_up, E, s_pref, s_off, s_end, s_cs);
+    const int v = down ? u - total_up : u;
+    const int n_mp = down ? n_mp_dn : n_mp_up;
+    if (!kPair) {
+      b.ntok = 0;
+      return decode(v, n_mp, E, s_pref, s_off, s_end, s_cs);
+    }
+    const int q = v / n_mp;
+    int lo = 0, hi = E;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_ppref[mid] <= q) lo = mid; else hi = mid;
+    }
+    const int npe = s_ppref[lo + 1] - s_ppref[lo];
+    const int local = v - s_ppref[lo] * n_mp;
+    Unit w;
+    w.e = lo;
+    w.mt = local / npe;
+    const int nch = s_pref[lo + 1] - s_pref[lo], cs = s_cs[lo];
+    const bool paired = cs <= kPairMaxCs;
+    const int ca = (paired ? 2 : 1) * (local - w.mt * npe);
+    w.chunk = s_pref[lo] + ca;
+    w.tok0 = s_off[lo] + ca * cs;
+    w.ntok = min(cs, s_end[lo] - w.tok0);
+    b.e = lo;
+    b.mt = w.mt;
+    b.chunk = w.chunk + 1;
+    b.tok0 = w.tok0 + cs;
+    b.ntok = paired && ca + 1 < nch ? min(cs, s_end[lo] - b.tok0) : 0;
+    return w;
+  };
+  auto unit_at = [&](int u, bool& down) -> Unit {
+    Unit b;
+    return unit_at2(u, down, b);
   };
 
   // unit scheduler (dynamic mode): the leader's otherwise idle warp 2
@@ -937,7 +1006,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       const CUtensorMap* tm = down ? &tmA_dn : &tmA_up;
       const int mt = min(2 * w.mt + static_cast<int>(rank), n_mt - 1);
       const int row0 = ((w.e * n_mt + mt) * nkb) * BM;
-      const uint64_t pol_w = (s_pref[w.e + 1] - s_pref[w.e] > 1) ? pol_shared : pol_once;
+      const int32_t* upf = kPair ? s_ppref : s_pref;   // units per (e, mt) > 1: siblings
+      const uint64_t pol_w = (upf[w.e + 1] - upf[w.e] > 1) ? pol_shared : pol_once;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&emptyA[stage], phase ^ 1);
         const uint32_t fb = leader_full + stage * 8;
@@ -960,48 +1030,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     const uint32_t leader_full = mapa_shared(smem_u32(fullB), 0);
     int stage = 0;
     uint32_t phase = 0;
-    for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
-      bool down;
-      const Unit w = unit_at(u, down);
-      const int nkb = down ? nkb_dn : nkb_up;
-      const CUtensorMap* tm = down ? &tmB_dn : &tmB_up;
-      if (down) {   // H rows of this token chunk complete? (acquire), then order the TMA after it
-        const int target = 2 * n_mp_up;   // both CTAs of every up pair-unit of (e, chunk)
-        if (elect_one()) {
-          uint32_t it = 0;
-          while (ld_acquire_gpu(fp.done + w.chunk) < target) {
-            if (++it > (1u << 24)) {   // a cluster never became resident: report, do not hang
-              atomicOr(fp.up.tb.stats + 3, 8);
-              break;
-            }
-            __nanosleep(128);
+    // H rows of a token chunk complete? (acquire), then order the TMA after it
+    auto wait_h = [&](int chunk, int k) {
+      const int target = 2 * n_mp_up;   // both CTAs of every up pair-unit of (e, chunk)
+      if (elect_one()) {
+        uint32_t it = 0;
+        while (ld_acquire_gpu(fp.done + chunk) < target) {
+          if (++it > (1u << 24)) {   // a cluster never became resident: report, do not hang
+            atomicOr(fp.up.tb.stats + 3, 8);
+            break;
           }
-          fence_proxy_async_global();
-          if (leader) TR(cid, k, 7);
+          __nanosleep(128);
         }
-        __syncwarp();
+        fence_proxy_async_global();
+        if (leader) TR(cid, k, 7);
       }
+      __syncwarp();
+    };
+    // one k-block of one chunk's token tile (this CTA's half of its rows) into the next stage
+    auto load_b = [&](const CUtensorMap* tm, const Unit& w, int kb) {
       const int half = ((w.ntok + 31) & ~31) / 2;
       const int nb = half / B2_BOX;
       const int r0 = w.tok0 + static_cast<int>(rank) * half;
       const uint32_t stage_bytes = nb * B2_BOX * BK * 2;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&emptyB[stage], phase ^ 1);
-        const uint32_t fb = leader_full + stage * 8;
-        if (elect_one()) {
+      mbar_wait(&emptyB[stage], phase ^ 1);
+      const uint32_t fb = leader_full + stage * 8;
+      if (elect_one()) {
 #ifdef MOESHARD_EXP_NO_BLOAD
-          if (leader) mbar_arrive(&fullB[stage]);
-          else mbar_arrive_cluster(fb);
+        if (leader) mbar_arrive(&fullB[stage]);
+        else mbar_arrive_cluster(fb);
 #else
-          if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * stage_bytes);
-          else mbar_arrive_cluster(fb);
-          for (int i = 0; i < nb; ++i)
-            tma_load_2d_2sm(tm, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
-                            r0 + i * B2_BOX, pol_x);
+        if (leader) mbar_arrive_expect_tx(&fullB[stage], 2 * stage_bytes);
+        else mbar_arrive_cluster(fb);
+        for (int i = 0; i < nb; ++i)
+          tma_load_2d_2sm(tm, fb, sB + stage * B2_BYTES + i * (B2_BOX * BK * 2), kb * BK,
+                          r0 + i * B2_BOX, pol_x);
 #endif
-        }
-        __syncwarp();
-        if (++stage == BS) { stage = 0; phase ^= 1; }
+      }
+      __syncwarp();
+      if (++stage == BS) { stage = 0; phase ^= 1; }
+    };
+    for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
+      bool down;
+      Unit wb;
+      const Unit w = unit_at2(u, down, wb);
+      const int nkb = down ? nkb_dn : nkb_up;
+      const CUtensorMap* tm = down ? &tmB_dn : &tmB_up;
+      if (down) {
+        wait_h(w.chunk, k);
+        if (wb.ntok > 0) wait_h(wb.chunk, k);
+      }
+      for (int kb = 0; kb < nkb; ++kb) {   // paired: chunk a, then chunk b, per k-block
+        load_b(tm, w, kb);
+        if (wb.ntok > 0) load_b(tm, wb, kb);
       }
     }
   } else if (warp == 1) {
@@ -1013,41 +1094,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       uint32_t aphase = 0;
       for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
         bool down;
-        const Unit w = unit_at(u, down);
+        Unit wb;
+        const Unit w = unit_at2(u, down, wb);
+        const bool two = wb.ntok > 0;   // paired chunks: a -> slot as, b -> slot as ^ 1
         const int nkb = down ? nkb_dn : nkb_up;
-        const int nmma = (w.ntok + 31) & ~31;
-        const uint32_t idesc = idesc_bf16_f32(2 * BM, nmma);
+        const uint32_t idesc = idesc_bf16_f32(2 * BM, (w.ntok + 31) & ~31);
+        const uint32_t idesc_b = idesc_bf16_f32(2 * BM, two ? (wb.ntok + 31) & ~31 : 32);
+        const int as_b = as ^ 1;
+        const uint32_t aphase_b = as_b == 0 ? aphase ^ 1 : aphase;   // the next virtual tile's
         if (lane == 0) TR(cid, k, 0);
         mbar_wait(&tempty[as], aphase ^ 1);
+        if (two) mbar_wait(&tempty[as_b], aphase_b ^ 1);
         tc_fence_after();
         if (lane == 0) TR(cid, k, 1);
-        const uint32_t d = tmem_base + as * ACC_STRIDE;
+        const uint32_t d = tmem_base + as * ACC_STRIDE, d_b = tmem_base + as_b * ACC_STRIDE;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&fullB[sb], pb);
           if (kb == 0 && lane == 0) TR(cid, k, 2);
           mbar_wait(&fullA[sa], pa);
           tc_fence_after();
           if (kb == 0 && lane == 0) TR(cid, k, 3);
+          const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
           if (elect_one()) {
-            const uint64_t ad = smem_desc_k_sw128(smem_u32(sA + sa * A_BYTES));
             const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B2_BYTES));
 #ifndef MOESHARD_EXP_NO_MMA
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
               mma_bf16_ss_2sm(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
 #endif
-            mma_commit_2sm(&emptyA[sa], 0x3);
             mma_commit_2sm(&emptyB[sb], 0x3);
           }
           __syncwarp();
-          if (++sa == AS) { sa = 0; pa ^= 1; }
           if (++sb == BS) { sb = 0; pb ^= 1; }
+          if (two) {   // the same weight stage, chunk b's token stage
+            mbar_wait(&fullB[sb], pb);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t bd = smem_desc_k_sw128(smem_u32(sB + sb * B2_BYTES));
+#ifndef MOESHARD_EXP_NO_MMA
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)
+                mma_bf16_ss_2sm(d_b, ad + 2 * kk, bd + 2 * kk, idesc_b, (kb | kk) != 0);
+#endif
+              mma_commit_2sm(&emptyB[sb], 0x3);
+            }
+            __syncwarp();
+            if (++sb == BS) { sb = 0; pb ^= 1; }
+          }
+          if (elect_one()) mma_commit_2sm(&emptyA[sa], 0x3);
+          __syncwarp();
+          if (++sa == AS) { sa = 0; pa ^= 1; }
         }
-        if (elect_one()) mma_commit_2sm(&tfull[as], 0x3);
+        if (elect_one()) {
+          mma_commit_2sm(&tfull[as], 0x3);
+          if (two) mma_commit_2sm(&tfull[as_b], 0x3);
+        }
         __syncwarp();
         if (lane == 0) TR(cid, k, 4);
-        as ^= 1;
-        if (as == 0) aphase ^= 1;
+        for (int v = 0; v < (two ? 2 : 1); ++v) {
+          as ^= 1;
+          if (as == 0) aphase ^= 1;
+        }
       }
     }
     if (leader && lane == 0) TL_MAX(3);   // last MMA issued
@@ -1064,7 +1171,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     uint32_t aphase = 0;
     for (int k = 0, u = fetch(0); u < total; u = fetch(++k)) {
       bool down;
-      const Unit w = unit_at(u, down);
+      Unit wb;
+      const Unit wa = unit_at2(u, down, wb);
+      for (int vt = 0; vt < (wb.ntok > 0 ? 2 : 1); ++vt) {   // paired chunks: two tiles
+      const Unit& w = vt ? wb : wa;
       // down: destination rows and gates loaded before the accumulator wait (their
       // latency hides behind it; at short K it was exposed once per tile)
       int rows_r[BN_MAX / 32];
@@ -1118,6 +1228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       }
       as ^= 1;
       if (as == 0) aphase ^= 1;
+      }   // virtual tiles
     }
     if (fp.dn.p2p_n > 0) __threadfence_system();   // remote partial rows before the signal kernel
   }
@@ -1135,7 +1246,7 @@ size_t smem_bytes(int E, int as, int bs) {
 }
 
 size_t smem_bytes_2sm(int E, int as, int bs) {
-  return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (4 * E + 2) * 4 +
+  return 1024 + as * A_BYTES + bs * B2_BYTES + (2 * as + 2 * bs + 4) * 8 + 16 + (5 * E + 3) * 4 +
          16 + kEpiWarps * kStmStage + 96;   // + epilogue staging (per epilogue warp) + unit queue
 }
 
@@ -1186,7 +1297,7 @@ TR_EXPORT(moeshard_tr_ffn)
 cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
                               const TcParams& up, const TcParams& dn, int32_t* done, bool dynamic,
-                              bool early_tables, int grid, cudaStream_t s) {
+                              bool early_tables, bool pair_chunks, int grid, cudaStream_t s) {
 #ifndef MOESHARD_FFN_AS
 #define MOESHARD_FFN_AS 6
 #define MOESHARD_FFN_BS 6
@@ -1194,15 +1305,17 @@ cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_
   constexpr int AS = MOESHARD_FFN_AS, BS = MOESHARD_FFN_BS;
   static PerDeviceOnce attr;
   if (attr.need()) {
-    cudaError_t e = cudaFuncSetAttribute(tc_moe_ffn_2sm<AS, BS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_bytes_2sm(kMaxExperts, AS, BS)));
-    if (e != cudaSuccess) return e;
+    for (auto* k : {tc_moe_ffn_2sm<AS, BS, false>, tc_moe_ffn_2sm<AS, BS, true>}) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem_bytes_2sm(kMaxExperts, AS, BS)));
+      if (e != cudaSuccess) return e;
+    }
     attr.done();
   }
   FusedParams fp{up, dn, done, dynamic, early_tables};
-  return launch_pdl(tc_moe_ffn_2sm<AS, BS>, dim3(grid & ~1), dim3(kFusedThreads),
-                    smem_bytes_2sm(up.E, AS, BS), s, tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
+  return launch_pdl(pair_chunks ? tc_moe_ffn_2sm<AS, BS, true> : tc_moe_ffn_2sm<AS, BS, false>,
+                    dim3(grid & ~1), dim3(kFusedThreads), smem_bytes_2sm(up.E, AS, BS), s,
+                    tmA_up, tmB_up, tmA_dn, tmB_dn, fp);
 }
 
 cudaError_t launch_tc_gemm(bool down, const CUtensorMap& tmA, const CUtensorMap& tmB,

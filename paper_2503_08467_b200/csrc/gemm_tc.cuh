@@ -67,7 +67,7 @@ cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, boo
 cudaError_t launch_tc_moe_ffn(const CUtensorMap& tmA_up, const CUtensorMap& tmB_up,
                               const CUtensorMap& tmA_dn, const CUtensorMap& tmB_dn,
                               const TcParams& up, const TcParams& dn, int32_t* done, bool dynamic,
-                              bool early_tables, int grid, cudaStream_t s);
+                              bool early_tables, bool pair_chunks, int grid, cudaStream_t s);
 
 // Both products of one expert and <= 128 of its tokens per cluster of F/128 CTAs with H
 // kept on chip (expert_mlp.cu); applicable when expert_mlp_supported(h, F, E).

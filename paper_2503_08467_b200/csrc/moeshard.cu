@@ -769,6 +769,13 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
         c->launches += 1;
       }
     } else if (fused) {
+      // paired token chunks when the assignments per expert average >= 256 (most experts
+      // then get two chunks of ~130-160 tokens; gemm_tc.cu kPair)
+      const long long n_assign = static_cast<long long>(c->coll ? c->world : 1) * ns * c->K;
+#ifndef MOESHARD_PAIR_MIN_F
+#define MOESHARD_PAIR_MIN_F 2048
+#endif
+      const bool pair_chunks = n_assign >= 256LL * Et && F >= MOESHARD_PAIR_MIN_F;
       TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), Et, c->tb,
                   static_cast<__nv_bfloat16*>(c->H), F, nullptr, nullptr};
       // top_k > 1: each (token, expert) assignment's row goes to y_assign, summed per token below
@@ -779,7 +786,8 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
       if (c->p2p) set_p2p_out(c, dn, ns);
       CUDA_TRY(c, launch_tc_moe_ffn(lw.tm_in, c->tm_xperm16, lw.tm_out, c->tm_H16, up, dn,
                                     c->tb.done, (c->cfg.flags & MOESHARD_FLAG_DYNAMIC_SCHED) != 0,
-                                    /*early_tables=*/n > 0 && !c->ep, c->num_sms, s));
+                                    /*early_tables=*/n > 0 && !c->ep,
+                                    /*pair_chunks=*/pair_chunks, c->num_sms, s));
       if (c->K > 1) {   // y[t] = sum_j y_assign[K t + j] (R21); rank-major rows of all ranks
         launch_combine_assignments(c->y_assign, P, (c->coll ? c->world : 1) * ns, h * c->elt, c->K,
                                    c->num_sms, s);

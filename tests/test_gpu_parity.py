@@ -159,6 +159,41 @@ def test_fused_and_unfused_gemm_agree_bitwise(N, h, d_ff, E):
     assert torch.equal(ys[0], ys[1])
 
 
+@pytest.mark.parametrize("flag", ["UNFUSED_GEMM", "DYNAMIC_SCHED"])
+def test_paired_chunks_bitwise_and_oracle(flag):
+    """Paired token chunks (gemm_tc.cu kPair, picked when the assignments per expert average
+    >= 256): experts cut into chunks of <= 192 tokens run two chunks per unit on one weight
+    stage. Planted counts give 2 paired chunks (300, 330 tokens), 3 chunks of 192 (520: a
+    pair and a single), chunks of 256 that stay unpaired (500, 700, 900), an empty and a
+    small expert. The fused kernel must equal the unfused two-launch path (no pairing, same
+    per-chunk arithmetic) bit for bit, and the dynamic scheduler must equal the static one;
+    both within 2e-2 of the oracle with exact tables."""
+    from paper_2503_08467_b200 import MoEShardLayer
+    from paper_2503_08467_b200 import moeshard as C
+    counts = [300, 700, 500, 330, 900, 520, 0, 50]
+    N, h, d_ff, E = sum(counts), 512, 1024, len(counts)
+    assert N >= 256 * E
+    inp = W.make_layer_inputs(23, N, h, d_ff, E, dtype=torch.bfloat16, routing="uniform")
+    ids = np.repeat(np.arange(E), counts)
+    ids = ids[np.random.default_rng(5).permutation(N)]
+    inp.forced = torch.from_numpy(ids.astype(np.int32))
+    f = inp.forced.cuda().contiguous()
+    ys, rs = [], []
+    for flags in (0, getattr(C, f"MOESHARD_FLAG_{flag}")):
+        L = MoEShardLayer(h, d_ff, E, max_tokens_per_rank=N, dtype=torch.bfloat16, flags=flags)
+        L.load_expert_shards(0, inp.w_i.cuda(), inp.w_o.cuda())
+        ys.append(L.forward(0, inp.x.cuda(), inp.w_r.cuda(), forced_expert=f))
+        rs.append({k: v.cpu().numpy() for k, v in L.routing(N).items()})
+        L.check()
+        torch.cuda.synchronize()
+        L.close()
+    assert torch.equal(ys[0], ys[1])
+    err = _check_layer(inp, ys[0], rs[0], tol=BF16_TOL)
+    y_ref = O.moe_layer(inp.x, inp.w_r, inp.w_i, inp.w_o, forced=ids)
+    assert per_row_rel(ys[0].float().cpu().numpy(), y_ref) <= BF16_TOL
+    print(f"paired chunks vs {flag}: bitwise equal, max-abs-rel {err:.2e}")
+
+
 def test_forced_collectives_path_world1():
     # exercises AllGather / partial buffer / ReduceScatter through NCCL with one rank
     from paper_2503_08467_b200.moeshard import MOESHARD_FLAG_FORCE_COLLECTIVES
