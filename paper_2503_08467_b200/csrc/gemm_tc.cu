@@ -766,8 +766,8 @@ struct FusedParams {
 // unit's time is its weight stream, ~50 GB/s per SM: scripts/micro/wstream.cu). The two
 // chunks are two "virtual tiles" of the accumulator sequence; a single-chunk unit is one.
 // Pays where most experts get ~2 chunks of ~130-160 tokens (C5: 256 tokens per expert on
-// average, -8 %); the launch picks it only when the assignments per expert average >= 256,
-// since the extra decode costs ~2 us where no expert is split (C2, C3).
+// average, -9 %); the launch picks it only when the assignments per expert average >= 256
+// and F >= 4096 (narrower shards and top-2 C2 / C3 measured slower paired).
 #ifndef MOESHARD_PAIR_MAX_CS
 #define MOESHARD_PAIR_MAX_CS 192
 #endif

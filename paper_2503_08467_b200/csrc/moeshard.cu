@@ -770,10 +770,11 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
       }
     } else if (fused) {
       // paired token chunks when the assignments per expert average >= 256 (most experts
-      // then get two chunks of ~130-160 tokens; gemm_tc.cu kPair)
+      // then get two chunks of ~130-160 tokens) and the shard is F >= 4096 wide (C5 at G = 1:
+      // -9 %; at F = 2048-3072, top-2 C2/C3 measured +4 %; gemm_tc.cu kPair)
       const long long n_assign = static_cast<long long>(c->coll ? c->world : 1) * ns * c->K;
 #ifndef MOESHARD_PAIR_MIN_F
-#define MOESHARD_PAIR_MIN_F 2048
+#define MOESHARD_PAIR_MIN_F 4096
 #endif
       const bool pair_chunks = n_assign >= 256LL * Et && F >= MOESHARD_PAIR_MIN_F;
       TcParams up{h, F / kTcFeatTile, static_cast<const __nv_bfloat16*>(lw.wt_in), Et, c->tb,

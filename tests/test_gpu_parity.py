@@ -162,7 +162,7 @@ def test_fused_and_unfused_gemm_agree_bitwise(N, h, d_ff, E):
 @pytest.mark.parametrize("flag", ["UNFUSED_GEMM", "DYNAMIC_SCHED"])
 def test_paired_chunks_bitwise_and_oracle(flag):
     """Paired token chunks (gemm_tc.cu kPair, picked when the assignments per expert average
-    >= 256): experts cut into chunks of <= 192 tokens run two chunks per unit on one weight
+    >= 256 and F >= 4096): experts cut into chunks of <= 192 tokens run two chunks per unit on one weight
     stage. Planted counts give 2 paired chunks (300, 330 tokens), 3 chunks of 192 (520: a
     pair and a single), chunks of 256 that stay unpaired (500, 700, 900), an empty and a
     small expert. The fused kernel must equal the unfused two-launch path (no pairing, same
@@ -171,8 +171,8 @@ def test_paired_chunks_bitwise_and_oracle(flag):
     from paper_2503_08467_b200 import MoEShardLayer
     from paper_2503_08467_b200 import moeshard as C
     counts = [300, 700, 500, 330, 900, 520, 0, 50]
-    N, h, d_ff, E = sum(counts), 512, 1024, len(counts)
-    assert N >= 256 * E
+    N, h, d_ff, E = sum(counts), 256, 4096, len(counts)
+    assert N >= 256 * E and d_ff >= 4096   # the launch's pairing condition (moeshard.cu)
     inp = W.make_layer_inputs(23, N, h, d_ff, E, dtype=torch.bfloat16, routing="uniform")
     ids = np.repeat(np.arange(E), counts)
     ids = ids[np.random.default_rng(5).permutation(N)]
