@@ -558,14 +558,20 @@ def main():
     # after an idle second so the board is back below its power limit: the bench's timed
     # region is short (40 ms) and runs at full clocks, while a pass right after the
     # skew / eager / per-step passes above would time the kernels under sw_power_cap
-    torch.cuda.synchronize()
-    time.sleep(1.0)
-    layer.profile(True)
-    for k in range(min(args.steps, 200)):
-        fwd_eager(k)
-    ph, cnt = layer.phase_ms()
-    layer.profile(False)
-    ph_us = {k: 1e3 * v / max(cnt, 1) for k, v in ph.items()}
+    # Three short passes (each about as long as the timed region), each after an idle
+    # half second, median per phase: one long pass drifted into the power cap (the FFN
+    # phase read 109 or 117 us on two boxes whose graph-replayed steps differed by 1 %).
+    passes = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        time.sleep(0.5)
+        layer.profile(True)
+        for k in range(min(args.steps, 40)):
+            fwd_eager(k)
+        ph, cnt = layer.phase_ms()
+        layer.profile(False)
+        passes.append({k: 1e3 * v / max(cnt, 1) for k, v in ph.items()})
+    ph_us = {k: sorted(p[k] for p in passes)[1] for k in passes[0]}
 
     # --- end to end through the public API with host buffers: every step copies its
     # tokens H2D from pinned memory and its output D2H; the streaming API overlaps the
@@ -631,7 +637,7 @@ def main():
                                               (ph_us[dom] * 1e-6) / 1e9 / hbm, 4),
                 "launch_us": round(ph_us[dom], 3),
                 "timing": "phase CUDA events on the launch stream around the kernel, averaged over "
-                          f"{cnt} eager forwards of a separate profiled pass after 1 s idle (includes "
+                          f"{cnt} eager forwards, median of three separate profiled passes, each after 0.5 s idle (includes "
                           "the ~2-3 us event gap and the kernel's launch without PDL overlap)"}
     # whole-layer roofline: T_TC, T_HBM (weights + x + partial), T_NV
     t_tc = 4 * N * h * F / (tf_burst * 1e12) * 1e6
