@@ -47,11 +47,11 @@ struct TcParams {
 // tmX: x [n][h] box {64, 128}. mn_major: tmW = router_w [h][E] box {64 experts, 64 k}
 // (E % 8 == 0); else router_w is first transposed to wt_r [EP][h] (zero rows E..EP-1)
 // and tmW = wt_r box {64, EP}.
-size_t router_tc_smem_bytes(int EP, bool mn_major);
+size_t router_tc_smem_bytes(int EP, bool mn_major, int stages);
 cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
                              const void* w_r, void* wt_r, int n, int h, int E, int EP,
                              const int32_t* forced, RouteRec* out, int32_t* hist_out,
-                             int32_t* err_flag, cudaStream_t s, int top_k = 1);
+                             int32_t* err_flag, cudaStream_t s, int top_k, int num_sms);
 
 // grid = number of persistent CTAs (normally the SM count).
 //   tmA:  packed weight tiles as a [rows][64] bf16 tensor, box {64, 128}, no swizzle

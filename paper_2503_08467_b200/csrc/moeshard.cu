@@ -702,7 +702,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
         (mn && !make_tmap(&tm_w, router_w, E, h, 64)))
       return fail(c, MOESHARD_ERR_CUDA, "cuTensorMapEncodeTiled failed for hidden/router_w");
     CUDA_TRY(c, launch_router_tc(tm_x, mn ? tm_w : c->tm_wt_r, mn, router_w, c->wt_r, n, h, E,
-                                 c->EP, forced, my_route, my_hist, err_flag, s, c->K));
+                                 c->EP, forced, my_route, my_hist, err_flag, s, c->K, c->num_sms));
     c->launches += mn ? 1 : 2;
   } else {
     launch_router(c->cfg.dtype, hidden, n, h, router_w, E, forced, my_route, my_hist, err_flag, s);

@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(192, 1)
     router_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      int n, int h, int E, int EP, const int32_t* __restrict__ forced,
                      RouteRec* __restrict__ out, int32_t* __restrict__ hist_out,
-                     int32_t* __restrict__ err_flag) {
+                     int32_t* __restrict__ err_flag, int RTC_STAGES) {
   using namespace ptx;
   constexpr int kTok = RTC_TOK;
   extern __shared__ uint8_t smem_raw[];
@@ -254,7 +254,6 @@ __global__ void __launch_bounds__(192, 1)
   __shared__ int32_t s_hist[kMaxExperts];
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
   constexpr int a_stage = kTok * 128;   // kTok rows x 64 k x 2 B
-  const int RTC_STAGES = min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (a_stage + b_bytes));
   uint8_t* sA = smem;
   uint8_t* sB = smem + RTC_STAGES * a_stage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + RTC_STAGES * b_bytes);
@@ -476,11 +475,19 @@ __global__ void __launch_bounds__(192, 1)
 
 TL_EXPORT(moeshard_tl_router)
 
-size_t router_tc_smem_bytes(int EP, bool mn) {
+// Ring stages: as deep as RTC_SMEM_BUDGET allows, except when the grid is more than one
+// wave of one CTA per SM (C5: 256 blocks of 128 tokens on 148 SMs): then half the budget,
+// so two CTAs share an SM and the grid runs as one wave.
+int router_tc_stages(int EP, bool mn, int blocks, int num_sms) {
   const int b = mn ? ((EP + 63) / 64) * 8192 : EP * 128;
   const int a = RTC_TOK * 128;
-  const int st = std::min(RTC_MAX_STAGES, RTC_SMEM_BUDGET / (a + b));
-  return 1024 + st * (a + b) + (2 * st + 1) * 8 + 16;
+  const int budget = blocks > num_sms ? 110 * 1024 : RTC_SMEM_BUDGET;   // 2 x 3 stages fit 228 KB
+  return std::max(2, std::min(RTC_MAX_STAGES, budget / (a + b)));
+}
+size_t router_tc_smem_bytes(int EP, bool mn, int stages) {
+  const int b = mn ? ((EP + 63) / 64) * 8192 : EP * 128;
+  const int a = RTC_TOK * 128;
+  return 1024 + stages * (a + b) + (2 * stages + 1) * 8 + 16;
 }
 
 namespace {
@@ -488,7 +495,7 @@ template <int kK>
 cudaError_t launch_router_tc_k(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
                                const void* w_r, void* wt_r, int n, int h, int E, int EP,
                                const int32_t* forced, RouteRec* out, int32_t* hist_out,
-                               int32_t* err_flag, cudaStream_t s) {
+                               int32_t* err_flag, cudaStream_t s, int num_sms) {
   static PerDeviceOnce attr;
   if (attr.need()) {
     cudaError_t e = cudaFuncSetAttribute(router_tc_kernel<true, kK>,
@@ -501,14 +508,17 @@ cudaError_t launch_router_tc_k(const CUtensorMap& tmX, const CUtensorMap& tmW, b
     attr.done();
   }
   const dim3 grid(ceil_div(n, RTC_TOK));
-  if (mn_major)
-    return launch_pdl(router_tc_kernel<true, kK>, grid, dim3(192), router_tc_smem_bytes(EP, true),
-                      s, tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
+  if (mn_major) {
+    const int st = router_tc_stages(EP, true, grid.x, num_sms);
+    return launch_pdl(router_tc_kernel<true, kK>, grid, dim3(192), router_tc_smem_bytes(EP, true, st),
+                      s, tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, st);
+  }
   dim3 tg(ceil_div(h, 32), ceil_div(EP, 32)), tb(32, 8);
   router_transpose<<<tg, tb, 0, s>>>(static_cast<const __nv_bfloat16*>(w_r), h, E, EP,
                                      static_cast<__nv_bfloat16*>(wt_r));
-  router_tc_kernel<false, kK><<<grid, 192, router_tc_smem_bytes(EP, false), s>>>(
-      tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag);
+  const int st = router_tc_stages(EP, false, grid.x, num_sms);
+  router_tc_kernel<false, kK><<<grid, 192, router_tc_smem_bytes(EP, false, st), s>>>(
+      tmX, tmW, n, h, E, EP, forced, out, hist_out, err_flag, st);
   return cudaGetLastError();
 }
 }  // namespace
@@ -516,13 +526,13 @@ cudaError_t launch_router_tc_k(const CUtensorMap& tmX, const CUtensorMap& tmW, b
 cudaError_t launch_router_tc(const CUtensorMap& tmX, const CUtensorMap& tmW, bool mn_major,
                              const void* w_r, void* wt_r, int n, int h, int E, int EP,
                              const int32_t* forced, RouteRec* out, int32_t* hist_out,
-                             int32_t* err_flag, cudaStream_t s, int top_k) {
+                             int32_t* err_flag, cudaStream_t s, int top_k, int num_sms) {
   if (n <= 0) return cudaSuccess;
   if (top_k == 2)
     return launch_router_tc_k<2>(tmX, tmW, mn_major, w_r, wt_r, n, h, E, EP, forced, out, hist_out,
-                                 err_flag, s);
+                                 err_flag, s, num_sms);
   return launch_router_tc_k<1>(tmX, tmW, mn_major, w_r, wt_r, n, h, E, EP, forced, out, hist_out,
-                               err_flag, s);
+                               err_flag, s, num_sms);
 }
 
 }  // namespace moeshard

@@ -43,6 +43,6 @@ def time_route(E, h, n, reps=200):
 
 res = {}
 for name, E, h in (("c2", 64, 768), ("c3", 128, 768), ("c5", 128, 1024)):
-    for n in (1024, 2048, 4096, 8192, 16384):
+    for n in (1024, 2048, 4096, 8192, 16384, 32768):
         res[f"{name}_n{n}"] = time_route(E, h, n)
 print(json.dumps(res))
