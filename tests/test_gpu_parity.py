@@ -362,6 +362,16 @@ def test_bf16_natural_routing_full_size(E):
     print(f"natural E={E}: max-abs-rel {err:.2e}, per-row {row:.2e}")
 
 
+@pytest.mark.parametrize("E", [64, 128])
+def test_bf16_natural_routing_two_router_ctas_per_sm(E):
+    """More than one wave of 128-token router CTAs (20000 tokens = 157 blocks > 148 SMs):
+    the launch shrinks the router's ring to 3 stages so two CTAs share an SM (router.cu
+    router_tc_stages). Natural routing with the R13 rule, tables, gates and every output row
+    vs the oracle (a narrow d_ff keeps the oracle quick)."""
+    err, row = _full_size_all_tokens(20000, 768, 512, E, 200 + E, "natural")
+    print(f"natural E={E}, 157 router blocks: max-abs-rel {err:.2e}, per-row {row:.2e}")
+
+
 def test_router_cross_chunk_argmax_and_ties():
     """Planted logits: the winning expert sits in the last 32-column chunk, in the first,
     and in a middle one, and exact ties across chunks resolve to the lowest index (R4).
