@@ -1230,7 +1230,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       if (as == 0) aphase ^= 1;
       }   // virtual tiles
     }
-    if (fp.dn.p2p_n > 0) __threadfence_system();   // remote partial rows before the signal kernel
+    if (fp.dn.p2p_n > 0) {   // remote partial rows before the signal kernel: bar.sync orders every
+      // epilogue thread's stores before one system-scope fence per CTA (cumulative)
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      if (warp == 4 && lane == 0) __threadfence_system();
+    }
   }
 
   tc_fence_before();

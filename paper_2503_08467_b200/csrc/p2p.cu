@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(256) push_tokens(P2PArgs a, const uint4* __res
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   const RouteRec* my_route = reinterpret_cast<const RouteRec*>(a.self + a.off_route) + a.rank * nrec;
   const int32_t* my_hist = reinterpret_cast<const int32_t*>(a.self + a.off_hist) + a.rank * nh;
-  // token rows: 4 vectors per thread in flight, each read once and stored to every rank
-  constexpr int kU = 4;
+  // token rows: 8 vectors per thread in flight, each read once and stored to every rank
+  constexpr int kU = 8;
   for (size_t i0 = tid; i0 < nx; i0 += kU * stride) {
     uint4 v[kU];
 #pragma unroll
@@ -117,18 +117,22 @@ __global__ void rs_signal(P2PArgs a) {
 }
 
 // Step 5 aggregate: out[i] = sum_g recv[g][i] (fp32, ascending g), then epoch += 1
-__global__ void __launch_bounds__(256) reduce_partials(P2PArgs a, int n, int row_vecs,
-                                                       uint4* __restrict__ out, int32_t* err) {
+// (every rank's partials for this rank's rows have landed: wait_partials, one CTA, just
+// before - the flags are acquired once instead of by every CTA of the reduce)
+__global__ void wait_partials(P2PArgs a, int32_t* err) {
   const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
   if (threadIdx.x == 0)
     wait_flags(reinterpret_cast<const int32_t*>(a.self) + 32 * (1 + a.world), a.world, epoch + 1,
                err);
-  __syncthreads();
+}
+__global__ void __launch_bounds__(256) reduce_partials(P2PArgs a, int n, int row_vecs,
+                                                       uint4* __restrict__ out, int32_t* err) {
+  const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
   const size_t nv = static_cast<size_t>(n) * row_vecs;
   const size_t slot = static_cast<size_t>(a.n_max) * row_vecs;
   const uint4* recv = reinterpret_cast<const uint4*>(a.self + a.off_recv);
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  constexpr int kU = 2;   // vectors per thread per pass; all G slots' loads of a pass in flight
+  constexpr int kU = 4;   // vectors per thread per pass; all G slots' loads of a pass in flight
   for (size_t i0 = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i0 < nv;
        i0 += kU * stride) {
     float acc[kU][8];
@@ -352,7 +356,7 @@ cudaError_t launch_p2p_push(const P2PArgs& a, const void* x, int n, int ns, int 
                             int E, int num_sms, cudaStream_t s) {
   if (ns <= 0) return cudaSuccess;
   const size_t work = static_cast<size_t>(std::max(n, 1)) * row_vecs;
-  const int grid = static_cast<int>(std::min<size_t>(4 * num_sms, (work + 1023) / 1024));
+  const int grid = static_cast<int>(std::min<size_t>(2 * num_sms, (work + 2047) / 2048));
   return launch_pdl(push_tokens, dim3(std::max(grid, 1)), dim3(256), 0, s, a,
                     static_cast<const uint4*>(x), n, ns, row_vecs, nbr, E);
 }
@@ -386,7 +390,8 @@ cudaError_t launch_p2p_reduce(const P2PArgs& a, int n, int row_vecs, void* out, 
                               int num_sms, cudaStream_t s) {
   // runs even for n = 0 (uneven token counts): it consumes the flags and advances the epoch
   const size_t work = static_cast<size_t>(n) * row_vecs;
-  const int grid = static_cast<int>(std::min<size_t>(4 * num_sms, (work + 511) / 512));
+  const int grid = static_cast<int>(std::min<size_t>(2 * num_sms, (work + 1023) / 1024));
+  wait_partials<<<1, 32, 0, s>>>(a, err);
   reduce_partials<<<std::max(grid, 1), 256, 0, s>>>(a, n, row_vecs, static_cast<uint4*>(out), err);
   return cudaGetLastError();
 }
