@@ -142,7 +142,9 @@ def test_unfused_two_launch_gemm_ablation_matches_oracle():
 @pytest.mark.parametrize("N,h,d_ff,E", [
     (3000, 512, 1024, 64),   # even tile counts: both schedules use CTA pairs
     (1500, 384, 640, 16),    # odd (3 and 5 tiles): fused duplicates the last pair's tile,
-])                           # the unfused path runs 1-CTA M=128 tiles
+                             # the unfused path runs 1-CTA M=128 tiles
+    (16384, 256, 4096, 16),  # 1024 tokens per expert, F = 4096: the fused kernel pairs
+])                           # chunks; H (128 MB) exceeds the L2 set-aside
 def test_fused_and_unfused_gemm_agree_bitwise(N, h, d_ff, E):
     # same arithmetic in both schedules: outputs must be identical bit for bit
     from paper_2503_08467_b200 import MoEShardLayer
