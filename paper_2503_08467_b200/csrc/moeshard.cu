@@ -728,7 +728,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
   } else if (st_route && c->p2p) {
     // Step 3 over peer memory: push this rank's tokens / records / histograms to every rank
     CUDA_TRY(c, launch_p2p_push(c->pa, hidden, n, ns, h * c->elt / 16, nbr, E, c->num_sms, s));
-    c->launches += 1;
+    c->launches += 2;   // push + publish
   } else if (st_route && c->coll) {
     if (!ag_x_side) CUDA_TRY_RET(c, allgather_tokens(c, hidden, n, ns, uneven, ndt, s));
     NCCL_TRY(c, nccl().GroupStart());
@@ -857,7 +857,7 @@ int moeshard_forward_stages(moeshard_ctx* c, int layer, const void* hidden, int 
     c->launches += 1;
   } else if (st_reduce && c->p2p) {
     CUDA_TRY(c, launch_p2p_reduce(c->pa, n, h * c->elt / 16, hidden_out, err_flag, c->num_sms, s));
-    c->launches += 1;
+    c->launches += 2;   // wait_partials + reduce
   } else if (st_reduce && c->coll && !uneven) {
     NCCL_TRY(c, nccl().ReduceScatter(c->partial, hidden_out, static_cast<size_t>(n) * h, ndt,
                                      ncclSum, c->comm, s));

@@ -92,21 +92,20 @@ __global__ void __launch_bounds__(256) push_tokens(P2PArgs a, const uint4* __res
       for (size_t i = tid; i < nh; i += stride) dh[i] = my_hist[i];
     }
   }
-  // bar.sync, then one acq_rel counter increment at system scope per CTA: its release is
-  // cumulative over the CTA's stores (ordered before it by the barrier), and the last CTA's
-  // acquire orders every CTA's stores before its release of the flags. (A fence.sc.sys per
-  // CTA instead cost ~15 us of the one-GPU push.)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t* ctr = reinterpret_cast<int32_t*>(a.self) + 1;
-    int prev;
-    asm volatile("atom.acq_rel.sys.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
-    if (prev == static_cast<int>(gridDim.x) - 1) {   // every CTA's stores released
-      *ctr = 0;
-      for (int g = 0; g < a.world; ++g)
-        st_release_sys(reinterpret_cast<int32_t*>(a.peers[g]) + 32 * (1 + a.rank), epoch + 1);
-    }
-  }
+  (void)epoch;   // the flags are published by push_publish, the next launch
+}
+
+// Step 3 publish (one thread, right after push_tokens in stream order): the push grid has
+// completed, one system-scope fence makes its stores visible to every peer, then flags_ag
+// are released. System-scope operations cost microseconds each on B200 (one-GPU ncu: a
+// one-thread fence + release kernel 5.3 us; a system-scope atomic per push CTA made the push
+// 18-22 us for 12.6 MB), so the push grid itself carries none.
+__global__ void push_publish(P2PArgs a) {
+  const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
+  __threadfence_system();
+  const int g = threadIdx.x;
+  if (g < a.world)
+    st_release_sys(reinterpret_cast<int32_t*>(a.peers[g]) + 32 * (1 + a.rank), epoch + 1);
 }
 
 // Step 5 signal: after the FFN's remote partial-row stores (stream order). The GEMM
@@ -360,8 +359,11 @@ cudaError_t launch_p2p_push(const P2PArgs& a, const void* x, int n, int ns, int 
   if (ns <= 0) return cudaSuccess;
   const size_t work = static_cast<size_t>(std::max(n, 1)) * row_vecs;
   const int grid = static_cast<int>(std::min<size_t>(2 * num_sms, (work + 2047) / 2048));
-  return launch_pdl(push_tokens, dim3(std::max(grid, 1)), dim3(256), 0, s, a,
-                    static_cast<const uint4*>(x), n, ns, row_vecs, nbr, E);
+  cudaError_t e = launch_pdl(push_tokens, dim3(std::max(grid, 1)), dim3(256), 0, s, a,
+                             static_cast<const uint4*>(x), n, ns, row_vecs, nbr, E);
+  if (e != cudaSuccess) return e;
+  push_publish<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_ep_dispatch(const P2PArgs& a, const void* x, int n, int row_vecs,
