@@ -1230,11 +1230,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       if (as == 0) aphase ^= 1;
       }   // virtual tiles
     }
-    if (fp.dn.p2p_n > 0) {   // remote partial rows before the signal kernel: bar.sync orders every
-      // epilogue thread's stores before one system-scope fence per CTA (cumulative)
-      asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
-      if (warp == 4 && lane == 0) __threadfence_system();
-    }
+    // (P2P: the remote partial rows are ordered before the peers' flags by the grid's completion
+    // and the system-scope fence of rs_signal, the next launch; a fence per CTA here delayed
+    // the end of the kernel by microseconds)
   }
 
   tc_fence_before();

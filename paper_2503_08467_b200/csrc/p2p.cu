@@ -108,11 +108,11 @@ __global__ void push_publish(P2PArgs a) {
     st_release_sys(reinterpret_cast<int32_t*>(a.peers[g]) + 32 * (1 + a.rank), epoch + 1);
 }
 
-// Step 5 signal: after the FFN's remote partial-row stores (stream order). The GEMM
-// kernels end with system-scope fences after those stores (one per CTA in the fused FFN),
-// so they are performed before this kernel starts; the release stores below need no fence.
+// Step 5 signal: after the FFN's remote partial-row stores (stream order): the FFN grid has
+// completed, one system-scope fence, then flags_rs are released to every peer.
 __global__ void rs_signal(P2PArgs a) {
   const int32_t epoch = *reinterpret_cast<volatile int32_t*>(a.self);
+  __threadfence_system();
   const int g = threadIdx.x;
   if (g < a.world)
     st_release_sys(reinterpret_cast<int32_t*>(a.peers[g]) + 32 * (1 + a.world + a.rank), epoch + 1);
