@@ -12,7 +12,8 @@ SHAPES = {"c2g1": (64, 768, 3072, 8192, 1), "c2g8": (64, 768, 3072, 8192, 8),
           "c3g4": (128, 768, 3072, 16384, 4), "c5g1": (128, 1024, 4096, 32768, 1),
           "c5g8": (128, 1024, 4096, 32768, 8), "c5g2": (128, 1024, 4096, 32768, 2),
           "c5g4": (128, 1024, 4096, 32768, 4), "c4g8": (256, 768, 3072, 16384, 8),
-          "c3g1": (128, 768, 3072, 16384, 1), "c3g8": (128, 768, 3072, 16384, 8)}
+          "c3g1": (128, 768, 3072, 16384, 1), "c3g8": (128, 768, 3072, 16384, 8),
+          "c2r1k": (64, 768, 3072, 1024, 8)}   # one G = 8 rank's own 1024 tokens (router timeline)
 # "<shape>k2": the same layer with top-2 routing (R21), natural router only
 
 
