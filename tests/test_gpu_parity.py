@@ -593,8 +593,10 @@ def test_schedules_bitwise_equal_and_match_oracle(flag, N, h, d_ff, E, routing):
 
 
 # --------------------------------------------------------------------- peer-memory exchange
-@pytest.mark.parametrize("G,routing", [(1, "zipf"), (2, "zipf"), (4, "uniform"), (8, "patho")])
-def test_p2p_exchange_virtual_ranks_match_oracle(G, routing):
+@pytest.mark.parametrize("G,routing,F,E", [(1, "zipf", 256, 16), (2, "zipf", 256, 16),
+                                           (4, "uniform", 256, 16), (8, "patho", 256, 16),
+                                           (2, "uniform", 4096, 8)])
+def test_p2p_exchange_virtual_ranks_match_oracle(G, routing, F, E):
     """MOESHARD_FLAG_P2P: G ranks share this GPU, each with its own context, weight
     shard and exchange region; the regions are connected directly and the ranks are
     driven in lock-step stages (ROUTE on every rank, then COMPUTE, then REDUCE), so
@@ -602,10 +604,12 @@ def test_p2p_exchange_virtual_ranks_match_oracle(G, routing):
     rank's x_all, partial rows are stored by the down-projection epilogues straight
     into their owner's receive slots, and the owners sum them: the concatenated
     outputs must match the unsharded oracle and the routing tables must be exact on
-    every rank, over several forwards (the epoch advances) with changing inputs."""
+    every rank, over several forwards (the epoch advances) with changing inputs. The last
+    case has F = 4096 per rank and 384 tokens per expert: the fused kernel pairs chunks
+    and its down epilogue stores paired tiles into the peers' slots."""
     from paper_2503_08467_b200 import MoEShardLayer, shard_columns
     from paper_2503_08467_b200 import moeshard as C
-    N, h, d_ff, E = 1024 * G if G > 1 else 1500, 256, 256 * G, 16
+    N, h, d_ff = (1024 * G if G > 1 else 1500) if F < 4096 else 1536 * G, 256, F * G
     n = N // G
     layers = [MoEShardLayer(h, d_ff, E, max_tokens_per_rank=n, dtype=torch.bfloat16, rank=r,
                             world=G, flags=C.MOESHARD_FLAG_P2P) for r in range(G)]
