@@ -850,6 +850,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   // no cluster barrier here: the mbarrier inits reach the peer through the cluster barrier
   // after the tables below, before any remote arrive (A/B: -0.3 us)
   if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+#ifndef MOESHARD_EARLY_ARRIVE
+#define MOESHARD_EARLY_ARRIVE 1
+#endif
+  // the cluster barrier that publishes the mbarrier inits and the TMEM address to both CTAs
+  // is split: arrive here, wait after the tables below (its latency hides behind them)
+  if (MOESHARD_EARLY_ARRIVE) {
+    tc_fence_before();
+    cluster_arrive_release();
+  }
   // PDL: everything above overlapped the grouping kernel's tail. early_tables: the
   // grouping launch's CTA 0 publishes the segment tables (release on tb.stats[6]) before
   // it copies its rows, so only the roles that read X_perm / perm / route wait for the
@@ -899,8 +908,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       if (lane == 0) s_ppref[E] = run;
     }
   }
-  tc_fence_before();
-  cluster_sync_all();
+  if (MOESHARD_EARLY_ARRIVE) {
+    __syncthreads();   // the tables in shared memory (the cluster barrier was arrived at above)
+    cluster_wait_acquire();
+  } else {
+    tc_fence_before();
+    cluster_sync_all();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch_dependents();
