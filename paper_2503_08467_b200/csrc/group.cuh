@@ -57,10 +57,13 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
 // totals through s_warp (>= 5 * kThreads / 32 + 5 ints), two CTA barriers in total (the
 // grouping CTAs sit on this before their row copies; five separate CTA-wide scans cost
 // 1-2.6 us of the pre-FFN critical path).
-template <int kThreads>
+// kNP = 5: all five prefixes (the publishing CTA); kNP = 2: only the compact and padded
+// offsets every other grouping CTA needs for its own rows.
+template <int kThreads, int kNP = 5>
 __device__ __forceinline__ void segment_tables(int E, const int* s_tot, const int* s_pre,
                                                int* s_base, int* s_bpad, int* s_warp, bool publish,
                                                Tables tb, int n_mt_up_tc, int n_mt_down_tc) {
+  static_assert(kNP == 2 || kNP == 5, "prefixes");
   constexpr int kWarps = kThreads / 32;
   const int e = threadIdx.x, lane = e & 31, w = e >> 5;
   int v[5] = {0, 0, 0, 0, 0};   // count, padded count, tc chunks, simt chunks, tc rows
@@ -75,9 +78,9 @@ __device__ __forceinline__ void segment_tables(int E, const int* s_tot, const in
     v[3] = ceil_div(cnt, kSimtTokTile);
     v[4] = nc > 0 ? (cnt / cs) * cs + round_up(cnt % cs, 32) : 0;
   }
-  int inc[5];
+  int inc[5] = {0, 0, 0, 0, 0};
 #pragma unroll
-  for (int i = 0; i < 5; ++i) {
+  for (int i = 0; i < kNP; ++i) {
     inc[i] = v[i];
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -88,12 +91,12 @@ __device__ __forceinline__ void segment_tables(int E, const int* s_tot, const in
   __syncthreads();   // s_warp may still be read by an earlier scan
   if (lane == 31) {
 #pragma unroll
-    for (int i = 0; i < 5; ++i) s_warp[i * kWarps + w] = inc[i];
+    for (int i = 0; i < kNP; ++i) s_warp[i * kWarps + w] = inc[i];
   }
   __syncthreads();
-  int ex[5], tot[5];
+  int ex[5] = {0, 0, 0, 0, 0}, tot[5] = {0, 0, 0, 0, 0};
 #pragma unroll
-  for (int i = 0; i < 5; ++i) {
+  for (int i = 0; i < kNP; ++i) {
     int before = 0, all = 0;
 #pragma unroll
     for (int q = 0; q < kWarps; ++q) {
@@ -108,7 +111,7 @@ __device__ __forceinline__ void segment_tables(int E, const int* s_tot, const in
     s_base[e] = ex[0] + s_pre[e];
     s_bpad[e] = ex[1] + s_pre[e];
   }
-  if (publish) {
+  if (kNP == 5 && publish) {
     for (int i = threadIdx.x; i < tot[2]; i += kThreads) tb.done[i] = 0;   // per token chunk
     if (e < E) {
       tb.pos[e] = ex[1];

@@ -164,8 +164,15 @@ __global__ void __launch_bounds__(1024 / kSplit) group_scatter_gather(
   }
   __syncthreads();
   if (threadIdx.x == 0) { TL_MIN(4); TL_MAX(4); }
-  segment_tables<kThreads>(E, s_tot, s_pre, s_base, s_bpad, s_warp, blockIdx.x == 0, tb,
-                           n_mt_up_tc, n_mt_down_tc);
+#ifndef MOESHARD_TABLES_2P
+#define MOESHARD_TABLES_2P 1
+#endif
+  if (!MOESHARD_TABLES_2P || blockIdx.x == 0)
+    segment_tables<kThreads, 5>(E, s_tot, s_pre, s_base, s_bpad, s_warp, blockIdx.x == 0, tb,
+                                n_mt_up_tc, n_mt_down_tc);
+  else   // only the two offsets this CTA's rows need
+    segment_tables<kThreads, 2>(E, s_tot, s_pre, s_base, s_bpad, s_warp, false, tb,
+                                n_mt_up_tc, n_mt_down_tc);
   if (threadIdx.x == 0) { TL_MIN(5); TL_MAX(5); }
   __syncthreads();   // s_base / s_bpad of every expert
   if (blockIdx.x == 0) {   // the tables are out: the FFN's weight stream may start (early_tables)
